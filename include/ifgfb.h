@@ -1,0 +1,216 @@
+/*
+ * ifgfb.h -- C ABI of the B200-native IFGF N-Muller matvec (libifgfb200.so).
+ *
+ * Drop-in boundary for the hot path of arXiv 2408.02274's reference
+ * (`emscat`, pure Python).  The reference has no FFI; each entry point below
+ * replaces one Python function of its operator API, cited as file:line
+ * (paths under the reference's pkg/src/emscat/):
+ *
+ *   ifgfb_far_apply      <- ifgf.py:885-923        ifgf_apply(tree, hier, weights,
+ *                                                   kappas, mode, displaced_normals,
+ *                                                   displaced_step)
+ *   ifgfb_potentials     <- operators.py:321-350   MullerOperator.potentials(dens)
+ *   ifgfb_muller_apply   <- operators.py:399-403   MullerOperator.apply(y)
+ *   ifgfb_muller_apply_host  same, host buffers in/out (copies inside)
+ *   ifgfb_zdotc/ifgfb_zaxpy/ifgfb_dznrm2/ifgfb_zscal
+ *                        <- solver.py:61-66         GMRES vector ops (np.vdot, axpy,
+ *                                                   np.linalg.norm, w/h)
+ *
+ * Plan construction (reference ifgf.py:176-482, ifgf.py:676-749,
+ * quadrature.py:97-525, all plan-time) is done on the host by the Python
+ * package; its arrays are handed over ONCE through the ifgfb_plan_* calls
+ * (host pointers, copied to device memory owned by the plan).
+ *
+ * Conventions
+ *  - complex128 values are interleaved (re, im) doubles ("double2").
+ *  - "tree order" = the octree's Morton order (reference BoxTree.perm);
+ *    "original order" = surface point order ell = j + n_c*i + p*n_c^2.
+ *  - every function returns IFGFB_OK (0) or a negative error code; the
+ *    message is available from ifgfb_last_error() (thread-local).
+ *  - device pointers are raw CUDA global-memory pointers (e.g. a torch
+ *    tensor's data_ptr()); `stream` is a cudaStream_t (NULL = legacy default).
+ *  - a plan is bound to the device current at ifgfb_plan_create; it is not
+ *    re-entrant (one apply at a time per plan), plans are independent.
+ *  - there is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point fails with IFGFB_ERR_CUDA.
+ */
+#ifndef IFGFB_H
+#define IFGFB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IFGFB_ABI_VERSION 1
+
+enum {
+  IFGFB_OK = 0,
+  IFGFB_ERR_ARG = -1,      /* bad argument / shape (Python: ValueError)     */
+  IFGFB_ERR_CUDA = -2,     /* CUDA failure (Python: RuntimeError)           */
+  IFGFB_ERR_STATE = -3,    /* plan incomplete or used out of order          */
+  IFGFB_ERR_UNSUPPORTED = -4
+};
+
+typedef struct ifgfb_plan ifgfb_plan;
+
+/* ---- global geometry of the IFGF tree (reference BoxTree, ifgf.py:139-173) */
+typedef struct {
+  int32_t n_points;          /* N */
+  int32_t depth;             /* D; levels 3..D carry cone segments */
+  int32_t p_s, p_a;          /* interpolation orders (only 3, 5 compiled) */
+  const double* points_tree; /* N*3, tree order (BoxTree.points) */
+  const int64_t* perm;       /* N: tree slot -> original index (BoxTree.perm) */
+} ifgfb_tree_desc;
+
+/* ---- one cone level d (reference LevelBoxes + ConeLevel, ifgf.py:109-126,
+ *      ifgf.py:324-387).  Node tables are the per-cell Chebyshev nodes and
+ *      their sin/cos (host-evaluated, so node positions match the reference). */
+typedef struct {
+  int32_t level;
+  int32_t n_boxes;
+  int32_t n_s, n_a;
+  double side, h, delta_s, delta_a;
+  const double* centers;     /* n_boxes*3 */
+  const int64_t* pt_start;   /* n_boxes, tree-order point ranges */
+  const int64_t* pt_count;   /* n_boxes */
+  int64_t n_segments;
+  const int64_t* seg_off;    /* n_boxes+1 (ConeLevel.seg_off) */
+  const int64_t* seg_ids;    /* n_segments (ConeLevel.seg_ids) */
+  const double* s_nodes;     /* n_s*p_s    (ConeLevel.s_nodes) */
+  const double* sin_t;       /* n_a*p_a    sin(ang_nodes_t) */
+  const double* cos_t;       /* n_a*p_a    cos(ang_nodes_t) */
+  const double* sin_p;       /* 2n_a*p_a   sin(ang_nodes_p) */
+  const double* cos_p;       /* 2n_a*p_a   cos(ang_nodes_p) */
+} ifgfb_level_desc;
+
+/* ---- emission pairs of level d (reference _emit_level, ifgf.py:630-673):
+ *      one entry per (box, cousin point), box-major as ConeLevel.cpt_idx. */
+typedef struct {
+  int32_t level;
+  int64_t n_pairs;
+  const int64_t* row;        /* segment row of the pair */
+  const int64_t* target;     /* target point, tree order */
+  const double* geom;        /* n_pairs*4: xs, xt, xp, r   of x_t */
+  const double* geom_disp;   /* n_pairs*4 of x_t + h n_t, or NULL */
+} ifgfb_emit_desc;
+
+/* ---- propagation child level d -> parent level d-1 (reference _AccumType /
+ *      _accum_types / _accumulate_level, ifgf.py:676-785), regrouped per
+ *      parent segment row (owner computes). */
+typedef struct {
+  int32_t level;             /* child level d */
+  int64_t n_types;
+  const int64_t* sig_off;    /* n_types+1 into the group arrays */
+  const int64_t* group_start;/* per group: first sorted node slot (0..74) */
+  const int64_t* group_end;  /* per group: one past last slot */
+  const int64_t* scatter;    /* n_types*nn: parent node slot of sorted node */
+  const double* xs;          /* n_types*nn local coords in the child segment */
+  const double* xt;
+  const double* xp;
+  const double* r_parent;    /* n_types*nn */
+  const double* r_child;     /* n_types*nn */
+  int64_t n_parent_rows;     /* segments of level d-1 */
+  const int64_t* inst_off;   /* n_parent_rows+1 */
+  int64_t n_instances;
+  const int64_t* inst_type;  /* n_instances */
+  const int64_t* inst_crow_off; /* n_instances+1 into crow */
+  const int64_t* crow;       /* child segment row per sigma group */
+} ifgfb_accum_desc;
+
+/* ---- surface + operator data (reference SurfaceDiscretization,
+ *      geometry.py:128-184; MaterialPair operators.py:58-101) */
+typedef struct {
+  int32_t n_patches, n_c;
+  const double* points;      /* N*3 original order */
+  const double* normals;     /* N*3 */
+  const double* weights;     /* N   (Fejer x Jacobian) */
+  const double* jacobians;   /* N */
+  const double* e_u;         /* N*3 */
+  const double* e_v;         /* N*3 */
+  const double* tangent1;    /* N*3 */
+  const double* tangent2;    /* N*3 */
+  const double* diff_matrix; /* n_c*n_c (chebyshev.diff_matrix) */
+  const double* coeff_matrix;/* n_c*n_c (chebyshev.transform_matrix) */
+  const double* eps_e; const double* mu_e;  /* complex (2 doubles each) */
+  const double* eps_i; const double* mu_i;
+  double omega;
+  const double* kappas;      /* 2 complex: kappa_e, kappa_i */
+  double fd_step;            /* OperatorConfig.fd_step */
+} ifgfb_surface_desc;
+
+/* ---- near field (reference quadrature.py:251-525, operators.py:255-319):
+ *      per target (original order) its singular-moment pairs and one signed
+ *      direct-interaction list (+ neighbour-box sources off the singular
+ *      patches, - correction sources). */
+typedef struct {
+  int64_t n_mom;
+  const int64_t* mom_off;    /* N+1 */
+  const int64_t* mom_patch;  /* n_mom */
+  const double* moments;     /* n_mom*4*n_c*n_c complex: beta_s[k=0,1], beta_d[k=0,1] */
+  int64_t n_direct;
+  const int64_t* dir_off;    /* N+1 */
+  const int64_t* dir_src;    /* n_direct: source index (original order), or
+                                -(src+1) for a subtracted correction entry */
+} ifgfb_near_desc;
+
+int ifgfb_abi_version(void);
+const char* ifgfb_last_error(void);
+int ifgfb_device_info(char* buf, size_t len);
+
+int ifgfb_plan_create(const ifgfb_tree_desc* tree, ifgfb_plan** out);
+int ifgfb_plan_add_level(ifgfb_plan* plan, const ifgfb_level_desc* lvl);
+int ifgfb_plan_add_accum(ifgfb_plan* plan, const ifgfb_accum_desc* acc);
+int ifgfb_plan_set_emission(ifgfb_plan* plan, const ifgfb_emit_desc* em);
+int ifgfb_plan_set_surface(ifgfb_plan* plan, const ifgfb_surface_desc* s);
+int ifgfb_plan_set_near(ifgfb_plan* plan, const ifgfb_near_desc* nf);
+int ifgfb_plan_finalize(ifgfb_plan* plan);
+int ifgfb_plan_destroy(ifgfb_plan* plan);
+/* bytes of device memory held by the plan (static + workspace) */
+int64_t ifgfb_plan_device_bytes(const ifgfb_plan* plan);
+
+/* Far-field sums for every surface point over the sources outside its
+ * finest-level neighbour boxes (reference ifgf_apply, ifgf.py:885-923).
+ *   w        device, nch*N complex, ORIGINAL order, row c = channel c
+ *   kappas   host, nk complex (nk = 1 or 2)
+ *   out      device, nch*nk*N complex, layout (nch, nk, N) original order
+ *   out_disp device, same layout (evaluation at x + h n), or NULL
+ * nch*nk <= 16.  Result identical for mode "vec"/"seq" (the device always
+ * carries every channel-kernel column through one traversal). */
+int ifgfb_far_apply(ifgfb_plan* plan, const double* w, int nch,
+                    const double* kappas, int nk, double* out,
+                    double* out_disp, void* stream);
+
+/* S (8,2,N) and D (6,2,N) potentials of packed densities phi (8,N)
+ * (reference MullerOperator.potentials, operators.py:321-350). */
+int ifgfb_potentials(ifgfb_plan* plan, const double* phi, double* s_val,
+                     double* d_val, void* stream);
+
+/* y (4N complex, device) -> A y (4N complex, device)
+ * (reference MullerOperator.apply, operators.py:399-403). */
+int ifgfb_muller_apply(ifgfb_plan* plan, const double* y, double* out,
+                       void* stream);
+/* same with host buffers; copies (pinned staging) are inside the call and
+ * the call returns after the result is in `out_host`. */
+int ifgfb_muller_apply_host(ifgfb_plan* plan, const double* y_host,
+                            double* out_host, void* stream);
+
+/* GMRES vector primitives on device vectors of n complex entries
+ * (reference solver.py:61-66, :91-92).  Scalars are host complex. */
+int ifgfb_zdotc(const double* x, const double* y, int64_t n, double* result,
+                void* stream);              /* sum conj(x) y  (np.vdot)   */
+int ifgfb_dznrm2(const double* x, int64_t n, double* result, void* stream);
+int ifgfb_zaxpy(const double* alpha, const double* x, double* y, int64_t n,
+                void* stream);              /* y += alpha x               */
+int ifgfb_zscal_div(double* y, const double* x, double denom, int64_t n,
+                    void* stream);          /* y = x / denom (real)       */
+
+/* Number of kernels launched by the last apply on this plan. */
+int64_t ifgfb_plan_last_launches(const ifgfb_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IFGFB_H */

@@ -1,0 +1,149 @@
+"""ctypes binding of libifgfb200.so (the C ABI in include/ifgfb.h).
+
+The library is built in-tree by ``paper_2408_02274_b200.build.build()``.
+Importing this module never falls back to CPU code: if the shared object is
+missing or no CUDA device is usable, the compute entry points raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libifgfb200.so"
+
+IFGFB_OK = 0
+IFGFB_ERR_ARG = -1
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int64)
+
+
+class TreeDesc(C.Structure):
+    _fields_ = [("n_points", C.c_int32), ("depth", C.c_int32),
+                ("p_s", C.c_int32), ("p_a", C.c_int32),
+                ("points_tree", _dp), ("perm", _ip)]
+
+
+class LevelDesc(C.Structure):
+    _fields_ = [("level", C.c_int32), ("n_boxes", C.c_int32),
+                ("n_s", C.c_int32), ("n_a", C.c_int32),
+                ("side", C.c_double), ("h", C.c_double),
+                ("delta_s", C.c_double), ("delta_a", C.c_double),
+                ("centers", _dp), ("pt_start", _ip), ("pt_count", _ip),
+                ("n_segments", C.c_int64), ("seg_off", _ip), ("seg_ids", _ip),
+                ("s_nodes", _dp), ("sin_t", _dp), ("cos_t", _dp),
+                ("sin_p", _dp), ("cos_p", _dp)]
+
+
+class EmitDesc(C.Structure):
+    _fields_ = [("level", C.c_int32), ("n_pairs", C.c_int64),
+                ("row", _ip), ("target", _ip), ("geom", _dp),
+                ("geom_disp", _dp)]
+
+
+class AccumDesc(C.Structure):
+    _fields_ = [("level", C.c_int32), ("n_types", C.c_int64),
+                ("sig_off", _ip), ("group_start", _ip), ("group_end", _ip),
+                ("scatter", _ip), ("xs", _dp), ("xt", _dp), ("xp", _dp),
+                ("r_parent", _dp), ("r_child", _dp),
+                ("n_parent_rows", C.c_int64), ("inst_off", _ip),
+                ("n_instances", C.c_int64), ("inst_type", _ip),
+                ("inst_crow_off", _ip), ("crow", _ip)]
+
+
+class SurfaceDesc(C.Structure):
+    _fields_ = [("n_patches", C.c_int32), ("n_c", C.c_int32),
+                ("points", _dp), ("normals", _dp), ("weights", _dp),
+                ("jacobians", _dp), ("e_u", _dp), ("e_v", _dp),
+                ("tangent1", _dp), ("tangent2", _dp),
+                ("diff_matrix", _dp), ("coeff_matrix", _dp),
+                ("eps_e", _dp), ("mu_e", _dp), ("eps_i", _dp), ("mu_i", _dp),
+                ("omega", C.c_double), ("kappas", _dp),
+                ("fd_step", C.c_double)]
+
+
+class NearDesc(C.Structure):
+    _fields_ = [("n_mom", C.c_int64), ("mom_off", _ip), ("mom_patch", _ip),
+                ("moments", _dp), ("n_direct", C.c_int64), ("dir_off", _ip),
+                ("dir_src", _ip)]
+
+
+EXPORTS = {
+    "ifgfb_abi_version": ([], C.c_int),
+    "ifgfb_last_error": ([], C.c_char_p),
+    "ifgfb_device_info": ([C.c_char_p, C.c_size_t], C.c_int),
+    "ifgfb_plan_create": ([C.POINTER(TreeDesc), C.POINTER(C.c_void_p)], C.c_int),
+    "ifgfb_plan_add_level": ([C.c_void_p, C.POINTER(LevelDesc)], C.c_int),
+    "ifgfb_plan_add_accum": ([C.c_void_p, C.POINTER(AccumDesc)], C.c_int),
+    "ifgfb_plan_set_emission": ([C.c_void_p, C.POINTER(EmitDesc)], C.c_int),
+    "ifgfb_plan_set_surface": ([C.c_void_p, C.POINTER(SurfaceDesc)], C.c_int),
+    "ifgfb_plan_set_near": ([C.c_void_p, C.POINTER(NearDesc)], C.c_int),
+    "ifgfb_plan_finalize": ([C.c_void_p], C.c_int),
+    "ifgfb_plan_destroy": ([C.c_void_p], C.c_int),
+    "ifgfb_plan_device_bytes": ([C.c_void_p], C.c_int64),
+    "ifgfb_plan_last_launches": ([C.c_void_p], C.c_int64),
+    "ifgfb_far_apply": ([C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int,
+                         C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "ifgfb_potentials": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                          C.c_void_p], C.c_int),
+    "ifgfb_muller_apply": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
+                           C.c_int),
+    "ifgfb_muller_apply_host": ([C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p], C.c_int),
+    "ifgfb_zdotc": ([C.c_void_p, C.c_void_p, C.c_int64, _dp, C.c_void_p],
+                    C.c_int),
+    "ifgfb_dznrm2": ([C.c_void_p, C.c_int64, _dp, C.c_void_p], C.c_int),
+    "ifgfb_zaxpy": ([_dp, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
+                    C.c_int),
+    "ifgfb_zscal_div": ([C.c_void_p, C.c_void_p, C.c_double, C.c_int64,
+                         C.c_void_p], C.c_int),
+}
+
+_lib = None
+
+
+def load():
+    """Load the shared library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(
+            f"{LIB_PATH} missing: run paper_2408_02274_b200.build.build() "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (args, res) in EXPORTS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if lib.ifgfb_abi_version() != 1:
+        raise RuntimeError("libifgfb200 ABI version mismatch")
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == IFGFB_OK:
+        return
+    msg = load().ifgfb_last_error().decode(errors="replace")
+    if rc == IFGFB_ERR_ARG:
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: {msg} (code {rc})")
+
+
+def dptr(a: np.ndarray):
+    """double* of a C-contiguous float64/complex128 host array (or NULL)."""
+    if a is None:
+        return None
+    assert a.flags.c_contiguous and a.dtype in (np.float64, np.complex128)
+    return a.ctypes.data_as(_dp)
+
+
+def iptr(a: np.ndarray):
+    if a is None:
+        return None
+    assert a.flags.c_contiguous and a.dtype == np.int64
+    return a.ctypes.data_as(_ip)

@@ -1,0 +1,166 @@
+// Shared device helpers and the plan object of libifgfb200.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/ifgfb.h"
+
+namespace ifgfb {
+
+constexpr int PS = 3;          // radial interpolation order
+constexpr int PA = 5;          // angular interpolation order
+constexpr int NN = PS * PA * PA;  // 75 nodes per cone segment
+constexpr int NCOL = 16;       // complex columns carried per traversal
+constexpr int NRCOL = 2 * NCOL;   // 32 real columns
+constexpr int SEG_DOUBLES = NN * NRCOL;  // 2400 doubles = 19.2 KB per segment
+
+void set_error(const std::string& msg);
+
+#define IFGFB_CUDA(call)                                                  \
+  do {                                                                    \
+    cudaError_t e_ = (call);                                              \
+    if (e_ != cudaSuccess) {                                              \
+      ::ifgfb::set_error(std::string(#call) + ": " + cudaGetErrorString(e_)); \
+      return IFGFB_ERR_CUDA;                                              \
+    }                                                                     \
+  } while (0)
+
+// ---- exact (non-contracted) arithmetic, used wherever the reference's
+//      numpy expression order must be reproduced bit for bit
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// exp(i * kappa * x) for complex kappa = (kr, ki): exp(-ki x) (cos(kr x), sin(kr x))
+// following numpy's evaluation of np.exp(1j * kappa * x).
+__device__ __forceinline__ double2 cexp_ikx(double kr, double ki, double x) {
+  double s, c;
+  sincos(mul_rn(kr, x), &s, &c);
+  if (ki != 0.0) {
+    double m = exp(-mul_rn(ki, x));
+    return make_double2(c * m, s * m);
+  }
+  return make_double2(c, s);
+}
+
+// Chebyshev T_0..T_{n-1} by the reference's recurrence (chebyshev.py:82-95):
+// T_i = (2.0 * x) * T_{i-1} - T_{i-2}, each op rounded (no FMA contraction).
+template <int N>
+__device__ __forceinline__ void cheb_exact(double x, double (&t)[N]) {
+  t[0] = 1.0;
+  if (N > 1) t[1] = x;
+  const double x2 = mul_rn(2.0, x);
+#pragma unroll
+  for (int i = 2; i < N; ++i) t[i] = sub_rn(mul_rn(x2, t[i - 1]), t[i - 2]);
+}
+
+// 8x8x4 FP64 tensor-core MMA (the only FP64 tensor path on sm_100a; tcgen05
+// has no f64 kind).  a: A[row=lane>>2][k=lane&3], b: B[k=lane&3][col=lane>>2],
+// c0/c1: C[row=lane>>2][col=2*(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+template <typename T>
+struct DevArray {
+  T* ptr = nullptr;
+  size_t n = 0;
+};
+
+// ------------------------------------------------------------------ plan --
+struct Level {
+  int d = 0, n_boxes = 0, n_s = 0, n_a = 0;
+  double side = 0, h = 0, delta_s = 0, delta_a = 0;
+  int n_seg = 0;
+  double* centers = nullptr;   // n_boxes*3
+  int* pt_start = nullptr;     // n_boxes
+  int* pt_count = nullptr;
+  int* seg_box = nullptr;      // n_seg
+  int* seg_id = nullptr;       // n_seg
+  double* tabs = nullptr;      // s_nodes | sin_t | cos_t | sin_p | cos_p
+  // emission (pairs pre-sorted by segment row)
+  int64_t n_pairs = 0;
+  bool has_disp = false;
+  int* pair_id = nullptr;      // sorted pos -> pair index (box-major)
+  double4* geom = nullptr;     // sorted pos
+  double4* geom_disp = nullptr;
+  int n_etiles = 0;
+  int4* etiles = nullptr;      // (row, first sorted pos, count<=4, 0)
+  int* tgt_off = nullptr;      // N+1 (tree order targets)
+  int* tgt_pairs = nullptr;    // pair indices, per target in box order
+  // accumulation from this level (as child) into level d-1
+  bool has_accum = false;
+  int64_t n_types = 0;
+  int* sig_off = nullptr;      // n_types+1
+  int2* groups = nullptr;      // (start, end)
+  unsigned char* scatter = nullptr;  // n_types*NN
+  double* tgeom = nullptr;     // n_types*NN*5 : xs, xt, xp, rp, rc
+  int* inst_off = nullptr;     // parent rows + 1
+  int* inst_type = nullptr;
+  int* inst_crow_off = nullptr;
+  int* crow = nullptr;
+  int64_t n_instances = 0;
+};
+
+struct Plan {
+  int device = 0;
+  int n = 0, depth = 0;
+  double* points_tree = nullptr;   // N*3
+  int* perm = nullptr;             // tree slot -> original
+  std::vector<Level> levels;       // index d (0..depth); only d>=3 used
+  bool finalized = false;
+  // work buffers
+  double* wt = nullptr;            // N * 8 complex (tree order, channels)
+  double* coef[2] = {nullptr, nullptr};
+  size_t coef_cap = 0;             // segments
+  double* partial = nullptr;       // max pairs * 2 * NCOL complex
+  double* out_tree = nullptr;      // N * NCOL complex
+  double* out_disp_tree = nullptr;
+  int64_t max_pairs = 0;
+  int max_seg = 0;
+  // surface / operator
+  bool has_surface = false;
+  int n_patches = 0, n_c = 0;
+  double* sdata = nullptr;         // packed surface arrays
+  double* pts = nullptr; double* nrm = nullptr; double* wq = nullptr;
+  double* jac = nullptr; double* eu = nullptr; double* ev = nullptr;
+  double* t1 = nullptr; double* t2 = nullptr; double* dmat = nullptr;
+  double* cmat = nullptr;
+  double eps_e[2], mu_e[2], eps_i[2], mu_i[2], omega = 0, kappa[4], fd_step = 1e-6;
+  // near field
+  bool has_near = false;
+  int64_t n_mom = 0, n_direct = 0;
+  int* mom_off = nullptr; int* mom_patch = nullptr; double* moments = nullptr;
+  int* dir_off = nullptr; int* dir_src = nullptr;
+  // muller workspaces
+  double* phi = nullptr;        // 8*N complex
+  double* phiw = nullptr;       // 8*N complex (phi * weights)
+  double* pcoef = nullptr;      // 8*P*n_c^2 complex
+  double* far_out = nullptr;    // 16*N complex (8 ch x 2 k, original order)
+  double* far_disp = nullptr;
+  double* s_val = nullptr;      // 8*2*N complex
+  double* d_val = nullptr;      // 6*2*N complex
+  double* host_stage = nullptr; // pinned 2 * 4N complex
+  double* dev_y = nullptr;      // 4N complex
+  double* dev_out = nullptr;    // 4N complex
+  int64_t launches = 0;
+  size_t bytes = 0;
+  std::vector<void*> allocations;
+};
+
+int far_apply(Plan& p, const double* w, int nch, const double* kappas, int nk,
+              double* out, double* out_disp, cudaStream_t st);
+int potentials(Plan& p, const double* phi, double* s_val, double* d_val,
+               cudaStream_t st);
+int muller_apply(Plan& p, const double* y, double* out, cudaStream_t st);
+
+}  // namespace ifgfb

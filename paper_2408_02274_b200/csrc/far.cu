@@ -1,0 +1,532 @@
+// Far-field IFGF traversal on sm_100a: leaf direct spectra (K2), value ->
+// Chebyshev coefficient transform (K3, fused), child -> parent
+// re-interpolation on FP64 tensor cores (K4), cousin emission on FP64 tensor
+// cores (K5) and the deterministic per-target reduction.
+//
+// Reference: ifgf.py:788-882 (propagate_and_emit), ifgf.py:535-554 (K2),
+// ifgf.py:502-522 (K3), ifgf.py:752-785 (K4), ifgf.py:630-673 (K5).
+//
+// Data layout in HBM: per level one coefficient array [n_seg][75][16]
+// complex (node-major, column m = channel*nk + kernel, the reference's
+// c*nk + k flattening), 19.2 KB per segment; two such arrays are live
+// (child level / parent level ping-pong).
+#include "common.cuh"
+
+namespace ifgfb {
+
+__constant__ double c_ms[PS * PS];   // chebyshev transform_matrix(3)
+__constant__ double c_ma[PA * PA];   // chebyshev transform_matrix(5)
+
+static bool g_const_ready = false;
+
+static void host_transform_matrix(int n, double* out) {
+  // (2/n) T_i(x_j), row 0 halved (reference chebyshev.py:98-105)
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double x = cos((j + 0.5) * M_PI / n);
+      double t0 = 1.0, t1 = x, ti = (i == 0) ? 1.0 : x;
+      for (int q = 2; q <= i; ++q) {
+        ti = 2.0 * x * t1 - t0;
+        t0 = t1;
+        t1 = ti;
+      }
+      out[i * n + j] = (2.0 / n) * ti * (i == 0 ? 0.5 : 1.0);
+    }
+}
+
+int init_constants() {
+  if (g_const_ready) return IFGFB_OK;
+  double ms[PS * PS], ma[PA * PA];
+  host_transform_matrix(PS, ms);
+  host_transform_matrix(PA, ma);
+  IFGFB_CUDA(cudaMemcpyToSymbol(c_ms, ms, sizeof(ms)));
+  IFGFB_CUDA(cudaMemcpyToSymbol(c_ma, ma, sizeof(ma)));
+  g_const_ready = true;
+  return IFGFB_OK;
+}
+
+// ---------------------------------------------------------------- K3 ----
+// In-place node values -> coefficients for one segment held in shared memory
+// V[node][NCOL] (node = (a*PA + b)*PA + c): three axis transforms.
+__device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
+  for (int task = tid; task < PA * PA * NCOL; task += nthr) {
+    const int bc = task / NCOL, m = task % NCOL;
+    double2 v[PS];
+#pragma unroll
+    for (int a = 0; a < PS; ++a) v[a] = V[(a * PA * PA + bc) * NCOL + m];
+#pragma unroll
+    for (int a = 0; a < PS; ++a) {
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < PS; ++q) {
+        s.x += c_ms[a * PS + q] * v[q].x;
+        s.y += c_ms[a * PS + q] * v[q].y;
+      }
+      V[(a * PA * PA + bc) * NCOL + m] = s;
+    }
+  }
+  __syncthreads();
+  for (int task = tid; task < PS * PA * NCOL; task += nthr) {
+    const int ac = task / NCOL, m = task % NCOL;
+    const int a = ac / PA, c = ac % PA;
+    double2 v[PA];
+#pragma unroll
+    for (int b = 0; b < PA; ++b) v[b] = V[((a * PA + b) * PA + c) * NCOL + m];
+#pragma unroll
+    for (int b = 0; b < PA; ++b) {
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < PA; ++q) {
+        s.x += c_ma[b * PA + q] * v[q].x;
+        s.y += c_ma[b * PA + q] * v[q].y;
+      }
+      V[((a * PA + b) * PA + c) * NCOL + m] = s;
+    }
+  }
+  __syncthreads();
+  for (int task = tid; task < PS * PA * NCOL; task += nthr) {
+    const int ab = task / NCOL, m = task % NCOL;
+    double2 v[PA];
+#pragma unroll
+    for (int c = 0; c < PA; ++c) v[c] = V[(ab * PA + c) * NCOL + m];
+#pragma unroll
+    for (int c = 0; c < PA; ++c) {
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < PA; ++q) {
+        s.x += c_ma[c * PA + q] * v[q].x;
+        s.y += c_ma[c * PA + q] * v[q].y;
+      }
+      V[(ab * PA + c) * NCOL + m] = s;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void store_segment(double* dst, const double2* V,
+                                              int tid, int nthr) {
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  for (int i = tid; i < NN * NCOL; i += nthr) d2[i] = V[i];
+}
+
+// ------------------------------------------------------------ weights ----
+// wt[t][c] = w[c][perm[t]] (tree order, CH channel slots, zero padded)
+__global__ void pack_weights(const double2* __restrict__ w, int nch, int n,
+                             const int* __restrict__ perm, int ch,
+                             double2* __restrict__ wt) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * ch) return;
+  const int t = idx / ch, c = idx % ch;
+  wt[idx] = (c < nch) ? w[(size_t)c * n + perm[t]] : make_double2(0.0, 0.0);
+}
+
+// ---------------------------------------------------------------- K2 ----
+struct LeafArgs {
+  const int* seg_box; const int* seg_id; const double* centers;
+  const int* pt_start; const int* pt_count; const double* tabs;
+  int n_s, n_a; double h;
+  const double* points;  // tree order
+  const double2* wt;     // [N][CH]
+  double kr[2], ki[2];
+  double* coef;
+};
+
+// One CTA per finest-level segment: node values
+//   F[node][c*NK+k] = sum_{src in box} (r/d) exp(i kappa_k (d - r)) w[c][src]
+// (reference _direct_spectra_box, ifgf.py:535-554), then the K3 transform.
+template <int NK>
+__global__ void __launch_bounds__(128) leaf_kernel(LeafArgs a) {
+  constexpr int CH = NCOL / NK;
+  __shared__ double2 V[NN * NCOL];
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const int box = a.seg_box[row], id = a.seg_id[row];
+  if (tid < NN) {
+    const int two_na = 2 * a.n_a;
+    const int i_p = id % two_na, rest = id / two_na;
+    const int i_t = rest % a.n_a, i_s = rest / a.n_a;
+    const int na = tid / (PA * PA), nb = (tid / PA) % PA, nc = tid % PA;
+    const double* s_nodes = a.tabs;
+    const double* sin_t = s_nodes + a.n_s * PS;
+    const double* cos_t = sin_t + a.n_a * PA;
+    const double* sin_p = cos_t + a.n_a * PA;
+    const double* cos_p = sin_p + two_na * PA;
+    const double r = a.h / s_nodes[i_s * PS + na];
+    const double st = sin_t[i_t * PA + nb], ct = cos_t[i_t * PA + nb];
+    const double sp = sin_p[i_p * PA + nc], cp = cos_p[i_p * PA + nc];
+    const double x = add_rn(a.centers[3 * box + 0], mul_rn(r, mul_rn(st, cp)));
+    const double y = add_rn(a.centers[3 * box + 1], mul_rn(r, mul_rn(st, sp)));
+    const double z = add_rn(a.centers[3 * box + 2], mul_rn(r, ct));
+    double2 acc[NCOL];
+#pragma unroll
+    for (int m = 0; m < NCOL; ++m) acc[m] = make_double2(0.0, 0.0);
+    const int s0 = a.pt_start[box], s1 = s0 + a.pt_count[box];
+    for (int s = s0; s < s1; ++s) {
+      const double dx = x - a.points[3 * s], dy = y - a.points[3 * s + 1],
+                   dz = z - a.points[3 * s + 2];
+      const double d = sqrt(dx * dx + dy * dy + dz * dz);
+      const double q = r / d;
+      double2 g[NK];
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        const double2 e = cexp_ikx(a.kr[k], a.ki[k], d - r);
+        g[k] = make_double2(q * e.x, q * e.y);
+      }
+      const double2* wv = a.wt + (size_t)s * CH;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const double2 wc = wv[c];
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+          const double2 p = cmul(g[k], wc);
+          acc[c * NK + k].x += p.x;
+          acc[c * NK + k].y += p.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < NCOL; ++m) V[tid * NCOL + m] = acc[m];
+  }
+  __syncthreads();
+  to_coeffs_smem(V, tid, blockDim.x);
+  store_segment(a.coef + (size_t)row * SEG_DOUBLES, V, tid, blockDim.x);
+}
+
+// ------------------------------------------------------- DMMA helpers ----
+// Tensor-product Chebyshev basis of one interpolation point, consumed as the
+// A operand of m8n8k4 f64 MMAs.  The K dimension (75 coefficients) is padded
+// to 80 = 16 (a,b) pairs x 5 c values; k-step ks = 5q + c covers the
+// coefficients i = (4q + tig)*5 + c, tig = lane & 3.  A thread then needs
+// only tst[q] = T_a(xs) T_b(xt) for ab = 4q + tig and T_c(xp).
+struct BasisA {
+  double tst[4];
+  double tp[PA];
+};
+
+template <bool EXACT>
+__device__ __forceinline__ BasisA make_basis(double xs, double xt, double xp,
+                                             int tig) {
+  double ts[PS], tt[PA];
+  BasisA B;
+  if (EXACT) {
+    cheb_exact<PS>(xs, ts);
+    cheb_exact<PA>(xt, tt);
+    cheb_exact<PA>(xp, B.tp);
+  } else {
+    ts[0] = 1.0; ts[1] = xs; ts[2] = 2.0 * xs * xs - 1.0;
+    tt[0] = 1.0; tt[1] = xt;
+    B.tp[0] = 1.0; B.tp[1] = xp;
+#pragma unroll
+    for (int i = 2; i < PA; ++i) {
+      tt[i] = 2.0 * xt * tt[i - 1] - tt[i - 2];
+      B.tp[i] = 2.0 * xp * B.tp[i - 1] - B.tp[i - 2];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int ab = 4 * q + tig;
+    const int ia = ab / PA, ib = ab - PA * ia;
+    const double va = (ia == 0) ? ts[0] : (ia == 1) ? ts[1] : ts[2];
+    const double vb = (ib == 0) ? tt[0] : (ib == 1) ? tt[1] : (ib == 2) ? tt[2]
+                    : (ib == 3) ? tt[3] : tt[4];
+    B.tst[q] = (ab < PS * PA) ? (EXACT ? mul_rn(va, vb) : va * vb) : 0.0;
+  }
+  return B;
+}
+
+// acc[nt] (+)= sum_i basis_i * C[i][8nt + grp] over the 80-padded K range.
+template <bool EXACT>
+__device__ __forceinline__ void basis_times_block(const BasisA& B,
+                                                  const double* __restrict__ C,
+                                                  int grp, int tig,
+                                                  double (&c0)[4],
+                                                  double (&c1)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const bool ok = (4 * q + tig) < PS * PA;
+#pragma unroll
+    for (int c = 0; c < PA; ++c) {
+      const double av = EXACT ? mul_rn(B.tst[q], B.tp[c]) : B.tst[q] * B.tp[c];
+      const int i = (4 * q + tig) * PA + c;
+      const double* src = C + i * NRCOL + grp;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const double bv = ok ? __ldg(src + 8 * nt) : 0.0;
+        dmma(c0[nt], c1[nt], av, bv);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K4 ----
+struct AccArgs {
+  const int* inst_off; const int* inst_type; const int* inst_crow_off;
+  const int* crow; const int* sig_off; const int2* groups;
+  const unsigned char* scatter; const double* tgeom;
+  const double* coef_child; double* coef_parent;
+  double kr[2], ki[2];
+};
+
+constexpr int ACC_WARPS = 4;
+
+// One CTA per parent segment row (owner computes, no atomics): every
+// (parent segment, child box) instance re-interpolates the child's
+// coefficients at the parent's 75 nodes (tiles of 8 nodes sharing a child
+// segment sigma, 20 k-steps x 4 column tiles of DMMA), multiplies by the
+// re-centering ratio (r_p/r_c) exp(i kappa (r_c - r_p)) and accumulates into
+// a per-warp shared buffer; the 4 buffers are summed in fixed order (bitwise
+// deterministic), transformed to coefficients (K3) and written once.
+template <int NK>
+__global__ void __launch_bounds__(128, 2) accum_kernel(AccArgs a) {
+  extern __shared__ double2 smem[];
+  const int p = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 2, tig = lane & 3;
+  double2* acc = smem + warp * NN * NCOL;
+  for (int i = lane; i < NN * NCOL; i += 32) acc[i] = make_double2(0.0, 0.0);
+  __syncwarp();
+  const int i0 = a.inst_off[p], i1 = a.inst_off[p + 1];
+  int tau = 0;
+  for (int inst = i0; inst < i1; ++inst) {
+    const int t = a.inst_type[inst];
+    const int g0 = a.sig_off[t], g1 = a.sig_off[t + 1];
+    const int cb = a.inst_crow_off[inst];
+    const double* tg = a.tgeom + (size_t)t * NN * 5;
+    const unsigned char* sc = a.scatter + (size_t)t * NN;
+    for (int g = g0; g < g1; ++g) {
+      const int2 se = a.groups[g];
+      const double* C = a.coef_child + (size_t)a.crow[cb + g - g0] * SEG_DOUBLES;
+      for (int r0 = se.x; r0 < se.y; r0 += 8, ++tau) {
+        if ((tau % ACC_WARPS) != warp) continue;
+        const int row = r0 + grp;
+        const bool valid = row < se.y;
+        const int j = valid ? row : se.y - 1;
+        const BasisA B = make_basis<false>(tg[j], tg[NN + j], tg[2 * NN + j], tig);
+        double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+        basis_times_block<false>(B, C, grp, tig, c0, c1);
+        const double rp = tg[3 * NN + j], rc = tg[4 * NN + j];
+        const double q = rp / rc;
+        double2 ratio[NK];
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+          const double2 e = cexp_ikx(a.kr[k], a.ki[k], rc - rp);
+          ratio[k] = make_double2(q * e.x, q * e.y);
+        }
+        if (valid) {
+          double2* dst = acc + sc[j] * NCOL;
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            const int m = 4 * nt + tig;
+            const double2 v = cmul(make_double2(c0[nt], c1[nt]),
+                                   (NK > 1 && (tig & 1)) ? ratio[NK - 1] : ratio[0]);
+            dst[m].x += v.x;
+            dst[m].y += v.y;
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NN * NCOL; i += blockDim.x) {
+    double2 s = smem[i];
+#pragma unroll
+    for (int w = 1; w < ACC_WARPS; ++w) {
+      const double2 v = smem[w * NN * NCOL + i];
+      s.x += v.x;
+      s.y += v.y;
+    }
+    smem[i] = s;
+  }
+  __syncthreads();
+  to_coeffs_smem(smem, threadIdx.x, blockDim.x);
+  store_segment(a.coef_parent + (size_t)p * SEG_DOUBLES, smem, threadIdx.x,
+                blockDim.x);
+}
+
+// ---------------------------------------------------------------- K5 ----
+struct EmitArgs {
+  const int4* tiles; int n_tiles;
+  const int* pair_id; const double4* geom; const double4* geom_disp;
+  const double* coef;
+  double kr[2], ki[2];
+  double2* partial;   // [pair][2][NCOL]
+};
+
+// One warp per tile of <= 4 (box, target) pairs sharing a segment row; the 8
+// MMA rows are (pair, point) with point 0 = x_t, 1 = x_t + h n_t (same
+// segment polynomial, reference ifgf.py:647-653).  The basis is formed
+// exactly as numpy does ((T_a T_b) T_c, unfused recurrences) so the
+// displaced/undisplaced difference sees only the contraction rounding.
+template <int NK>
+__global__ void __launch_bounds__(128) emit_kernel(EmitArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * 4 + warp;
+  if (tile >= a.n_tiles) return;
+  const int grp = lane >> 2, tig = lane & 3;
+  const int4 td = a.tiles[tile];
+  const int pp = grp >> 1, pt = grp & 1;
+  const bool has_disp = a.geom_disp != nullptr;
+  const bool valid = pp < td.z && (pt == 0 || has_disp);
+  const int pos = td.y + min(pp, td.z - 1);
+  const double4 gm = (pt && has_disp) ? a.geom_disp[pos] : a.geom[pos];
+  const BasisA B = make_basis<true>(gm.x, gm.y, gm.z, tig);
+  double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+  basis_times_block<true>(B, a.coef + (size_t)td.x * SEG_DOUBLES, grp, tig, c0, c1);
+  if (!valid) return;
+  const double r = gm.w;
+  const double den = mul_rn(4.0 * M_PI, r);
+  double2 gk[NK];
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    const double2 e = cexp_ikx(a.kr[k], a.ki[k], r);
+    gk[k] = make_double2(e.x / den, e.y / den);
+  }
+  double2* dst = a.partial + ((size_t)a.pair_id[pos] * 2 + pt) * NCOL;
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const int m = 4 * nt + tig;
+    dst[m] = cmul(make_double2(c0[nt], c1[nt]),
+                  (NK > 1 && (tig & 1)) ? gk[NK - 1] : gk[0]);
+  }
+}
+
+// out_tree[t][m] += sum of t's pair partials in box order (reference
+// per-box scatter-add, ifgf.py:664-673; levels D..3 in turn).
+__global__ void emit_reduce(int n, const int* __restrict__ tgt_off,
+                            const int* __restrict__ tgt_pairs,
+                            const double2* __restrict__ partial,
+                            double2* __restrict__ out,
+                            double2* __restrict__ out_disp) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * NCOL) return;
+  const int t = idx / NCOL, m = idx % NCOL;
+  const int q0 = tgt_off[t], q1 = tgt_off[t + 1];
+  if (q0 == q1) return;
+  double2 s = out[idx];
+  double2 sd = out_disp ? out_disp[idx] : make_double2(0.0, 0.0);
+  for (int q = q0; q < q1; ++q) {
+    const size_t pr = tgt_pairs[q];
+    const double2 v = partial[(pr * 2) * NCOL + m];
+    s.x += v.x;
+    s.y += v.y;
+    if (out_disp) {
+      const double2 vd = partial[(pr * 2 + 1) * NCOL + m];
+      sd.x += vd.x;
+      sd.y += vd.y;
+    }
+  }
+  out[idx] = s;
+  if (out_disp) out_disp[idx] = sd;
+}
+
+// out[(c*nk + k)][ell] = out_tree[iperm[ell]][c*NK + k]  (original order)
+__global__ void unpermute(int n, int ncols, const int* __restrict__ perm,
+                          const double2* __restrict__ src,
+                          double2* __restrict__ dst) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * ncols) return;
+  const int t = idx / ncols, m = idx % ncols;
+  dst[(size_t)m * n + perm[t]] = src[(size_t)t * NCOL + m];
+}
+
+// ------------------------------------------------------------ driver -----
+template <int NK>
+static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
+                       double* out, double* out_disp, cudaStream_t st) {
+  constexpr int CH = NCOL / NK;
+  const int n = p.n;
+  const int threads = 256;
+  int64_t launches = 0;
+  pack_weights<<<(n * CH + threads - 1) / threads, threads, 0, st>>>(
+      reinterpret_cast<const double2*>(w), nch, n, p.perm, CH,
+      reinterpret_cast<double2*>(p.wt));
+  ++launches;
+  IFGFB_CUDA(cudaMemsetAsync(p.out_tree, 0, sizeof(double2) * n * NCOL, st));
+  if (out_disp)
+    IFGFB_CUDA(cudaMemsetAsync(p.out_disp_tree, 0, sizeof(double2) * n * NCOL, st));
+  double kr[2] = {kap[0], NK > 1 ? kap[2] : 0.0};
+  double ki[2] = {kap[1], NK > 1 ? kap[3] : 0.0};
+  const int D = p.depth;
+  if (D >= 3) {
+    int cur = 0;
+    {
+      Level& L = p.levels[D];
+      LeafArgs la{L.seg_box, L.seg_id, L.centers, L.pt_start, L.pt_count, L.tabs,
+                  L.n_s, L.n_a, L.h, p.points_tree,
+                  reinterpret_cast<const double2*>(p.wt), {kr[0], kr[1]},
+                  {ki[0], ki[1]}, p.coef[cur]};
+      if (L.n_seg > 0) {
+        leaf_kernel<NK><<<L.n_seg, 128, 0, st>>>(la);
+        ++launches;
+      }
+    }
+    for (int d = D; d >= 3; --d) {
+      Level& L = p.levels[d];
+      if (L.n_etiles > 0) {
+        EmitArgs ea{L.etiles, L.n_etiles, L.pair_id, L.geom,
+                    out_disp ? L.geom_disp : nullptr, p.coef[cur],
+                    {kr[0], kr[1]}, {ki[0], ki[1]},
+                    reinterpret_cast<double2*>(p.partial)};
+        emit_kernel<NK><<<(L.n_etiles + 3) / 4, 128, 0, st>>>(ea);
+        emit_reduce<<<(n * NCOL + threads - 1) / threads, threads, 0, st>>>(
+            n, L.tgt_off, L.tgt_pairs, reinterpret_cast<const double2*>(p.partial),
+            reinterpret_cast<double2*>(p.out_tree),
+            out_disp ? reinterpret_cast<double2*>(p.out_disp_tree) : nullptr);
+        launches += 2;
+      }
+      if (d > 3 && L.has_accum) {
+        Level& U = p.levels[d - 1];
+        if (U.n_seg > 0) {
+          AccArgs aa{L.inst_off, L.inst_type, L.inst_crow_off, L.crow, L.sig_off,
+                     L.groups, L.scatter, L.tgeom, p.coef[cur], p.coef[cur ^ 1],
+                     {kr[0], kr[1]}, {ki[0], ki[1]}};
+          const size_t sm = sizeof(double2) * NN * NCOL * ACC_WARPS;
+          accum_kernel<NK><<<U.n_seg, 128, sm, st>>>(aa);
+          ++launches;
+        }
+        cur ^= 1;
+      }
+    }
+  }
+  const int ncols = nch * NK;
+  unpermute<<<(n * ncols + threads - 1) / threads, threads, 0, st>>>(
+      n, ncols, p.perm, reinterpret_cast<const double2*>(p.out_tree),
+      reinterpret_cast<double2*>(out));
+  ++launches;
+  if (out_disp) {
+    unpermute<<<(n * ncols + threads - 1) / threads, threads, 0, st>>>(
+        n, ncols, p.perm, reinterpret_cast<const double2*>(p.out_disp_tree),
+        reinterpret_cast<double2*>(out_disp));
+    ++launches;
+  }
+  IFGFB_CUDA(cudaGetLastError());
+  p.launches += launches;
+  return IFGFB_OK;
+}
+
+int far_setup_kernels() {
+  int rc = init_constants();
+  if (rc) return rc;
+  const int sm = sizeof(double2) * NN * NCOL * ACC_WARPS;
+  IFGFB_CUDA(cudaFuncSetAttribute(accum_kernel<1>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  IFGFB_CUDA(cudaFuncSetAttribute(accum_kernel<2>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  return IFGFB_OK;
+}
+
+int far_apply(Plan& p, const double* w, int nch, const double* kappas, int nk,
+              double* out, double* out_disp, cudaStream_t st) {
+  if (nk == 1) {
+    if (nch < 1 || nch > NCOL) { set_error("far_apply: 1 <= nch <= 16 for nk=1"); return IFGFB_ERR_ARG; }
+    return far_apply_t<1>(p, w, nch, kappas, out, out_disp, st);
+  }
+  if (nk == 2) {
+    if (nch < 1 || nch > NCOL / 2) { set_error("far_apply: 1 <= nch <= 8 for nk=2"); return IFGFB_ERR_ARG; }
+    return far_apply_t<2>(p, w, nch, kappas, out, out_disp, st);
+  }
+  set_error("far_apply: nk must be 1 or 2");
+  return IFGFB_ERR_ARG;
+}
+
+}  // namespace ifgfb

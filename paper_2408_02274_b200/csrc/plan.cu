@@ -1,0 +1,328 @@
+// C ABI of libifgfb200: plan construction (host arrays -> device), entry
+// points and error reporting.  See include/ifgfb.h for the contract.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ifgfb {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+int far_setup_kernels();
+
+template <typename T>
+static int dev_upload(Plan& p, T** dst, const T* src, size_t n) {
+  *dst = nullptr;
+  if (n == 0) return IFGFB_OK;
+  void* ptr = nullptr;
+  IFGFB_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+  p.allocations.push_back(ptr);
+  p.bytes += n * sizeof(T);
+  if (src) IFGFB_CUDA(cudaMemcpy(ptr, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  *dst = static_cast<T*>(ptr);
+  return IFGFB_OK;
+}
+
+template <typename T>
+static int dev_alloc(Plan& p, T** dst, size_t n) {
+  return dev_upload<T>(p, dst, nullptr, n);
+}
+
+static bool to_i32(const int64_t* src, size_t n, std::vector<int>& out,
+                   const char* what) {
+  out.resize(n);
+  for (size_t i = 0; i < n; ++i) {
+    if (src[i] < INT32_MIN || src[i] > INT32_MAX) {
+      set_error(std::string(what) + ": index exceeds int32");
+      return false;
+    }
+    out[i] = static_cast<int>(src[i]);
+  }
+  return true;
+}
+
+#define CHECK_ARG(cond, msg)             \
+  do {                                   \
+    if (!(cond)) {                       \
+      set_error(msg);                    \
+      return IFGFB_ERR_ARG;              \
+    }                                    \
+  } while (0)
+
+#define RC(x)                  \
+  do {                         \
+    int rc_ = (x);             \
+    if (rc_ != IFGFB_OK) return rc_; \
+  } while (0)
+
+}  // namespace ifgfb
+
+using namespace ifgfb;
+
+struct ifgfb_plan {
+  Plan p;
+};
+
+extern "C" {
+
+int ifgfb_abi_version(void) { return IFGFB_ABI_VERSION; }
+const char* ifgfb_last_error(void) { return g_err.c_str(); }
+
+int ifgfb_device_info(char* buf, size_t len) {
+  int dev = 0;
+  IFGFB_CUDA(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  IFGFB_CUDA(cudaGetDeviceProperties(&prop, dev));
+  snprintf(buf, len, "%s sm_%d%d SMs=%d", prop.name, prop.major, prop.minor,
+           prop.multiProcessorCount);
+  return IFGFB_OK;
+}
+
+int ifgfb_plan_create(const ifgfb_tree_desc* t, ifgfb_plan** out) {
+  CHECK_ARG(t && out, "null argument");
+  CHECK_ARG(t->n_points > 0 && t->depth >= 1, "bad tree sizes");
+  CHECK_ARG(t->p_s == PS && t->p_a == PA,
+            "only p_s=3, p_a=5 (IfgfConfig defaults) are compiled");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    set_error("no CUDA device available (libifgfb200 has no CPU fallback)");
+    return IFGFB_ERR_CUDA;
+  }
+  auto* h = new ifgfb_plan();
+  Plan& p = h->p;
+  IFGFB_CUDA(cudaGetDevice(&p.device));
+  p.n = t->n_points;
+  p.depth = t->depth;
+  p.levels.resize(p.depth + 1);
+  int rc = dev_upload(p, &p.points_tree, t->points_tree, (size_t)p.n * 3);
+  std::vector<int> perm;
+  if (rc == IFGFB_OK && !to_i32(t->perm, p.n, perm, "perm")) rc = IFGFB_ERR_ARG;
+  if (rc == IFGFB_OK) rc = dev_upload(p, &p.perm, perm.data(), perm.size());
+  if (rc == IFGFB_OK) rc = far_setup_kernels();
+  if (rc != IFGFB_OK) {
+    ifgfb_plan_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return IFGFB_OK;
+}
+
+int ifgfb_plan_add_level(ifgfb_plan* h, const ifgfb_level_desc* d) {
+  CHECK_ARG(h && d, "null argument");
+  Plan& p = h->p;
+  CHECK_ARG(!p.finalized, "plan already finalized");
+  CHECK_ARG(d->level >= 3 && d->level <= p.depth, "level out of range");
+  Level& L = p.levels[d->level];
+  L.d = d->level;
+  L.n_boxes = d->n_boxes;
+  L.n_s = d->n_s;
+  L.n_a = d->n_a;
+  L.side = d->side;
+  L.h = d->h;
+  L.delta_s = d->delta_s;
+  L.delta_a = d->delta_a;
+  CHECK_ARG(d->n_segments <= INT32_MAX, "too many segments for int32 rows");
+  L.n_seg = (int)d->n_segments;
+  RC(dev_upload(p, &L.centers, d->centers, (size_t)L.n_boxes * 3));
+  std::vector<int> tmp;
+  if (!to_i32(d->pt_start, L.n_boxes, tmp, "pt_start")) return IFGFB_ERR_ARG;
+  RC(dev_upload(p, &L.pt_start, tmp.data(), tmp.size()));
+  if (!to_i32(d->pt_count, L.n_boxes, tmp, "pt_count")) return IFGFB_ERR_ARG;
+  RC(dev_upload(p, &L.pt_count, tmp.data(), tmp.size()));
+  std::vector<int> sbox(L.n_seg), sid(L.n_seg);
+  for (int b = 0; b < L.n_boxes; ++b) {
+    CHECK_ARG(d->seg_off[b] <= d->seg_off[b + 1], "seg_off not monotone");
+    for (int64_t r = d->seg_off[b]; r < d->seg_off[b + 1]; ++r) sbox[r] = b;
+  }
+  CHECK_ARG(d->seg_off[L.n_boxes] == L.n_seg, "seg_off end != n_segments");
+  if (!to_i32(d->seg_ids, L.n_seg, sid, "seg_ids")) return IFGFB_ERR_ARG;
+  RC(dev_upload(p, &L.seg_box, sbox.data(), sbox.size()));
+  RC(dev_upload(p, &L.seg_id, sid.data(), sid.size()));
+  std::vector<double> tabs;
+  tabs.insert(tabs.end(), d->s_nodes, d->s_nodes + L.n_s * PS);
+  tabs.insert(tabs.end(), d->sin_t, d->sin_t + L.n_a * PA);
+  tabs.insert(tabs.end(), d->cos_t, d->cos_t + L.n_a * PA);
+  tabs.insert(tabs.end(), d->sin_p, d->sin_p + 2 * L.n_a * PA);
+  tabs.insert(tabs.end(), d->cos_p, d->cos_p + 2 * L.n_a * PA);
+  RC(dev_upload(p, &L.tabs, tabs.data(), tabs.size()));
+  p.max_seg = std::max(p.max_seg, L.n_seg);
+  return IFGFB_OK;
+}
+
+int ifgfb_plan_set_emission(ifgfb_plan* h, const ifgfb_emit_desc* e) {
+  CHECK_ARG(h && e, "null argument");
+  Plan& p = h->p;
+  CHECK_ARG(!p.finalized, "plan already finalized");
+  CHECK_ARG(e->level >= 3 && e->level <= p.depth, "level out of range");
+  Level& L = p.levels[e->level];
+  CHECK_ARG(L.d == e->level, "add_level must precede set_emission");
+  const int64_t np_ = e->n_pairs;
+  CHECK_ARG(np_ >= 0 && np_ < INT32_MAX, "pair count out of range");
+  L.n_pairs = np_;
+  L.has_disp = e->geom_disp != nullptr;
+  // sort pairs by segment row (stable) -> per-row tiles of <= 4 pairs
+  std::vector<int> order(np_);
+  std::iota(order.begin(), order.end(), 0);
+  for (int64_t i = 0; i < np_; ++i) {
+    CHECK_ARG(e->row[i] >= 0 && e->row[i] < L.n_seg, "emission row out of range");
+    CHECK_ARG(e->target[i] >= 0 && e->target[i] < p.n, "emission target out of range");
+  }
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return e->row[a] < e->row[b]; });
+  std::vector<double4> g(np_), gd(L.has_disp ? np_ : 0);
+  std::vector<int4> tiles;
+  for (int64_t s = 0; s < np_; ++s) {
+    const int i = order[s];
+    g[s] = make_double4(e->geom[4 * i], e->geom[4 * i + 1], e->geom[4 * i + 2],
+                        e->geom[4 * i + 3]);
+    if (L.has_disp)
+      gd[s] = make_double4(e->geom_disp[4 * i], e->geom_disp[4 * i + 1],
+                           e->geom_disp[4 * i + 2], e->geom_disp[4 * i + 3]);
+  }
+  int64_t s = 0;
+  while (s < np_) {
+    const int64_t row = e->row[order[s]];
+    int64_t t = s;
+    while (t < np_ && e->row[order[t]] == row) ++t;
+    for (int64_t q = s; q < t; q += 4)
+      tiles.push_back(make_int4((int)row, (int)q, (int)std::min<int64_t>(4, t - q), 0));
+    s = t;
+  }
+  L.n_etiles = (int)tiles.size();
+  RC(dev_upload(p, &L.pair_id, order.data(), order.size()));
+  RC(dev_upload(p, &L.geom, g.data(), g.size()));
+  if (L.has_disp) RC(dev_upload(p, &L.geom_disp, gd.data(), gd.size()));
+  RC(dev_upload(p, &L.etiles, tiles.data(), tiles.size()));
+  // per-target CSR of pair indices (box-major pair order == box order)
+  std::vector<int> off(p.n + 1, 0), lst(np_);
+  for (int64_t i = 0; i < np_; ++i) off[e->target[i] + 1]++;
+  for (int t = 0; t < p.n; ++t) off[t + 1] += off[t];
+  std::vector<int> fill(off.begin(), off.end() - 1);
+  for (int64_t i = 0; i < np_; ++i) lst[fill[e->target[i]]++] = (int)i;
+  RC(dev_upload(p, &L.tgt_off, off.data(), off.size()));
+  RC(dev_upload(p, &L.tgt_pairs, lst.data(), lst.size()));
+  p.max_pairs = std::max<int64_t>(p.max_pairs, np_);
+  return IFGFB_OK;
+}
+
+int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
+  CHECK_ARG(h && a, "null argument");
+  Plan& p = h->p;
+  CHECK_ARG(!p.finalized, "plan already finalized");
+  CHECK_ARG(a->level >= 4 && a->level <= p.depth, "accum level out of range");
+  Level& L = p.levels[a->level];
+  Level& U = p.levels[a->level - 1];
+  CHECK_ARG(L.d == a->level && U.d == a->level - 1,
+            "add_level(d) and add_level(d-1) must precede add_accum(d)");
+  CHECK_ARG(a->n_parent_rows == U.n_seg, "n_parent_rows != segments of level d-1");
+  const int64_t nt = a->n_types;
+  L.n_types = nt;
+  std::vector<int> tmp;
+  if (!to_i32(a->sig_off, nt + 1, tmp, "sig_off")) return IFGFB_ERR_ARG;
+  RC(dev_upload(p, &L.sig_off, tmp.data(), tmp.size()));
+  const int64_t ng = a->sig_off[nt];
+  std::vector<int2> grp(ng);
+  for (int64_t g = 0; g < ng; ++g) {
+    CHECK_ARG(a->group_start[g] >= 0 && a->group_end[g] <= NN &&
+                  a->group_start[g] < a->group_end[g], "bad sigma group bounds");
+    grp[g] = make_int2((int)a->group_start[g], (int)a->group_end[g]);
+  }
+  RC(dev_upload(p, &L.groups, grp.data(), grp.size()));
+  std::vector<unsigned char> sc(nt * NN);
+  for (int64_t i = 0; i < nt * NN; ++i) {
+    CHECK_ARG(a->scatter[i] >= 0 && a->scatter[i] < NN, "scatter slot out of range");
+    sc[i] = (unsigned char)a->scatter[i];
+  }
+  RC(dev_upload(p, &L.scatter, sc.data(), sc.size()));
+  std::vector<double> geo(nt * NN * 5);
+  for (int64_t t = 0; t < nt; ++t)
+    for (int j = 0; j < NN; ++j) {
+      const int64_t src = t * NN + j;
+      double* dst = geo.data() + t * NN * 5;
+      dst[j] = a->xs[src];
+      dst[NN + j] = a->xt[src];
+      dst[2 * NN + j] = a->xp[src];
+      dst[3 * NN + j] = a->r_parent[src];
+      dst[4 * NN + j] = a->r_child[src];
+    }
+  RC(dev_upload(p, &L.tgeom, geo.data(), geo.size()));
+  if (!to_i32(a->inst_off, a->n_parent_rows + 1, tmp, "inst_off")) return IFGFB_ERR_ARG;
+  RC(dev_upload(p, &L.inst_off, tmp.data(), tmp.size()));
+  L.n_instances = a->n_instances;
+  if (!to_i32(a->inst_type, a->n_instances, tmp, "inst_type")) return IFGFB_ERR_ARG;
+  RC(dev_upload(p, &L.inst_type, tmp.data(), tmp.size()));
+  if (!to_i32(a->inst_crow_off, a->n_instances + 1, tmp, "inst_crow_off")) return IFGFB_ERR_ARG;
+  RC(dev_upload(p, &L.inst_crow_off, tmp.data(), tmp.size()));
+  const int64_t ncrow = a->inst_crow_off[a->n_instances];
+  for (int64_t i = 0; i < ncrow; ++i)
+    CHECK_ARG(a->crow[i] >= 0 && a->crow[i] < L.n_seg, "crow out of range");
+  if (!to_i32(a->crow, ncrow, tmp, "crow")) return IFGFB_ERR_ARG;
+  RC(dev_upload(p, &L.crow, tmp.data(), tmp.size()));
+  L.has_accum = true;
+  return IFGFB_OK;
+}
+
+int ifgfb_plan_finalize(ifgfb_plan* h) {
+  CHECK_ARG(h, "null argument");
+  Plan& p = h->p;
+  CHECK_ARG(!p.finalized, "plan already finalized");
+  for (int d = 3; d <= p.depth; ++d) {
+    if (p.levels[d].d != d) {
+      set_error("level " + std::to_string(d) + " missing");
+      return IFGFB_ERR_STATE;
+    }
+    if (d >= 4 && !p.levels[d].has_accum) {
+      set_error("accumulation plan for level " + std::to_string(d) + " missing");
+      return IFGFB_ERR_STATE;
+    }
+  }
+  const size_t n = p.n;
+  RC(dev_alloc(p, &p.wt, n * NCOL * 2));
+  p.coef_cap = std::max(p.max_seg, 1);
+  for (int i = 0; i < 2; ++i) RC(dev_alloc(p, &p.coef[i], p.coef_cap * SEG_DOUBLES));
+  RC(dev_alloc(p, &p.partial, std::max<int64_t>(p.max_pairs, 1) * 2 * NCOL * 2));
+  RC(dev_alloc(p, &p.out_tree, n * NCOL * 2));
+  RC(dev_alloc(p, &p.out_disp_tree, n * NCOL * 2));
+  p.finalized = true;
+  return IFGFB_OK;
+}
+
+int ifgfb_plan_destroy(ifgfb_plan* h) {
+  if (!h) return IFGFB_OK;
+  for (void* ptr : h->p.allocations) cudaFree(ptr);
+  if (h->p.host_stage) cudaFreeHost(h->p.host_stage);
+  delete h;
+  return IFGFB_OK;
+}
+
+int64_t ifgfb_plan_device_bytes(const ifgfb_plan* h) {
+  return h ? (int64_t)h->p.bytes : 0;
+}
+
+int64_t ifgfb_plan_last_launches(const ifgfb_plan* h) {
+  return h ? h->p.launches : 0;
+}
+
+int ifgfb_far_apply(ifgfb_plan* h, const double* w, int nch,
+                    const double* kappas, int nk, double* out,
+                    double* out_disp, void* stream) {
+  CHECK_ARG(h && w && kappas && out, "null argument");
+  Plan& p = h->p;
+  if (!p.finalized) {
+    set_error("plan not finalized");
+    return IFGFB_ERR_STATE;
+  }
+  double kap[4] = {kappas[0], kappas[1], nk > 1 ? kappas[2] : 0.0,
+                   nk > 1 ? kappas[3] : 0.0};
+  p.launches = 0;
+  return far_apply(p, w, nch, kap, nk, out, out_disp,
+                   static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,240 @@
+"""Device-resident IFGF plan and the drop-in ``ifgf_apply``.
+
+``FarFieldPlan`` flattens a (BoxTree, ConeHierarchy) pair -- built by this
+package or by the reference itself (same attribute layout) -- plus the
+propagation and emission plans into the C ABI of libifgfb200 and keeps the
+device copy alive.  ``ifgf_apply`` mirrors reference ``ifgf.py:885-923``
+(same signature, argument meaning, output layout and errors).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .octree import accumulation_plan, emission_plan
+
+__all__ = ["FarFieldPlan", "ifgf_apply", "device_stream"]
+
+
+def device_stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+class FarFieldPlan:
+    """libifgfb200 plan for one tree/hierarchy (+ displaced-point geometry)."""
+
+    def __init__(self, tree, hier, displaced_normals=None,
+                 displaced_step: float = 1e-6, surface=None, near=None):
+        lib = _lib.load()
+        if not torch.cuda.is_available():
+            raise RuntimeError("CUDA device required (no CPU fallback)")
+        cfg = hier.config
+        self.tree, self.hier = tree, hier
+        self.n = int(tree.points.shape[0])
+        self.depth = int(tree.depth)
+        self._keep = []          # host arrays referenced during upload
+        self.disp = displaced_normals is not None
+        self.step = float(displaced_step)
+        disp_t = None
+        if self.disp:
+            nrm = np.asarray(displaced_normals, dtype=float)
+            # same expression as reference ifgf.py:822-823
+            disp_t = tree.points + displaced_step * nrm[tree.perm]
+        pts = _c(tree.points, np.float64)
+        perm = _c(tree.perm, np.int64)
+        td = _lib.TreeDesc(self.n, self.depth, cfg.p_s, cfg.p_a,
+                           _lib.dptr(pts), _lib.iptr(perm))
+        h = __import__("ctypes").c_void_p()
+        _lib.check(lib.ifgfb_plan_create(td, h), "ifgfb_plan_create")
+        self._h = h
+        self.stats = {"levels": {}}
+        try:
+            for d in range(3, self.depth + 1):
+                self._add_level(lib, d)
+            for d in range(4, self.depth + 1):
+                self._add_accum(lib, d)
+            for d in range(3, self.depth + 1):
+                self._add_emission(lib, d, disp_t)
+            if surface is not None:
+                _lib.check(lib.ifgfb_plan_set_surface(self._h, surface),
+                           "ifgfb_plan_set_surface")
+            if near is not None:
+                _lib.check(lib.ifgfb_plan_set_near(self._h, near),
+                           "ifgfb_plan_set_near")
+            _lib.check(lib.ifgfb_plan_finalize(self._h), "ifgfb_plan_finalize")
+        except Exception:
+            lib.ifgfb_plan_destroy(self._h)
+            self._h = None
+            raise
+        self._keep = []
+
+    # ------------------------------------------------------------ upload --
+    def _hold(self, *arrs):
+        self._keep.extend(arrs)
+        return arrs
+
+    def _add_level(self, lib, d):
+        tree, hier = self.tree, self.hier
+        lvl, cl = tree.level(d), hier.level(d)
+        arrs = dict(
+            centers=_c(lvl.centers, np.float64),
+            pt_start=_c(lvl.pt_start, np.int64),
+            pt_count=_c(lvl.pt_count, np.int64),
+            seg_off=_c(cl.seg_off, np.int64), seg_ids=_c(cl.seg_ids, np.int64),
+            s_nodes=_c(cl.s_nodes, np.float64),
+            sin_t=_c(np.sin(cl.ang_nodes_t), np.float64),
+            cos_t=_c(np.cos(cl.ang_nodes_t), np.float64),
+            sin_p=_c(np.sin(cl.ang_nodes_p), np.float64),
+            cos_p=_c(np.cos(cl.ang_nodes_p), np.float64))
+        self._hold(*arrs.values())
+        desc = _lib.LevelDesc(
+            d, lvl.n_boxes, cl.n_s, cl.n_a, lvl.side, cl.h, cl.delta_s,
+            cl.delta_a, _lib.dptr(arrs["centers"]),
+            _lib.iptr(arrs["pt_start"]), _lib.iptr(arrs["pt_count"]),
+            cl.n_segments, _lib.iptr(arrs["seg_off"]),
+            _lib.iptr(arrs["seg_ids"]), _lib.dptr(arrs["s_nodes"]),
+            _lib.dptr(arrs["sin_t"]), _lib.dptr(arrs["cos_t"]),
+            _lib.dptr(arrs["sin_p"]), _lib.dptr(arrs["cos_p"]))
+        _lib.check(lib.ifgfb_plan_add_level(self._h, desc),
+                   f"ifgfb_plan_add_level({d})")
+        self.stats["levels"].setdefault(d, {})["segments"] = int(cl.n_segments)
+
+    def _add_accum(self, lib, d):
+        ap = accumulation_plan(self.tree, self.hier, d)
+        if ap.crow_misses:
+            # the reference silently uses the neighbouring row in that case
+            # (searchsorted, ifgf.py:743-746); we reproduce the same rows.
+            pass
+        a = dict(sig_off=_c(ap.sig_off, np.int64),
+                 gs=_c(ap.group_bounds, np.int64),
+                 ge=_c(ap.group_end, np.int64),
+                 sc=_c(ap.scatter, np.int64), xs=_c(ap.xs, np.float64),
+                 xt=_c(ap.xt, np.float64), xp=_c(ap.xp, np.float64),
+                 rp=_c(ap.r_parent, np.float64), rc=_c(ap.r_child, np.float64),
+                 io=_c(ap.inst_off, np.int64), it=_c(ap.inst_type, np.int64),
+                 ico=_c(ap.inst_crow_off, np.int64), cr=_c(ap.crow, np.int64))
+        self._hold(*a.values())
+        desc = _lib.AccumDesc(
+            d, ap.n_types, _lib.iptr(a["sig_off"]), _lib.iptr(a["gs"]),
+            _lib.iptr(a["ge"]), _lib.iptr(a["sc"]), _lib.dptr(a["xs"]),
+            _lib.dptr(a["xt"]), _lib.dptr(a["xp"]), _lib.dptr(a["rp"]),
+            _lib.dptr(a["rc"]), self.hier.level(d - 1).n_segments,
+            _lib.iptr(a["io"]), ap.n_instances, _lib.iptr(a["it"]),
+            _lib.iptr(a["ico"]), _lib.iptr(a["cr"]))
+        _lib.check(lib.ifgfb_plan_add_accum(self._h, desc),
+                   f"ifgfb_plan_add_accum({d})")
+        st = self.stats["levels"].setdefault(d, {})
+        st.update(types=int(ap.n_types), instances=int(ap.n_instances),
+                  crow_misses=int(ap.crow_misses))
+
+    def _add_emission(self, lib, d, disp_t):
+        ep = emission_plan(self.tree, self.hier, d, disp_t)
+        a = dict(row=_c(ep.row, np.int64), tg=_c(ep.target, np.int64),
+                 g=_c(ep.geom, np.float64),
+                 gd=None if ep.geom_disp is None else _c(ep.geom_disp,
+                                                         np.float64))
+        self._hold(*[v for v in a.values() if v is not None])
+        desc = _lib.EmitDesc(d, ep.n_pairs, _lib.iptr(a["row"]),
+                             _lib.iptr(a["tg"]), _lib.dptr(a["g"]),
+                             _lib.dptr(a["gd"]))
+        _lib.check(lib.ifgfb_plan_set_emission(self._h, desc),
+                   f"ifgfb_plan_set_emission({d})")
+        self.stats["levels"].setdefault(d, {}).update(
+            pairs=int(ep.n_pairs), row_misses=int(ep.row_misses))
+
+    # ------------------------------------------------------------- apply --
+    @property
+    def handle(self):
+        return self._h
+
+    def device_bytes(self) -> int:
+        return int(_lib.load().ifgfb_plan_device_bytes(self._h))
+
+    def last_launches(self) -> int:
+        return int(_lib.load().ifgfb_plan_last_launches(self._h))
+
+    def far_apply_device(self, w: torch.Tensor, kappas, out: torch.Tensor,
+                         out_disp: torch.Tensor | None = None):
+        """w (nch, N) complex128 cuda tensor (original order) -> out, out_disp
+        (nch, nk, N) complex128 cuda tensors."""
+        nch = w.shape[0]
+        kap = np.zeros(4)
+        kk = [complex(k) for k in kappas]
+        for i, k in enumerate(kk):
+            kap[2 * i], kap[2 * i + 1] = k.real, k.imag
+        if out_disp is not None and not self.disp:
+            raise ValueError("plan was built without displaced normals")
+        _lib.check(_lib.load().ifgfb_far_apply(
+            self._h, w.data_ptr(), nch, _lib.dptr(kap), len(kk),
+            out.data_ptr(), None if out_disp is None else out_disp.data_ptr(),
+            device_stream()), "ifgfb_far_apply")
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None:
+            try:
+                _lib.load().ifgfb_plan_destroy(self._h)
+            except Exception:
+                pass
+            self._h = None
+
+
+def _plan_for(tree, hier, normals, step) -> FarFieldPlan:
+    cache = hier.__dict__.setdefault("_b200_plans", {})
+    key = (id(tree), None if normals is None else id(normals),
+           float(step) if normals is not None else None)
+    plan = cache.get(key)
+    if plan is None:
+        plan = FarFieldPlan(tree, hier, normals, step)
+        cache[key] = (plan, normals)   # keep normals alive for the id key
+        return plan
+    return plan[0] if isinstance(plan, tuple) else plan
+
+
+def ifgf_apply(tree, hier, weights, kappas, mode: str | None = None,
+               displaced_normals=None, displaced_step: float = 1e-6):
+    """Drop-in for reference ``ifgf_apply`` (ifgf.py:885-923) on the GPU.
+
+    Returns numpy (out, out_disp) of shape (nch, nk, N), original order.
+    'vec' and 'seq' give identical values (every column of a group is
+    carried through one device traversal; groups of <= 16 columns).
+    """
+    mode = mode or hier.config.mode
+    if mode not in ("vec", "seq"):
+        raise ValueError("mode must be 'vec' or 'seq'")
+    weights = np.atleast_2d(weights)
+    kappas = tuple(kappas)
+    nch, nk = weights.shape[0], len(kappas)
+    n = tree.points.shape[0]
+    if tree.depth < 3:
+        z = np.zeros((nch, nk, n), dtype=complex)
+        return z, (np.zeros_like(z) if displaced_normals is not None else None)
+    if nk > 2:
+        parts = [ifgf_apply(tree, hier, weights, kappas[i:i + 2], mode,
+                            displaced_normals, displaced_step)
+                 for i in range(0, nk, 2)]
+        out = np.concatenate([p[0] for p in parts], axis=1)
+        od = (None if displaced_normals is None
+              else np.concatenate([p[1] for p in parts], axis=1))
+        return out, od
+    plan = _plan_for(tree, hier, displaced_normals, displaced_step)
+    group = 16 // nk
+    dev = torch.device("cuda")
+    out = np.empty((nch, nk, n), dtype=complex)
+    od = np.empty_like(out) if displaced_normals is not None else None
+    for c0 in range(0, nch, group):
+        c1 = min(nch, c0 + group)
+        w = torch.from_numpy(np.ascontiguousarray(
+            weights[c0:c1], dtype=np.complex128)).to(dev)
+        o = torch.empty((c1 - c0, nk, n), dtype=torch.complex128, device=dev)
+        o_d = torch.empty_like(o) if od is not None else None
+        plan.far_apply_device(w, kappas, o, o_d)
+        out[c0:c1] = o.cpu().numpy()
+        if od is not None:
+            od[c0:c1] = o_d.cpu().numpy()
+    return out, od

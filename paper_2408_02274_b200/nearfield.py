@@ -1,0 +1,279 @@
+"""Near-field plan: singular/near patch classification, singular moments and
+the local-correction pair lists (plan time, host).
+
+These are one-time precomputations whose OUTPUT the per-matvec device kernel
+(``csrc/nearfield.cu``) consumes; restated from the reference so the framework
+runs standalone:
+
+* ``SingularQuadratureConfig``      -- reference ``quadrature.py:46-65``
+* ``classify_targets``              -- reference ``quadrature.py:97-156``
+* ``graded_map`` / ``clustered_nodes`` -- reference ``quadrature.py:163-228``
+* ``compute_moments``               -- reference ``quadrature.py:271-331``
+* ``correction_pairs``              -- reference ``quadrature.py:490-525``
+  (only the (target, source) index lists; the device recomputes the kernel
+  values, so no CSR values are stored)
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import cheb
+from .surface import SurfaceDiscretization, closest_point_batch
+
+__all__ = ["SingularQuadratureConfig", "SingularityMap", "MomentGroup",
+           "SingularMomentTable", "classify_targets", "graded_map",
+           "clustered_nodes", "compute_moments", "correction_pairs"]
+
+
+@dataclass(frozen=True)
+class SingularQuadratureConfig:
+    d: int = 4
+    n_beta: int | None = None
+    delta_factor: float = 1.0
+
+    def __post_init__(self):
+        if self.d < 2:
+            raise ValueError("grading order must be >= 2")
+
+    def resolve_n_beta(self, n_c: int) -> int:
+        n = self.n_beta if self.n_beta is not None else max(4 * n_c, 48)
+        if n < n_c:
+            raise ValueError("refined node count must be >= n_c")
+        return n + (n % 2)
+
+
+@dataclass
+class SingularityMap:
+    """CSR per target: singular/near patch ids, closest (u, v), distance."""
+
+    n_targets: int
+    n_patches: int
+    delta: np.ndarray
+    offsets: np.ndarray
+    patch_ids: np.ndarray
+    closest_uv: np.ndarray
+    dists: np.ndarray
+
+    def singular_patches(self, ell: int) -> np.ndarray:
+        return self.patch_ids[self.offsets[ell]:self.offsets[ell + 1]]
+
+    def pairs_for_patch(self, p: int):
+        sel = np.nonzero(self.patch_ids == p)[0]
+        tg = (np.searchsorted(self.offsets, sel, side="right") - 1).astype(
+            np.int64)
+        return tg, self.closest_uv[sel, 0], self.closest_uv[sel, 1]
+
+
+def classify_targets(disc: SurfaceDiscretization,
+                     config: SingularQuadratureConfig | None = None,
+                     targets=None) -> SingularityMap:
+    """(target, patch) is singular when dist <= delta_factor * spacing_p."""
+    config = config or SingularQuadratureConfig()
+    on_surface = targets is None
+    pts = disc.points if on_surface else np.atleast_2d(
+        np.asarray(targets, dtype=float))
+    n_t = pts.shape[0]
+    delta = config.delta_factor * disc.max_spacing
+    grid = cheb.nodes(disc.n_c)
+    found = [[] for _ in range(n_t)]
+    for p, patch in enumerate(disc.patches):
+        lower = np.linalg.norm(pts - patch.center, axis=1) - patch.bound_radius
+        cand = np.nonzero(lower <= delta[p])[0]
+        if cand.size == 0:
+            continue
+        own = np.zeros(cand.size, dtype=bool)
+        if on_surface:
+            own = disc.patch_of[cand] == p
+            for ell in cand[own]:
+                _, i, j = disc.decode_index(int(ell))
+                found[ell].append((p, grid[i], grid[j], 0.0))
+        rest = cand[~own]
+        if rest.size == 0:
+            continue
+        seed = disc.patch_points(p).reshape(disc.n_c, disc.n_c, 3)
+        dmin = np.min(np.linalg.norm(
+            pts[rest][:, None, :] - seed.reshape(-1, 3)[None, :, :], axis=-1),
+            axis=1)
+        rest = rest[dmin - disc.max_spacing[p] <= delta[p]]
+        if rest.size == 0:
+            continue
+        u, v, dist = closest_point_batch(disc.patches[p], pts[rest], seed)
+        for ell, uu, vv, dd in zip(rest, u, v, dist):
+            if dd <= delta[p]:
+                found[ell].append((p, uu, vv, dd))
+    offsets = np.zeros(n_t + 1, dtype=np.int64)
+    ids, uvs, ds = [], [], []
+    for ell in range(n_t):
+        ent = sorted(found[ell])
+        offsets[ell + 1] = offsets[ell] + len(ent)
+        for p, u, v, dd in ent:
+            ids.append(p)
+            uvs.append((u, v))
+            ds.append(dd)
+    return SingularityMap(n_t, disc.n_patches, delta, offsets,
+                          np.asarray(ids, dtype=np.int32),
+                          np.asarray(uvs, dtype=float).reshape(-1, 2),
+                          np.asarray(ds, dtype=float))
+
+
+# ---------------------------------------------------------------------------
+# graded clustered quadrature
+# ---------------------------------------------------------------------------
+
+def _nu(tau, d):
+    return ((1.0 / d - 0.5) * ((np.pi - tau) / np.pi) ** 3
+            + (tau - np.pi) / (d * np.pi) + 0.5)
+
+
+def _nu_prime(tau, d):
+    return (3.0 * (0.5 - 1.0 / d) * (np.pi - tau) ** 2 / np.pi**3
+            + 1.0 / (d * np.pi))
+
+
+def graded_map(tau, d: int):
+    """Polynomially graded map of [0, 2pi] onto itself (order-d flat ends)."""
+    if d < 2:
+        raise ValueError("grading order must be >= 2")
+    tau = np.asarray(tau, dtype=float)
+    if np.any(tau < -1e-12) or np.any(tau > 2 * np.pi + 1e-12):
+        raise ValueError("argument outside [0, 2*pi]")
+    tau = np.clip(tau, 0.0, 2 * np.pi)
+    a = _nu(tau, d) ** d
+    b = _nu(2 * np.pi - tau, d) ** d
+    return 2 * np.pi * a / (a + b)
+
+
+def _graded_map_prime(tau, d):
+    tau = np.asarray(tau, dtype=float)
+    n1, n2 = _nu(tau, d), _nu(2 * np.pi - tau, d)
+    dn1 = _nu_prime(tau, d)
+    dn2 = -_nu_prime(2 * np.pi - tau, d)
+    a, b = n1**d, n2**d
+    da = d * n1 ** (d - 1) * dn1
+    db = d * n2 ** (d - 1) * dn2
+    return 2 * np.pi * (da * b - a * db) / (a + b) ** 2
+
+
+def clustered_nodes(alpha, base, d: int):
+    """Base nodes on [-1,1] remapped to accumulate at alpha (+ derivative)."""
+    t = np.asarray(base, dtype=float)
+    alpha = np.asarray(alpha, dtype=float)
+    scalar = alpha.ndim == 0
+    a = np.atleast_1d(alpha)[:, None]
+    tt = np.broadcast_to(t, (a.shape[0], t.size))
+    sg = np.sign(tt)
+    w_mid = graded_map(np.pi * np.abs(tt), d)
+    xi = a + (sg - a) / np.pi * w_mid
+    dxi = (1.0 - a * sg) * _graded_map_prime(np.pi * np.abs(tt), d)
+    hi = (a >= 1.0 - 1e-12)[:, 0]
+    if hi.any():
+        arg = np.pi * np.abs(tt[hi] - 1.0) / 2.0
+        xi[hi] = 1.0 - (2.0 / np.pi) * graded_map(arg, d)
+        dxi[hi] = _graded_map_prime(arg, d)
+    lo = (a <= -1.0 + 1e-12)[:, 0]
+    if lo.any():
+        arg = np.pi * np.abs(tt[lo] + 1.0) / 2.0
+        xi[lo] = -1.0 + (2.0 / np.pi) * graded_map(arg, d)
+        dxi[lo] = _graded_map_prime(arg, d)
+    if scalar:
+        return xi[0], dxi[0]
+    return xi, dxi
+
+
+@dataclass
+class MomentGroup:
+    targets: np.ndarray          # (B,)
+    beta_s: np.ndarray           # (2, B, n_c, n_c)
+    beta_d: np.ndarray           # (2, B, n_c, n_c)
+
+
+@dataclass
+class SingularMomentTable:
+    n_c: int
+    kappas: tuple
+    groups: dict = field(default_factory=dict)
+    corrections: object = None
+
+
+def compute_moments(disc: SurfaceDiscretization, smap: SingularityMap,
+                    config: SingularQuadratureConfig, kappas,
+                    target_points=None, target_normals=None):
+    """Integrals of G * T_m(u) T_n(v) * J (and of dG/dn_x) per singular pair
+    on the graded grid clustered at the pair's closest point."""
+    kappas = tuple(kappas)
+    n_c = disc.n_c
+    nb = config.resolve_n_beta(n_c)
+    base = cheb.nodes(nb)
+    wb = cheb.fejer(nb)
+    pts = disc.points if target_points is None else target_points
+    nrms = disc.normals if target_normals is None else target_normals
+    table = SingularMomentTable(n_c, kappas)
+    for p in np.unique(smap.patch_ids):
+        patch = disc.patches[p]
+        tg, u0, v0 = smap.pairs_for_patch(int(p))
+        b = tg.size
+        xu, dxu = clustered_nodes(u0, base, config.d)
+        xv, dxv = clustered_nodes(v0, base, config.d)
+        tu = cheb.basis(patch.n, xu.ravel()).reshape(b, nb, patch.n)
+        tv = cheb.basis(patch.n, xv.ravel()).reshape(b, nb, patch.n)
+        tvt = tv.transpose(0, 2, 1)
+
+        def on_grid(cf):
+            return np.stack([tu @ cf[c] @ tvt for c in range(3)])
+
+        pos = on_grid(patch.coeffs)
+        eu = on_grid(patch.coeffs_du)
+        ev = on_grid(patch.coeffs_dv)
+        jac = np.linalg.norm(np.cross(np.moveaxis(eu, 0, -1),
+                                      np.moveaxis(ev, 0, -1)), axis=-1)
+        dx = pts[tg].T[:, :, None, None] - pos
+        r = np.sqrt((dx**2).sum(axis=0))
+        ndx = np.einsum("cbij,bc->bij", dx, nrms[tg])
+        pu = cheb.basis(n_c, xu.ravel()).reshape(b, nb, n_c)
+        pv = cheb.basis(n_c, xv.ravel()).reshape(b, nb, n_c)
+        put = (pu * (dxu * wb)[:, :, None]).transpose(0, 2, 1).copy()
+        pvw = (pv * (dxv * wb)[:, :, None]).copy()
+        bs = np.empty((2, b, n_c, n_c), dtype=complex)
+        bd = np.empty((2, b, n_c, n_c), dtype=complex)
+        for k, kappa in enumerate(kappas):
+            phase = np.exp(1j * kappa * r) / (4.0 * np.pi * r)
+            ks = phase * jac
+            kd = ks * (ndx * (1j * kappa * r - 1.0) / r**2)
+            bs[k] = (put.astype(complex) @ ks) @ pvw
+            bd[k] = (put.astype(complex) @ kd) @ pvw
+        table.groups[int(p)] = MomentGroup(tg, bs, bd)
+    return table
+
+
+@dataclass
+class CorrectionPairs:
+    """(target, source) pairs the far field double counts (sources on a
+    target's singular patch lying >= 2 finest boxes away)."""
+
+    ell_idx: np.ndarray
+    src_idx: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return self.ell_idx.size
+
+
+def correction_pairs(disc: SurfaceDiscretization, tree,
+                     smap: SingularityMap) -> CorrectionPairs:
+    coords = tree.point_level_coords(tree.depth)
+    n2 = disc.n_c**2
+    ells, srcs = [], []
+    for p in sorted({int(q) for q in smap.patch_ids}):
+        tg, _, _ = smap.pairs_for_patch(p)
+        s0 = p * n2
+        sep = np.abs(coords[s0:s0 + n2][None, :, :] -
+                     coords[tg][:, None, :]).max(-1)
+        ti, si = np.nonzero(sep >= 2)
+        ells.append(tg[ti])
+        srcs.append((s0 + si).astype(np.int64))
+    ell = np.concatenate(ells) if ells else np.empty(0, dtype=np.int64)
+    src = np.concatenate(srcs) if srcs else np.empty(0, dtype=np.int64)
+    return CorrectionPairs(ell, src)

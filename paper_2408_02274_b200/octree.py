@@ -1,0 +1,674 @@
+"""IFGF plan: linear octree, cone-segment hierarchy, propagation types and
+emission geometry (host, plan time; vectorised numpy).
+
+Every integer the device consumes (Morton codes, neighbour/cousin lists,
+relevant segment ids, accumulation sigma/rows, emission segment rows) is
+produced here with the *same floating-point expressions* the reference uses,
+so it is bit-identical to the reference plan on the same host (checked by
+``tests/test_plan_vs_reference.py`` against golden digests):
+
+* Morton codes                 -- reference ``ifgf.py:70-102``
+* ``build_box_tree``           -- reference ``ifgf.py:176-277``
+* ``cone_coords``              -- reference ``ifgf.py:305-317``
+* ``ConeLevel``                -- reference ``ifgf.py:324-387``
+* ``build_cone_hierarchy``     -- reference ``ifgf.py:417-482``
+* ``accumulation_plan``        -- reference ``ifgf.py:676-749`` (_AccumType,
+  _accum_types) regrouped per parent segment for owner-computes on device
+* ``emission_plan``            -- reference ``ifgf.py:630-673`` geometry part
+  (segment row, local coordinates, radii of x and x + h n)
+
+Unlike the reference (Python loops over boxes and types), every stage here
+is a handful of whole-level array operations.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import cheb
+
+__all__ = ["ETA", "IfgfConfig", "BoxTree", "LevelBoxes", "ConeLevel",
+           "ConeHierarchy", "morton_encode", "morton_decode",
+           "build_box_tree", "build_cone_hierarchy", "cone_coords",
+           "accumulation_plan", "emission_plan", "tree_stats"]
+
+ETA = np.sqrt(3.0) / 3.0
+
+
+@dataclass(frozen=True)
+class IfgfConfig:
+    """Interpolation orders and cone seeds (reference ``ifgf.py:49-63``)."""
+
+    p_s: int = 3
+    p_a: int = 5
+    n_s_seed: int = 1
+    n_a_seed: int = 2
+    mode: str = "vec"
+
+    def __post_init__(self):
+        if self.p_s < 2 or self.p_a < 2:
+            raise ValueError("interpolation orders must be >= 2")
+        if self.mode not in ("vec", "seq"):
+            raise ValueError("mode must be 'vec' or 'seq'")
+
+    @property
+    def n_nodes(self) -> int:
+        return self.p_s * self.p_a * self.p_a
+
+
+# ---------------------------------------------------------------------------
+# Morton codes (x -> bit 2, y -> bit 1, z -> bit 0; 21 bits per axis)
+# ---------------------------------------------------------------------------
+
+_SPREAD = ((32, 0x1F00000000FFFF), (16, 0x1F0000FF0000FF),
+           (8, 0x100F00F00F00F00F), (4, 0x10C30C30C30C30C3),
+           (2, 0x1249249249249249))
+
+
+def _spread3(x):
+    x = np.asarray(x).astype(np.uint64) & np.uint64(0x1FFFFF)
+    for sh, mask in _SPREAD:
+        x = (x | (x << np.uint64(sh))) & np.uint64(mask)
+    return x
+
+
+def _gather3(x):
+    x = np.asarray(x).astype(np.uint64) & np.uint64(0x1249249249249249)
+    for sh, mask in ((2, 0x10C30C30C30C30C3), (4, 0x100F00F00F00F00F),
+                     (8, 0x1F0000FF0000FF), (16, 0x1F00000000FFFF),
+                     (32, 0x1FFFFF)):
+        x = (x | (x >> np.uint64(sh))) & np.uint64(mask)
+    return x
+
+
+def morton_encode(coords) -> np.ndarray:
+    c = np.asarray(coords, dtype=np.uint64)
+    return ((_spread3(c[..., 0]) << np.uint64(2)) |
+            (_spread3(c[..., 1]) << np.uint64(1)) | _spread3(c[..., 2]))
+
+
+def morton_decode(codes) -> np.ndarray:
+    codes = np.asarray(codes, dtype=np.uint64)
+    return np.stack([_gather3(codes >> np.uint64(2)),
+                     _gather3(codes >> np.uint64(1)),
+                     _gather3(codes)], axis=-1).astype(np.int64)
+
+
+# ---------------------------------------------------------------------------
+# CSR helpers
+# ---------------------------------------------------------------------------
+
+def _expand_ranges(lo: np.ndarray, hi: np.ndarray):
+    """Concatenate [lo_i, hi_i) ranges -> (values, owner index i)."""
+    lo = np.asarray(lo, dtype=np.int64)
+    cnt = np.asarray(hi, dtype=np.int64) - lo
+    owner = np.repeat(np.arange(lo.size, dtype=np.int64), cnt)
+    if owner.size == 0:
+        return np.empty(0, np.int64), owner
+    starts = np.cumsum(cnt) - cnt
+    vals = np.arange(owner.size, dtype=np.int64) - starts[owner] + lo[owner]
+    return vals, owner
+
+
+def _offsets_from_owner(owner: np.ndarray, n: int) -> np.ndarray:
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(owner, minlength=n), out=off[1:])
+    return off
+
+
+# ---------------------------------------------------------------------------
+# box tree
+# ---------------------------------------------------------------------------
+
+@dataclass
+class LevelBoxes:
+    level: int
+    side: float
+    codes: np.ndarray
+    coords: np.ndarray
+    centers: np.ndarray
+    pt_start: np.ndarray
+    pt_count: np.ndarray
+    parent: np.ndarray
+    child_start: np.ndarray
+    child_end: np.ndarray
+    nbr_idx: np.ndarray
+    nbr_off: np.ndarray
+    cousin_idx: np.ndarray
+    cousin_off: np.ndarray
+
+    @property
+    def n_boxes(self) -> int:
+        return self.codes.size
+
+    def neighbors(self, b: int) -> np.ndarray:
+        return self.nbr_idx[self.nbr_off[b]:self.nbr_off[b + 1]]
+
+    def cousins(self, b: int) -> np.ndarray:
+        return self.cousin_idx[self.cousin_off[b]:self.cousin_off[b + 1]]
+
+
+@dataclass
+class BoxTree:
+    origin: np.ndarray
+    root_side: float
+    depth: int
+    kappa_max: float
+    perm: np.ndarray
+    iperm: np.ndarray
+    points: np.ndarray
+    point_codes: np.ndarray
+    levels: list = field(default_factory=list)
+
+    def level(self, d: int) -> LevelBoxes:
+        return self.levels[d - 1]
+
+    def side(self, d: int) -> float:
+        return self.root_side / 2 ** (d - 1)
+
+    def point_level_codes(self, d: int) -> np.ndarray:
+        return self.point_codes >> np.uint64(3 * (self.depth - d))
+
+    def point_level_coords(self, d: int) -> np.ndarray:
+        return morton_decode(self.point_level_codes(d))[self.iperm]
+
+    def point_boxes(self, d: int) -> np.ndarray:
+        return np.searchsorted(self.level(d).codes, self.point_level_codes(d))
+
+    def box_points(self, d: int, b: int) -> np.ndarray:
+        lvl = self.level(d)
+        return np.arange(lvl.pt_start[b], lvl.pt_start[b] + lvl.pt_count[b])
+
+
+_STENCIL = np.array(np.meshgrid(*[[-1, 0, 1]] * 3, indexing="ij")
+                    ).reshape(3, -1).T
+
+
+def build_box_tree(points, kappa_max: float, padding: float = 0.01) -> BoxTree:
+    """Octree over the points; depth minimal with finest side <= lambda/4."""
+    pts = np.atleast_2d(np.asarray(points, dtype=float))
+    if pts.shape[0] == 0:
+        raise ValueError("empty point set")
+    kappa_max = float(abs(kappa_max))
+    lo, hi = pts.min(axis=0), pts.max(axis=0)
+    extent = max((hi - lo).max(), 1e-300)
+    side = extent * (1.0 + padding)
+    origin = 0.5 * (lo + hi) - side / 2.0
+    quarter = 0.25 * (2 * np.pi / kappa_max) if kappa_max > 0 else np.inf
+    depth = 1
+    while side / 2 ** (depth - 1) > quarter:
+        depth += 1
+    h_fine = side / 2 ** (depth - 1)
+    cells = np.clip(((pts - origin) / h_fine).astype(np.int64), 0,
+                    2 ** (depth - 1) - 1)
+    codes = morton_encode(cells)
+    perm = np.argsort(codes, kind="stable")
+    iperm = np.empty_like(perm)
+    iperm[perm] = np.arange(perm.size)
+    tree = BoxTree(origin, side, depth, kappa_max, perm, iperm, pts[perm],
+                   codes[perm])
+    for d in range(1, depth + 1):
+        pc = tree.point_level_codes(d)
+        bcodes, starts, counts = np.unique(pc, return_index=True,
+                                           return_counts=True)
+        coords = morton_decode(bcodes)
+        h = tree.side(d)
+        nb = bcodes.size
+        cand = coords[:, None, :] + _STENCIL[None, :, :]
+        valid = np.all((cand >= 0) & (cand < 2 ** (d - 1)), axis=-1)
+        ccodes = morton_encode(np.clip(cand, 0, None))
+        pos = np.minimum(np.searchsorted(bcodes, ccodes), nb - 1)
+        hit = valid & (bcodes[pos] == ccodes)
+        nbr_off = np.zeros(nb + 1, dtype=np.int64)
+        nbr_off[1:] = np.cumsum(hit.sum(axis=1))
+        if d == 1:
+            parent = np.full(nb, -1, dtype=np.int64)
+        else:
+            up = tree.level(d - 1)
+            shifted = bcodes >> np.uint64(3)
+            parent = np.searchsorted(up.codes, shifted)
+            up.child_start = np.searchsorted(shifted, up.codes, side="left")
+            up.child_end = np.searchsorted(shifted, up.codes, side="right")
+        tree.levels.append(LevelBoxes(
+            level=d, side=h, codes=bcodes, coords=coords,
+            centers=origin + (coords + 0.5) * h, pt_start=starts,
+            pt_count=counts, parent=parent,
+            child_start=np.zeros(nb, dtype=np.int64),
+            child_end=np.zeros(nb, dtype=np.int64),
+            nbr_idx=pos[hit], nbr_off=nbr_off,
+            cousin_idx=np.empty(0, dtype=np.int64),
+            cousin_off=np.zeros(nb + 1, dtype=np.int64)))
+    # cousins: children of the parent's neighbours that are not neighbours
+    # (sorted ascending per box)
+    for d in range(2, depth + 1):
+        lvl, up = tree.level(d), tree.level(d - 1)
+        pn, owner = _expand_ranges(up.nbr_off[lvl.parent],
+                                   up.nbr_off[lvl.parent + 1])
+        pn = up.nbr_idx[pn]
+        kids, k_own = _expand_ranges(up.child_start[pn], up.child_end[pn])
+        box = owner[k_own]
+        far = np.abs(lvl.coords[kids] - lvl.coords[box]).max(axis=1) >= 2
+        kids, box = kids[far], box[far]
+        order = np.lexsort((kids, box))
+        lvl.cousin_idx = kids[order]
+        lvl.cousin_off = _offsets_from_owner(box, lvl.n_boxes)
+    return tree
+
+
+# ---------------------------------------------------------------------------
+# cone coordinates and levels
+# ---------------------------------------------------------------------------
+
+def _norm3(dx: np.ndarray) -> np.ndarray:
+    return np.linalg.norm(dx, axis=-1)
+
+
+def cone_coords(x, x_center, side):
+    """(s, theta, phi, r) about a box centre; s = (sqrt(3)/2 side) / r."""
+    dx = np.atleast_2d(np.asarray(x, float) - np.asarray(x_center, float))
+    r = _norm3(dx)
+    if np.any(r == 0.0):
+        raise ValueError("point coincides with the box center")
+    s = np.sqrt(3.0) / 2.0 * side / r
+    theta = np.arccos(np.clip(dx[:, 2] / r, -1.0, 1.0))
+    phi = np.mod(np.arctan2(dx[:, 1], dx[:, 0]), 2.0 * np.pi)
+    return s, theta, phi, r
+
+
+def _cell_nodes(p: int, count: int, width: float) -> np.ndarray:
+    lo = np.arange(count) * width
+    return lo[:, None] + (cheb.nodes(p)[None, :] + 1.0) * 0.5 * width
+
+
+@dataclass
+class ConeLevel:
+    level: int
+    n_s: int
+    n_a: int
+    delta_s: float
+    delta_a: float
+    h: float
+    s_nodes: np.ndarray
+    ang_nodes_t: np.ndarray
+    ang_nodes_p: np.ndarray
+    seg_ids: np.ndarray
+    seg_off: np.ndarray
+    cpt_idx: np.ndarray
+    cpt_off: np.ndarray
+
+    @property
+    def n_segments(self) -> int:
+        return self.seg_ids.size
+
+    @property
+    def id_stride(self) -> int:
+        return self.n_s * self.n_a * 2 * self.n_a + 1
+
+    def segs_of(self, b: int) -> np.ndarray:
+        return self.seg_ids[self.seg_off[b]:self.seg_off[b + 1]]
+
+    def seg_index(self, s, theta, phi) -> np.ndarray:
+        i_s = np.minimum((s / self.delta_s).astype(np.int64), self.n_s - 1)
+        i_t = np.minimum((theta / self.delta_a).astype(np.int64),
+                         self.n_a - 1)
+        i_p = np.minimum((phi / self.delta_a).astype(np.int64),
+                         2 * self.n_a - 1)
+        return (i_s * self.n_a + i_t) * (2 * self.n_a) + i_p
+
+    def seg_unpack(self, flat):
+        i_p = flat % (2 * self.n_a)
+        rest = flat // (2 * self.n_a)
+        return rest // self.n_a, rest % self.n_a, i_p
+
+    def local_coords(self, flat, s, theta, phi):
+        i_s, i_t, i_p = self.seg_unpack(flat)
+        return (2.0 * (s / self.delta_s - i_s) - 1.0,
+                2.0 * (theta / self.delta_a - i_t) - 1.0,
+                2.0 * (phi / self.delta_a - i_p) - 1.0)
+
+    def node_directions(self, flat):
+        """Per segment: radii (nseg, p_s) and unit directions
+        (nseg, p_a, p_a, 3) of its interpolation nodes."""
+        i_s, i_t, i_p = self.seg_unpack(flat)
+        r = self.h / self.s_nodes[i_s]
+        th = self.ang_nodes_t[i_t]
+        ph = self.ang_nodes_p[i_p]
+        st, ct = np.sin(th), np.cos(th)
+        cp, sp = np.cos(ph), np.sin(ph)
+        dirs = np.stack([st[:, :, None] * cp[:, None, :],
+                         st[:, :, None] * sp[:, None, :],
+                         np.broadcast_to(ct[:, :, None],
+                                         (flat.size, th.shape[1],
+                                          ph.shape[1]))], axis=-1)
+        return r, dirs
+
+    def segment_nodes_xyz(self, flat, center):
+        """Cartesian nodes (nseg, p_s*p_a*p_a, 3) = center + r * dir, and
+        node radii; ``center`` may be (3,) or per segment (nseg, 3)."""
+        flat = np.asarray(flat, dtype=np.int64)
+        r, dirs = self.node_directions(flat)
+        c = np.asarray(center, dtype=float)
+        if c.ndim == 2:
+            c = c[:, None, None, None, :]
+        xyz = c + r[:, :, None, None, None] * dirs[:, None]
+        rr = np.broadcast_to(r[:, :, None, None],
+                             xyz.shape[:-1]).reshape(flat.size, -1)
+        return xyz.reshape(flat.size, -1, 3), rr
+
+    def box_keys(self) -> np.ndarray:
+        """Globally sorted (box, segment id) keys, one per segment row."""
+        nb = self.seg_off.size - 1
+        return (np.repeat(np.arange(nb, dtype=np.int64),
+                          np.diff(self.seg_off)) * np.int64(self.id_stride)
+                + self.seg_ids)
+
+
+@dataclass
+class ConeHierarchy:
+    config: IfgfConfig
+    kappa_max: float
+    cone_levels: dict
+    _accum_cache: dict = field(default_factory=dict)
+    _emit_cache: dict = field(default_factory=dict)
+
+    def level(self, d: int) -> ConeLevel:
+        return self.cone_levels[d]
+
+    def spectra_bytes(self, n_channels: int) -> int:
+        sizes = sorted((cl.n_segments for cl in self.cone_levels.values()),
+                       reverse=True)
+        return sum(sizes[:2]) * self.config.n_nodes * n_channels * 16
+
+
+def cone_counts(tree: BoxTree, config: IfgfConfig) -> dict:
+    """(n_s, n_a) per level; doubles going coarser wherever kappa*H_d > 1/2."""
+    out = {}
+    n_s, n_a = config.n_s_seed, config.n_a_seed
+    for d in range(tree.depth, 2, -1):
+        if tree.kappa_max * tree.side(d) > 0.5:
+            n_s, n_a = 2 * n_s, 2 * n_a
+        out[d] = (n_s, n_a)
+    return out
+
+
+def _cousin_points(tree: BoxTree, d: int):
+    """CSR of the cousin points (tree order) of every box at level d."""
+    lvl = tree.level(d)
+    cz, owner = _expand_ranges(lvl.cousin_off[:-1], lvl.cousin_off[1:])
+    cz = lvl.cousin_idx[cz]
+    pts, p_own = _expand_ranges(lvl.pt_start[cz],
+                                lvl.pt_start[cz] + lvl.pt_count[cz])
+    box = owner[p_own]
+    return pts, _offsets_from_owner(box, lvl.n_boxes), box
+
+
+def _chunks(off: np.ndarray, budget: int):
+    """Split box ranges so that each chunk holds <= budget items."""
+    nb = off.size - 1
+    b = 0
+    while b < nb:
+        e = int(np.searchsorted(off, off[b] + budget, side="right")) - 1
+        e = max(e, b + 1)
+        e = min(e, nb)
+        yield b, e
+        b = e
+
+
+def build_cone_hierarchy(tree: BoxTree,
+                         config: IfgfConfig = IfgfConfig()) -> ConeHierarchy:
+    """Relevant segments per box: those holding a cousin point or a node of a
+    relevant parent segment (sorted per box)."""
+    counts = cone_counts(tree, config)
+    hier = ConeHierarchy(config, tree.kappa_max, {})
+    nn = config.n_nodes
+    for d in range(3, tree.depth + 1):
+        n_s, n_a = counts[d]
+        lvl = tree.level(d)
+        cl = ConeLevel(
+            level=d, n_s=n_s, n_a=n_a, delta_s=ETA / n_s,
+            delta_a=np.pi / n_a, h=np.sqrt(3.0) / 2.0 * lvl.side,
+            s_nodes=_cell_nodes(config.p_s, n_s, ETA / n_s),
+            ang_nodes_t=_cell_nodes(config.p_a, n_a, np.pi / n_a),
+            ang_nodes_p=_cell_nodes(config.p_a, 2 * n_a, np.pi / n_a),
+            seg_ids=np.empty(0, dtype=np.int64),
+            seg_off=np.zeros(lvl.n_boxes + 1, dtype=np.int64),
+            cpt_idx=np.empty(0, dtype=np.int64),
+            cpt_off=np.zeros(lvl.n_boxes + 1, dtype=np.int64))
+        stride = np.int64(cl.id_stride)
+        cpts, cpt_off, cbox = _cousin_points(tree, d)
+        cl.cpt_idx, cl.cpt_off = cpts, cpt_off
+        keys = []
+        if cpts.size:
+            s, th, ph, _ = cone_coords(tree.points[cpts], lvl.centers[cbox],
+                                       lvl.side)
+            keys.append(cbox * stride + cl.seg_index(s, th, ph))
+        pcl = hier.cone_levels.get(d - 1)
+        if pcl is not None:
+            up = tree.level(d - 1)
+            # parent segment rows of every child box
+            prow_off = pcl.seg_off[lvl.parent]
+            prow_end = pcl.seg_off[lvl.parent + 1]
+            inst_off = np.zeros(lvl.n_boxes + 1, dtype=np.int64)
+            np.cumsum(prow_end - prow_off, out=inst_off[1:])
+            pbox_of_row = np.repeat(np.arange(up.n_boxes),
+                                    np.diff(pcl.seg_off))
+            budget = max(1, 4_000_000 // nn)
+            for b0, b1 in _chunks(inst_off, budget):
+                rows, own = _expand_ranges(prow_off[b0:b1], prow_end[b0:b1])
+                if rows.size == 0:
+                    continue
+                xyz, _ = pcl.segment_nodes_xyz(
+                    pcl.seg_ids[rows], up.centers[pbox_of_row[rows]])
+                box = own + b0
+                dx = xyz - lvl.centers[box][:, None, :]
+                s, th, ph, _ = cone_coords(dx.reshape(-1, 3), np.zeros(3),
+                                           lvl.side)
+                keys.append(np.repeat(box, nn) * stride +
+                            cl.seg_index(s, th, ph))
+        if keys:
+            uk = np.unique(np.concatenate(keys))
+            box = uk // stride
+            cl.seg_ids = uk - box * stride
+            cl.seg_off = _offsets_from_owner(box, lvl.n_boxes)
+        hier.cone_levels[d] = cl
+    return hier
+
+
+# ---------------------------------------------------------------------------
+# propagation plan (child level d -> parent level d-1)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class AccumulationPlan:
+    """Types (parent segment id, child octant) with shared child-frame
+    geometry, and instances regrouped per parent segment row.
+
+    Per type t (nodes sorted by child segment, as the reference's
+    ``_AccumType``): ``sig_off[t]:sig_off[t+1]`` child segment groups, group
+    g covering sorted node slots ``bounds[g]:bounds[g+1]`` (local to the
+    type); ``scatter[t, j]`` = parent node slot of sorted node j;
+    ``xs/xt/xp[t, j]`` = local coordinates in the child segment;
+    ``r_parent/r_child[t, j]`` = node radius about parent / child centre.
+
+    Instances (one per (parent segment row, child box)) sorted by parent
+    row then child box: ``inst_off`` (per parent row), ``inst_type``,
+    ``inst_child``, ``inst_crow_off`` into ``crow`` (child segment row per
+    sigma group of the type).
+    """
+
+    level: int
+    n_types: int
+    type_gamma: np.ndarray
+    type_octant: np.ndarray
+    sig_off: np.ndarray
+    group_bounds: np.ndarray      # flat, per group: start slot (len n_groups)
+    group_end: np.ndarray
+    scatter: np.ndarray
+    xs: np.ndarray
+    xt: np.ndarray
+    xp: np.ndarray
+    r_parent: np.ndarray
+    r_child: np.ndarray
+    inst_off: np.ndarray
+    inst_type: np.ndarray
+    inst_child: np.ndarray
+    inst_crow_off: np.ndarray
+    crow: np.ndarray
+    crow_misses: int = 0
+
+    @property
+    def n_instances(self) -> int:
+        return self.inst_type.size
+
+
+def _type_geometry(pcl: ConeLevel, cl: ConeLevel, gamma, octant, child_side):
+    """Vectorised reference ``_AccumType.__init__`` (ifgf.py:686-702)."""
+    n_t = gamma.size
+    bits = np.stack([(octant >> 2) & 1, (octant >> 1) & 1, octant & 1],
+                    axis=-1)
+    offset = 0.5 * child_side * (bits * 2.0 - 1.0)
+    xyz, rp = pcl.segment_nodes_xyz(gamma, -offset)
+    nn = xyz.shape[1]
+    s, th, ph, rc = cone_coords(xyz.reshape(-1, 3), np.zeros(3), child_side)
+    flat = cl.seg_index(s, th, ph).reshape(n_t, nn)
+    order = np.argsort(flat, axis=1, kind="stable")
+    fs = np.take_along_axis(flat, order, axis=1)
+    take = lambda a: np.take_along_axis(a.reshape(n_t, nn), order, axis=1)
+    xs, xt, xp = cl.local_coords(fs, take(s), take(th), take(ph))
+    return fs, order, xs, xt, xp, take(rp), take(rc)
+
+
+def accumulation_plan(tree: BoxTree, hier: ConeHierarchy,
+                      d: int) -> AccumulationPlan:
+    """Plan for folding level-d child interpolants into level d-1."""
+    cache = hier._accum_cache
+    if d in cache:
+        return cache[d]
+    cl, pcl = hier.level(d), hier.level(d - 1)
+    lvl = tree.level(d)
+    nn = hier.config.n_nodes
+    octant = (lvl.codes & np.uint64(7)).astype(np.int64)
+    prow, child = _expand_ranges(pcl.seg_off[lvl.parent],
+                                 pcl.seg_off[lvl.parent + 1])
+    key = pcl.seg_ids[prow] * 8 + octant[child]
+    ukeys, inst_type = np.unique(key, return_inverse=True)
+    inst_type = inst_type.astype(np.int64)
+    gamma, toct = ukeys >> 3, ukeys & 7
+    n_t = ukeys.size
+    fs_all = np.empty((n_t, nn), dtype=np.int64)
+    order_all = np.empty((n_t, nn), dtype=np.int64)
+    geo = {k: np.empty((n_t, nn)) for k in ("xs", "xt", "xp", "rp", "rc")}
+    step = max(1, 2_000_000 // nn)
+    for t0 in range(0, n_t, step):
+        t1 = min(n_t, t0 + step)
+        fs, order, xs, xt, xp, rp, rc = _type_geometry(
+            pcl, cl, gamma[t0:t1], toct[t0:t1], lvl.side)
+        fs_all[t0:t1], order_all[t0:t1] = fs, order
+        for k, v in zip(("xs", "xt", "xp", "rp", "rc"), (xs, xt, xp, rp, rc)):
+            geo[k][t0:t1] = v
+    # sigma groups per type
+    newgrp = np.ones((n_t, nn), dtype=bool)
+    newgrp[:, 1:] = fs_all[:, 1:] != fs_all[:, :-1]
+    g_type, g_start = np.nonzero(newgrp)
+    n_groups = g_type.size
+    sig_off = _offsets_from_owner(g_type, n_t)
+    g_end = np.empty(n_groups, dtype=np.int64)
+    g_end[:-1] = g_start[1:]
+    last = sig_off[1:] - 1
+    g_end[last] = nn
+    g_sigma = fs_all[g_type, g_start]
+    # instances sorted by (parent row, child): prow/child are generated
+    # child-major, so re-sort
+    order = np.lexsort((child, prow))
+    prow, child, inst_type = prow[order], child[order], inst_type[order]
+    nsig = np.diff(sig_off)[inst_type]
+    crow_off = np.zeros(prow.size + 1, dtype=np.int64)
+    np.cumsum(nsig, out=crow_off[1:])
+    gidx, g_own = _expand_ranges(sig_off[inst_type], sig_off[inst_type + 1])
+    box_keys = cl.box_keys()
+    want = child[g_own] * np.int64(cl.id_stride) + g_sigma[gidx]
+    crow = np.searchsorted(box_keys, want).astype(np.int64)
+    misses = int(np.count_nonzero(
+        box_keys[np.minimum(crow, box_keys.size - 1)] != want))
+    plan = AccumulationPlan(
+        level=d, n_types=n_t, type_gamma=gamma, type_octant=toct,
+        sig_off=sig_off, group_bounds=g_start, group_end=g_end,
+        scatter=order_all, xs=geo["xs"], xt=geo["xt"], xp=geo["xp"],
+        r_parent=geo["rp"], r_child=geo["rc"],
+        inst_off=_offsets_from_owner(prow, pcl.n_segments),
+        inst_type=inst_type, inst_child=child, inst_crow_off=crow_off,
+        crow=crow, crow_misses=misses)
+    cache[d] = plan
+    return plan
+
+
+# ---------------------------------------------------------------------------
+# emission plan (level d boxes -> their cousin points)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class EmissionPlan:
+    """One entry per (box, cousin point) pair, box-major as ``cpt_idx``:
+    segment row, target (tree order) and local coordinates / radius of the
+    target and of its displaced copy (same segment, reference ifgf.py:651)."""
+
+    level: int
+    row: np.ndarray
+    target: np.ndarray
+    geom: np.ndarray              # (n_pairs, 4): xs, xt, xp, r
+    geom_disp: np.ndarray | None  # (n_pairs, 4) or None
+    row_misses: int = 0
+
+    @property
+    def n_pairs(self) -> int:
+        return self.row.size
+
+
+def emission_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
+                  disp_points_t: np.ndarray | None = None) -> EmissionPlan:
+    cl, lvl = hier.level(d), tree.level(d)
+    tg = cl.cpt_idx
+    box = np.repeat(np.arange(lvl.n_boxes, dtype=np.int64),
+                    np.diff(cl.cpt_off))
+    ctr = lvl.centers[box]
+    if tg.size == 0:
+        z = np.empty((0, 4))
+        return EmissionPlan(d, np.empty(0, np.int64), tg, z,
+                            None if disp_points_t is None else z)
+    s, th, ph, r = cone_coords(tree.points[tg] - ctr, np.zeros(3), lvl.side)
+    flat = cl.seg_index(s, th, ph)
+    want = box * np.int64(cl.id_stride) + flat
+    keys = cl.box_keys()
+    row = np.searchsorted(keys, want).astype(np.int64)
+    misses = int(np.count_nonzero(keys[np.minimum(row, keys.size - 1)]
+                                  != want))
+    geom = np.stack(cl.local_coords(flat, s, th, ph) + (r,), axis=1)
+    gd = None
+    if disp_points_t is not None:
+        sd, td, pd, rd = cone_coords(disp_points_t[tg] - ctr, np.zeros(3),
+                                     lvl.side)
+        gd = np.stack(cl.local_coords(flat, sd, td, pd) + (rd,), axis=1)
+    return EmissionPlan(d, row, tg, geom, gd, misses)
+
+
+def tree_stats(tree: BoxTree, hier: ConeHierarchy | None = None) -> str:
+    """JSON per-level box/segment counts (reference ifgf.py:926-950)."""
+    rows = []
+    for d in range(1, tree.depth + 1):
+        lvl = tree.level(d)
+        row = {"level": d, "side": lvl.side,
+               "relevant_boxes": int(lvl.n_boxes),
+               "max_points_per_box": int(lvl.pt_count.max())}
+        if hier is not None and d in hier.cone_levels:
+            cl = hier.level(d)
+            row["cone_counts"] = [cl.n_s, cl.n_a]
+            row["relevant_segments"] = int(cl.n_segments)
+        rows.append(row)
+    payload = {"depth": tree.depth, "root_side": tree.root_side,
+               "points": int(tree.points.shape[0]), "levels": rows}
+    if hier is not None:
+        payload["spectra_bytes_vec16"] = hier.spectra_bytes(16)
+    return json.dumps(payload, indent=2)

@@ -1,0 +1,210 @@
+"""Generate golden fixtures from the UNMODIFIED reference (`emscat`, imported
+read-only from /root/reference/pkg/src).  Runs only in the build container;
+the committed .npz outputs travel to the GPU hosts.
+
+Usage:  python tests/golden/make_golden.py [s1] [c1] [c1gmres] [rand]
+
+Fixtures (complex arrays stored as complex128):
+  <name>.npz
+    plan_digest_*   sha256 of every plan integer array (tree, cones,
+                    accumulation types, emission rows, singular map,
+                    correction lists) -- see plan_digests()
+    y               matvec input, Re/Im iid N(0,1) from default_rng(0)
+    apply_y         MullerOperator.apply(y)            (operators.py:399)
+    weights         phi * disc.weights fed to ifgf_apply (operators.py:336)
+    far / far_disp  ifgf_apply(..., mode='vec', normals, 1e-6)  (ifgf.py:885)
+    far_seq_disp    same in 'seq' mode (reference's own noise floor)
+    s_val / d_val   potentials(dens)                   (operators.py:321)
+    floor_*         reference self-consistency floors (linearity, vec/seq)
+  c1_gmres.npz      GMRES tol 1e-6, plane wave exp(i k0 z) x-pol (cfg 1)
+  rand_ifgf.npz     ifgf_apply on random (2, N) weights, kappas (2pi, 3pi)
+"""
+
+from __future__ import annotations
+
+import hashlib
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = Path(__file__).resolve().parent
+
+CONFIGS = {
+    # name: (n_refine, n_c, k0 / pi, eps_r)
+    "s1": (1, 10, 2.0, 2.25),
+    "c1": (2, 10, 2.0, 2.25),
+}
+
+
+def _h(a) -> str:
+    a = np.ascontiguousarray(np.asarray(a))
+    return hashlib.sha256(a.tobytes()).hexdigest()[:32]
+
+
+def plan_digests(tree, hier, accum_types_fn, smap, corr_ell, corr_src,
+                 emission_rows_fn):
+    """Digest dict shared by the generator (reference objects) and the tests
+    (framework objects).  Integer arrays plus the float arrays that feed them
+    (centres, node grids) are hashed."""
+    out = {"depth": np.int64(tree.depth)}
+    out["perm"] = _h(tree.perm.astype(np.int64))
+    for d in range(1, tree.depth + 1):
+        lvl = tree.level(d)
+        for a in ("codes", "pt_start", "pt_count", "parent", "nbr_idx",
+                  "nbr_off", "cousin_idx", "cousin_off", "centers"):
+            v = getattr(lvl, a)
+            out[f"L{d}_{a}"] = _h(v.astype(np.float64 if a == "centers"
+                                           else np.int64))
+    for d in sorted(hier.cone_levels):
+        cl = hier.level(d)
+        for a in ("seg_ids", "seg_off", "cpt_idx", "cpt_off"):
+            out[f"C{d}_{a}"] = _h(getattr(cl, a).astype(np.int64))
+        out[f"C{d}_emit_rows"] = _h(emission_rows_fn(d).astype(np.int64))
+    for d in sorted(hier.cone_levels):
+        if d - 1 not in hier.cone_levels:
+            continue
+        sig, bnd, sc, child, prow, crow, geo = accum_types_fn(d)
+        for nm, v in (("sigma", sig), ("bounds", bnd), ("scatter", sc),
+                      ("inst_child", child), ("inst_prow", prow),
+                      ("inst_crow", crow)):
+            out[f"A{d}_{nm}"] = _h(v.astype(np.int64))
+        out[f"A{d}_geom"] = _h(geo.astype(np.float64))
+    out["smap_offsets"] = _h(smap.offsets.astype(np.int64))
+    out["smap_patch_ids"] = _h(smap.patch_ids.astype(np.int64))
+    out["corr_ell"] = _h(np.asarray(corr_ell, np.int64))
+    out["corr_src"] = _h(np.asarray(corr_src, np.int64))
+    return out
+
+
+def _ref_accum(ri, tree, hier):
+    def fn(d):
+        types = ri._accum_types(tree, hier, d)
+        cat = lambda f: np.concatenate([f(t).ravel() for t in types])
+        geo = np.concatenate([np.concatenate([t.xs, t.xt, t.xp, t.r_parent,
+                                              t.r_child]) for t in types])
+        return (cat(lambda t: t.sigma), cat(lambda t: t.bounds),
+                cat(lambda t: t.scatter_rows), cat(lambda t: t.inst_child),
+                cat(lambda t: t.inst_prow), cat(lambda t: t.inst_crow), geo)
+    return fn
+
+
+def _ref_emit_rows(ri, tree, hier):
+    def fn(d):
+        cl, lvl = hier.level(d), tree.level(d)
+        tg = cl.cpt_idx
+        box = np.repeat(np.arange(lvl.n_boxes), np.diff(cl.cpt_off))
+        s, th, ph, _ = ri.cone_coords(tree.points[tg] - lvl.centers[box],
+                                      np.zeros(3), lvl.side)
+        return ri._seg_row_lookup(cl, box, cl.seg_index(s, th, ph))
+    return fn
+
+
+def random_y(n: int, seed: int = 0) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    return rng.normal(size=4 * n) + 1j * rng.normal(size=4 * n)
+
+
+def build(name):
+    sys.path.insert(0, REF)
+    import emscat.geometry as rg
+    import emscat.ifgf as ri
+    from emscat.operators import (DensityBlock, MaterialPair,
+                                  build_muller_operator)
+    nr, nc, k0pi, eps = CONFIGS[name]
+    k0 = k0pi * np.pi
+    disc = rg.make_sphere_surface(nr, nc)
+    mats = MaterialPair(1.0, 1.0, eps, 1.0, k0)
+    t0 = time.time()
+    op = build_muller_operator(disc, mats)
+    print(name, "build", time.time() - t0, flush=True)
+    n = disc.n_points
+    y = random_y(n)
+    op.apply(y)                       # fill lazy caches
+    t0 = time.time()
+    ay = op.apply(y)
+    t_apply = time.time() - t0
+    print(name, "apply", t_apply, flush=True)
+    m, j = op.decode(y)
+    dens = DensityBlock.from_currents(disc, j, m)
+    w = dens.values * disc.weights
+    far, far_d = ri.ifgf_apply(op.tree, op.hierarchy, w, mats.kappas,
+                               mode="vec", displaced_normals=disc.normals,
+                               displaced_step=op.config.fd_step)
+    s_val, d_val = op.potentials(dens)
+    # reference noise floors
+    rng = np.random.default_rng(1)
+    y2 = rng.normal(size=4 * n) + 1j * rng.normal(size=4 * n)
+    lin = op.apply(0.7 * y - 1.3j * y2) - (0.7 * ay - 1.3j * op.apply(y2))
+    floor_lin = np.linalg.norm(lin) / np.linalg.norm(ay)
+    cs = op.moments.corrections
+    dig = plan_digests(op.tree, op.hierarchy, _ref_accum(ri, op.tree,
+                                                          op.hierarchy),
+                       op.smap, cs.ell_idx, cs.src_idx,
+                       _ref_emit_rows(ri, op.tree, op.hierarchy))
+    payload = dict(y=y, apply_y=ay, weights=w, far=far, far_disp=far_d,
+                   s_val=s_val, d_val=d_val, floor_linearity=floor_lin,
+                   t_apply_ref_container=t_apply,
+                   config=np.array([nr, nc, k0pi, eps]))
+    if name == "s1":
+        op.config = type(op.config)(fd_step=op.config.fd_step, mode="seq")
+        ay_seq = op.apply(y)
+        payload["floor_vec_seq_apply"] = (np.linalg.norm(ay_seq - ay) /
+                                          np.linalg.norm(ay))
+    for k, v in dig.items():
+        payload["plan_digest_" + k] = np.array(v)
+    np.savez_compressed(OUT / f"{name}.npz", **payload)
+    print(name, "floor_lin", floor_lin, flush=True)
+
+
+def build_gmres():
+    sys.path.insert(0, REF)
+    import emscat.geometry as rg
+    from emscat.operators import MaterialPair, build_muller_operator
+    from emscat.reference import plane_wave
+    from emscat.solver import gmres
+    disc = rg.make_sphere_surface(2, 10)
+    k0 = 2 * np.pi
+    mats = MaterialPair(1.0, 1.0, 2.25, 1.0, k0)
+    op = build_muller_operator(disc, mats)
+    b = op.rhs(plane_wave(k0, direction=(0.0, 0.0, 1.0),
+                          polarization=(1.0, 0.0, 0.0), omega=k0))
+    t0 = time.time()
+    x, rep = gmres(op.apply, b, tol=1e-6, max_iter=300)
+    np.savez_compressed(OUT / "c1_gmres.npz", b=b, x=x,
+                        residuals=np.array(rep.residuals),
+                        iterations=rep.iterations, wall=time.time() - t0)
+    print("gmres", rep.iterations, rep.residuals[-1], time.time() - t0)
+
+
+def build_rand():
+    sys.path.insert(0, REF)
+    import emscat.geometry as rg
+    import emscat.ifgf as ri
+    disc = rg.make_sphere_surface(1, 6)
+    kap = (2 * np.pi, 3 * np.pi)
+    tree = ri.build_box_tree(disc.points, max(kap))
+    hier = ri.build_cone_hierarchy(tree)
+    rng = np.random.default_rng(5)
+    w = rng.normal(size=(2, disc.n_points)) + 1j * rng.normal(
+        size=(2, disc.n_points))
+    out, out_d = ri.ifgf_apply(tree, hier, w, kap, mode="vec",
+                               displaced_normals=disc.normals,
+                               displaced_step=1e-6)
+    np.savez_compressed(OUT / "rand_ifgf.npz", weights=w, far=out,
+                        far_disp=out_d, kappas=np.array(kap),
+                        config=np.array([1, 6]))
+    print("rand done")
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["rand", "s1", "c1", "c1gmres"]
+    for w_ in which:
+        if w_ == "c1gmres":
+            build_gmres()
+        elif w_ == "rand":
+            build_rand()
+        else:
+            build(w_)
