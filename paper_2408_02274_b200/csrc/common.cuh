@@ -157,6 +157,38 @@ struct Plan {
   std::vector<void*> allocations;
 };
 
+template <typename T>
+inline int dev_upload(Plan& p, T** dst, const T* src, size_t n) {
+  *dst = nullptr;
+  if (n == 0) return IFGFB_OK;
+  void* ptr = nullptr;
+  IFGFB_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+  p.allocations.push_back(ptr);
+  p.bytes += n * sizeof(T);
+  if (src) IFGFB_CUDA(cudaMemcpy(ptr, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  *dst = static_cast<T*>(ptr);
+  return IFGFB_OK;
+}
+
+template <typename T>
+inline int dev_alloc(Plan& p, T** dst, size_t n) {
+  return dev_upload<T>(p, dst, nullptr, n);
+}
+
+#define IFGFB_CHECK_ARG(cond, msg) \
+  do {                             \
+    if (!(cond)) {                 \
+      ::ifgfb::set_error(msg);     \
+      return IFGFB_ERR_ARG;        \
+    }                              \
+  } while (0)
+
+#define IFGFB_RC(x)                  \
+  do {                               \
+    int rc_ = (x);                   \
+    if (rc_ != IFGFB_OK) return rc_; \
+  } while (0)
+
 int far_apply(Plan& p, const double* w, int nch, const double* kappas, int nk,
               double* out, double* out_disp, cudaStream_t st);
 int potentials(Plan& p, const double* phi, double* s_val, double* d_val,
@@ -164,3 +196,7 @@ int potentials(Plan& p, const double* phi, double* s_val, double* d_val,
 int muller_apply(Plan& p, const double* y, double* out, cudaStream_t st);
 
 }  // namespace ifgfb
+
+struct ifgfb_plan {
+  ifgfb::Plan p;
+};

@@ -1,0 +1,706 @@
+// N-Muller operator around the far field: density packing (K1), near field
+// (K6), surface assembly (K7), the apply driver and GMRES vector primitives.
+//
+// Reference: operators.py:230-245 (decode/encode), :121-128 + :148-189
+// (DensityBlock.from_currents, surface_divergence), :249-253 (_patch_coeffs),
+// :321-350 (potentials), :354-397 (apply_block), quadrature.py:343-360
+// (apply_singular_block), :457-487 (CorrectionSet), operators.py:279-319
+// (_neighbor_sums), solver.py:61-66 (GMRES vector ops).
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ifgfb {
+
+constexpr int MAXNC = 16;       // largest patch grid n_c supported on device
+
+struct SurfPtrs {
+  int n, n_c, n_patches;
+  const double* pts; const double* nrm; const double* wq; const double* jac;
+  const double* eu; const double* ev; const double* t1; const double* t2;
+  const double* dmat; const double* cmat;
+};
+
+__device__ __forceinline__ double2 cscale(double s, double2 a) {
+  return make_double2(s * a.x, s * a.y);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+
+// ---------------------------------------------------------------- K1 ----
+// One CTA per patch (n_c^2 threads): y -> (m, j) Cartesian, surface
+// divergences, phi (8,N), phi * weights (8,N) and per-patch Chebyshev
+// coefficient grids of phi (8,P,n_c,n_c).
+__global__ void pack_kernel(SurfPtrs s, const double2* __restrict__ y,
+                            const double2* __restrict__ phi_in,
+                            double2* __restrict__ phi, double2* __restrict__ phiw,
+                            double2* __restrict__ pcoef) {
+  extern __shared__ double2 sh[];
+  const int nc = s.n_c, n2 = nc * nc;
+  double2* gu = sh;            // 2 x n2 : J f^u for (j, m)
+  double2* gv = gu + 2 * n2;   // 2 x n2 : J f^v
+  double2* gp = gv + 2 * n2;   // 8 x n2 : phi grid
+  double2* gx = gp + 8 * n2;   // 8 x n2 : T @ phi
+  const int p = blockIdx.x, loc = threadIdx.x;
+  const int n = s.n;
+  const int ell = p * n2 + loc;
+  const bool act = loc < n2;
+  double2 J[3], M[3];
+  double e = 0, f = 0, g = 0, det = 1, jac = 1;
+  if (act && phi_in) {
+    // densities given directly (potentials(dens)): skip decode/divergence
+    const double wq = s.wq[ell];
+    for (int c = 0; c < 8; ++c) {
+      const double2 v = phi_in[(size_t)c * n + ell];
+      phi[(size_t)c * n + ell] = v;
+      phiw[(size_t)c * n + ell] = cscale(wq, v);
+      gp[c * n2 + loc] = v;
+    }
+  }
+  if (act && !phi_in) {
+    const double2 y1 = y[ell], y2 = y[n + ell], y3 = y[2 * n + ell], y4 = y[3 * n + ell];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double a = s.t1[3 * ell + c], b = s.t2[3 * ell + c];
+      M[c] = cadd(cscale(a, y1), cscale(b, y2));
+      J[c] = cadd(cscale(a, y3), cscale(b, y4));
+    }
+    const double* eu = s.eu + 3 * ell;
+    const double* ev = s.ev + 3 * ell;
+    e = eu[0] * eu[0] + eu[1] * eu[1] + eu[2] * eu[2];
+    f = eu[0] * ev[0] + eu[1] * ev[1] + eu[2] * ev[2];
+    g = ev[0] * ev[0] + ev[1] * ev[1] + ev[2] * ev[2];
+    det = e * g - f * f;
+    jac = s.jac[ell];
+    for (int q = 0; q < 2; ++q) {
+      const double2* V = q == 0 ? J : M;
+      double2 cu = make_double2(0, 0), cv = make_double2(0, 0);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        cu = cadd(cu, cscale(eu[c], V[c]));
+        cv = cadd(cv, cscale(ev[c], V[c]));
+      }
+      const double2 fu = cscale(1.0 / det, csub(cscale(g, cu), cscale(f, cv)));
+      const double2 fv = cscale(1.0 / det, csub(cscale(e, cv), cscale(f, cu)));
+      gu[q * n2 + loc] = cscale(jac, fu);
+      gv[q * n2 + loc] = cscale(jac, fv);
+    }
+  }
+  __syncthreads();
+  if (act && !phi_in) {
+    const int i = loc / nc, jj = loc % nc;
+    double2 div[2];
+    for (int q = 0; q < 2; ++q) {
+      double2 du = make_double2(0, 0), dv = make_double2(0, 0);
+      for (int k = 0; k < nc; ++k) {
+        du = cadd(du, cscale(s.dmat[i * nc + k], gu[q * n2 + k * nc + jj]));
+        dv = cadd(dv, cscale(s.dmat[jj * nc + k], gv[q * n2 + i * nc + k]));
+      }
+      div[q] = cscale(1.0 / jac, cadd(du, dv));
+    }
+    double2 vals[8] = {J[0], J[1], J[2], M[0], M[1], M[2], div[0], div[1]};
+    const double wq = s.wq[ell];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      phi[(size_t)c * n + ell] = vals[c];
+      phiw[(size_t)c * n + ell] = cscale(wq, vals[c]);
+      gp[c * n2 + loc] = vals[c];
+    }
+  }
+  __syncthreads();
+  // coefficient grids: X = T @ Phi, A = X @ T^T  (reference _patch_coeffs)
+  if (act) {
+    const int i = loc / nc, jj = loc % nc;
+    for (int c = 0; c < 8; ++c) {
+      double2 x = make_double2(0, 0);
+      for (int k = 0; k < nc; ++k) x = cadd(x, cscale(s.cmat[i * nc + k], gp[c * n2 + k * nc + jj]));
+      gx[c * n2 + loc] = x;
+    }
+  }
+  __syncthreads();
+  if (act) {
+    const int i = loc / nc, jj = loc % nc;
+    for (int c = 0; c < 8; ++c) {
+      double2 a = make_double2(0, 0);
+      for (int k = 0; k < nc; ++k) a = cadd(a, cscale(s.cmat[jj * nc + k], gx[c * n2 + i * nc + k]));
+      pcoef[((size_t)c * s.n_patches + p) * n2 + loc] = a;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K6 ----
+struct NearArgs {
+  SurfPtrs s;
+  const int* mom_off; const int* mom_patch; const double2* moments;
+  const int* dir_off; const int* dir_src;
+  const double2* phi; const double2* phiw; const double2* pcoef;
+  const double2* far; const double2* far_disp;  // (8,2,N)
+  double kr[2], ki[2];
+  double fd_step;
+  double2* s_val; double2* d_val;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// S kernel e^{i k r}/(4 pi r) and its target-normal derivative factor.
+__device__ __forceinline__ void kernel_pair(double kr, double ki, double r,
+                                            double ndx, double2& gk,
+                                            double2& qk) {
+  const double2 e = cexp_ikx(kr, ki, r);
+  const double inv = 1.0 / (4.0 * M_PI * r);
+  gk = make_double2(e.x * inv, e.y * inv);
+  // (ndx * (i kappa r - 1) / r^2): i*kappa*r = (-ki r, kr r)
+  const double2 f = make_double2(ndx * (-ki * r - 1.0) / (r * r), ndx * (kr * r) / (r * r));
+  qk = cmul(gk, f);
+}
+
+// Sums 28 complex per-lane partials over the warp; lane c*2+k keeps the
+// totals of channel c, kernel k (S in tot_s, D in tot_d for c < 6).
+__device__ __forceinline__ void warp_reduce_owned(const double2 (&s)[8][2],
+                                                  const double2 (&d)[6][2],
+                                                  int lane, double2& tot_s,
+                                                  double2& tot_d) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double2 ts = make_double2(warp_sum(s[c][k].x), warp_sum(s[c][k].y));
+      if (lane == c * 2 + k) tot_s = ts;
+      if (c < 6) {
+        const double2 td = make_double2(warp_sum(d[c][k].x), warp_sum(d[c][k].y));
+        if (lane == c * 2 + k) tot_d = td;
+      }
+    }
+}
+
+// One warp per target: singular moments (S, D), neighbour-box direct sums
+// (+ entries) and local corrections (- entries), then the reference's
+// combination with the far field (operators.py:341-350), including
+// D_far = (S_disp - S) / h.  Three phases keep 28 complex accumulators live.
+__global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n = a.s.n, n2 = a.s.n_c * a.s.n_c;
+  if (warp >= n) return;
+  const int ell = warp;
+  double2 S[8][2], D[6][2];
+  double2 near_s = make_double2(0, 0), near_d = make_double2(0, 0);
+  double2 nb_s = make_double2(0, 0), nb_d = make_double2(0, 0);
+  double2 cr_s = make_double2(0, 0), cr_d = make_double2(0, 0);
+  auto zero = [&]() {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) S[c][0] = S[c][1] = make_double2(0, 0);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) D[c][0] = D[c][1] = make_double2(0, 0);
+  };
+  // ---- phase 1: singular moments (quadrature.py:343-360)
+  zero();
+  for (int q = a.mom_off[ell]; q < a.mom_off[ell + 1]; ++q) {
+    const int p = a.mom_patch[q];
+    const double2* beta = a.moments + (size_t)q * 4 * n2;
+    for (int mn = lane; mn < n2; mn += 32) {
+      const double2 bs0 = beta[mn], bs1 = beta[n2 + mn];
+      const double2 bd0 = beta[2 * n2 + mn], bd1 = beta[3 * n2 + mn];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double2 co = a.pcoef[((size_t)c * a.s.n_patches + p) * n2 + mn];
+        S[c][0] = cadd(S[c][0], cmul(bs0, co));
+        S[c][1] = cadd(S[c][1], cmul(bs1, co));
+        if (c < 6) {
+          D[c][0] = cadd(D[c][0], cmul(bd0, co));
+          D[c][1] = cadd(D[c][1], cmul(bd1, co));
+        }
+      }
+    }
+  }
+  warp_reduce_owned(S, D, lane, near_s, near_d);
+  const double x0 = a.s.pts[3 * ell], x1 = a.s.pts[3 * ell + 1], x2 = a.s.pts[3 * ell + 2];
+  const double n0 = a.s.nrm[3 * ell], n1 = a.s.nrm[3 * ell + 1], n2v = a.s.nrm[3 * ell + 2];
+  const int e0 = a.dir_off[ell], e1 = a.dir_off[ell + 1];
+  // ---- phases 2/3: + neighbour sources (operators.py:279-319, phi*w),
+  //                  - corrections (quadrature.py:457-487, (G*jw)*phi)
+#pragma unroll 1
+  for (int phase = 0; phase < 2; ++phase) {
+    zero();
+    for (int e = e0 + lane; e < e1; e += 32) {
+      const int code = a.dir_src[e];
+      const bool neg = code < 0;
+      if (neg != (phase == 1)) continue;
+      const int src = neg ? -code - 1 : code;
+      const double dx = x0 - a.s.pts[3 * src], dy = x1 - a.s.pts[3 * src + 1],
+                   dz = x2 - a.s.pts[3 * src + 2];
+      const double r = sqrt(dx * dx + dy * dy + dz * dz);
+      const double ndx = dx * n0 + dy * n1 + dz * n2v;
+      double2 gk[2], qk[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) kernel_pair(a.kr[k], a.ki[k], r, ndx, gk[k], qk[k]);
+      const double jw = neg ? a.s.wq[src] : 1.0;
+      const double2* wsrc = neg ? a.phi : a.phiw;
+      if (neg) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          gk[k] = cscale(jw, gk[k]);
+          qk[k] = cscale(jw, qk[k]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double2 w = wsrc[(size_t)c * n + src];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          S[c][k] = cadd(S[c][k], cmul(gk[k], w));
+          if (c < 6) D[c][k] = cadd(D[c][k], cmul(qk[k], w));
+        }
+      }
+    }
+    if (phase == 0) warp_reduce_owned(S, D, lane, nb_s, nb_d);
+    else warp_reduce_owned(S, D, lane, cr_s, cr_d);
+  }
+  if (lane < 16) {
+    const int c = lane >> 1;
+    const size_t o = (size_t)lane * n + ell;   // (c*2+k)*N + ell
+    const double2 s_if = a.far[o];
+    a.s_val[o] = cadd(near_s, csub(cadd(s_if, nb_s), cr_s));
+    if (c < 6) {
+      const double2 sd = a.far_disp[o];
+      const double2 d_if = make_double2((sd.x - s_if.x) / a.fd_step,
+                                        (sd.y - s_if.y) / a.fd_step);
+      a.d_val[o] = cadd(near_d, csub(cadd(d_if, nb_d), cr_d));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K7 ----
+struct AsmArgs {
+  SurfPtrs s;
+  const double2* s_val; const double2* d_val; const double2* y;
+  double2 eps_e, mu_e, eps_i, mu_i, kap[2];
+  double omega;
+  double2* out;
+};
+
+__device__ __forceinline__ void cross3(const double* n, const double2* v, double2* o) {
+  o[0] = csub(cscale(n[1], v[2]), cscale(n[2], v[1]));
+  o[1] = csub(cscale(n[2], v[0]), cscale(n[0], v[2]));
+  o[2] = csub(cscale(n[0], v[1]), cscale(n[1], v[0]));
+}
+
+// One CTA per patch: tangential gradients of the 16 S fields (per-patch
+// spectral differentiation), n x curl and R+T terms, the N-Muller rows and
+// the tangent-frame encoding (operators.py:354-403).
+__global__ void assemble_kernel(AsmArgs a) {
+  extern __shared__ double2 sh[];   // 16 x n2
+  const int nc = a.s.n_c, n2 = nc * nc, n = a.s.n;
+  const int p = blockIdx.x, loc = threadIdx.x;
+  const bool act = loc < n2;
+  const int ell = p * n2 + loc;
+  if (act)
+    for (int f = 0; f < 16; ++f) sh[f * n2 + loc] = a.s_val[(size_t)f * n + ell];
+  __syncthreads();
+  if (!act) return;
+  const int i = loc / nc, jj = loc % nc;
+  const double* eu = a.s.eu + 3 * ell;
+  const double* ev = a.s.ev + 3 * ell;
+  const double e = eu[0] * eu[0] + eu[1] * eu[1] + eu[2] * eu[2];
+  const double f = eu[0] * ev[0] + eu[1] * ev[1] + eu[2] * ev[2];
+  const double g = ev[0] * ev[0] + ev[1] * ev[1] + ev[2] * ev[2];
+  const double det = e * g - f * f;
+  const double nr[3] = {a.s.nrm[3 * ell], a.s.nrm[3 * ell + 1], a.s.nrm[3 * ell + 2]};
+  // grad[field][3]
+  double2 grad[16][3];
+#pragma unroll
+  for (int fld = 0; fld < 16; ++fld) {
+    double2 du = make_double2(0, 0), dv = make_double2(0, 0);
+    for (int k = 0; k < nc; ++k) {
+      du = cadd(du, cscale(a.s.dmat[i * nc + k], sh[fld * n2 + k * nc + jj]));
+      dv = cadd(dv, cscale(a.s.dmat[jj * nc + k], sh[fld * n2 + i * nc + k]));
+    }
+    const double2 ca = cscale(1.0 / det, csub(cscale(g, du), cscale(f, dv)));
+    const double2 cb = cscale(1.0 / det, csub(cscale(e, dv), cscale(f, du)));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) grad[fld][c] = cadd(cscale(eu[c], ca), cscale(ev[c], cb));
+  }
+  // field index fld = channel*2 + k
+  auto curl_trace = [&](int k, int c0, double2* res) {
+    double2 w[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) w[c] = a.d_val[((size_t)(c0 + c) * 2 + k) * n + ell];
+    double2 nw = make_double2(0, 0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) nw = cadd(nw, cscale(nr[c], w[c]));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double2 wt = csub(w[c], cscale(nr[c], nw));
+      double2 gg = make_double2(0, 0);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) gg = cadd(gg, cscale(nr[q], grad[(c0 + q) * 2 + k][c]));
+      res[c] = csub(gg, wt);
+    }
+  };
+  auto rt_terms = [&](int c0, int cdiv, double2* res) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) res[c] = make_double2(0, 0);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double sign = k == 0 ? 1.0 : -1.0;
+      double2 sv[3], c1[3], c2[3], gd[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        sv[c] = sh[((c0 + c) * 2 + k) * n2 + loc];
+        gd[c] = grad[cdiv * 2 + k][c];
+      }
+      cross3(nr, sv, c1);
+      cross3(nr, gd, c2);
+      const double2 k2 = cmul(a.kap[k], a.kap[k]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double2 term = cadd(cmul(k2, c1[c]), c2[c]);
+        res[c] = cadd(res[c], cscale(sign, term));
+      }
+    }
+    const double2 fac = make_double2(0.0, -1.0 / a.omega);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) res[c] = cmul(fac, res[c]);
+  };
+  double2 ctm0[3], ctm1[3], ctj0[3], ctj1[3], rtj[3], rtm[3];
+  curl_trace(0, 3, ctm0);
+  curl_trace(1, 3, ctm1);
+  curl_trace(0, 0, ctj0);
+  curl_trace(1, 0, ctj1);
+  rt_terms(0, 6, rtj);
+  rt_terms(3, 7, rtm);
+  // decoded currents
+  const double2 y1 = a.y[ell], y2 = a.y[n + ell], y3 = a.y[2 * n + ell], y4 = a.y[3 * n + ell];
+  const double* t1 = a.s.t1 + 3 * ell;
+  const double* t2 = a.s.t2 + 3 * ell;
+  const double2 hmu = cscale(0.5, cadd(a.mu_e, a.mu_i));
+  const double2 heps = cscale(0.5, cadd(a.eps_e, a.eps_i));
+  double2 rm[3], rj[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double2 mc = cadd(cscale(t1[c], y1), cscale(t2[c], y2));
+    const double2 jc = cadd(cscale(t1[c], y3), cscale(t2[c], y4));
+    const double2 km = csub(cmul(a.mu_e, ctm0[c]), cmul(a.mu_i, ctm1[c]));
+    const double2 kj = csub(cmul(a.eps_e, ctj0[c]), cmul(a.eps_i, ctj1[c]));
+    rm[c] = csub(cadd(cmul(hmu, mc), km), rtj[c]);
+    rj[c] = cadd(cadd(rtm[c], cmul(heps, jc)), kj);
+  }
+  double2 o[4] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0),
+                  make_double2(0, 0)};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    o[0] = cadd(o[0], cscale(t1[c], rm[c]));
+    o[1] = cadd(o[1], cscale(t2[c], rm[c]));
+    o[2] = cadd(o[2], cscale(t1[c], rj[c]));
+    o[3] = cadd(o[3], cscale(t2[c], rj[c]));
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) a.out[(size_t)q * n + ell] = o[q];
+}
+
+// ------------------------------------------------------------ drivers ----
+static SurfPtrs surf(const Plan& p) {
+  return SurfPtrs{p.n, p.n_c, p.n_patches, p.pts, p.nrm, p.wq, p.jac,
+                  p.eu, p.ev, p.t1, p.t2, p.dmat, p.cmat};
+}
+
+int potentials_from_phi(Plan& p, cudaStream_t st) {
+  // far field on phi * weights (operators.py:336-340)
+  int rc = far_apply(p, p.phiw, 8, p.kappa, 2, p.far_out, p.far_disp, st);
+  if (rc) return rc;
+  NearArgs na{surf(p), p.mom_off, p.mom_patch,
+              reinterpret_cast<const double2*>(p.moments), p.dir_off, p.dir_src,
+              reinterpret_cast<const double2*>(p.phi),
+              reinterpret_cast<const double2*>(p.phiw),
+              reinterpret_cast<const double2*>(p.pcoef),
+              reinterpret_cast<const double2*>(p.far_out),
+              reinterpret_cast<const double2*>(p.far_disp),
+              {p.kappa[0], p.kappa[2]}, {p.kappa[1], p.kappa[3]}, p.fd_step,
+              reinterpret_cast<double2*>(p.s_val), reinterpret_cast<double2*>(p.d_val)};
+  const int warps_per_block = 4;
+  near_kernel<<<(p.n + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(na);
+  p.launches += 1;
+  IFGFB_CUDA(cudaGetLastError());
+  return IFGFB_OK;
+}
+
+static int pack_launch(Plan& p, const double* y, const double* phi_in,
+                       cudaStream_t st) {
+  const int n2 = p.n_c * p.n_c;
+  const int threads = ((n2 + 31) / 32) * 32;
+  const size_t sm = sizeof(double2) * 20 * n2;
+  pack_kernel<<<p.n_patches, threads, sm, st>>>(
+      surf(p), reinterpret_cast<const double2*>(y),
+      reinterpret_cast<const double2*>(phi_in), reinterpret_cast<double2*>(p.phi),
+      reinterpret_cast<double2*>(p.phiw), reinterpret_cast<double2*>(p.pcoef));
+  p.launches += 1;
+  IFGFB_CUDA(cudaGetLastError());
+  return IFGFB_OK;
+}
+
+int muller_apply(Plan& p, const double* y, double* out, cudaStream_t st) {
+  p.launches = 0;
+  int rc = pack_launch(p, y, nullptr, st);
+  if (rc) return rc;
+  rc = potentials_from_phi(p, st);
+  if (rc) return rc;
+  const int n2 = p.n_c * p.n_c;
+  const int threads = ((n2 + 31) / 32) * 32;
+  AsmArgs aa{surf(p), reinterpret_cast<const double2*>(p.s_val),
+             reinterpret_cast<const double2*>(p.d_val),
+             reinterpret_cast<const double2*>(y),
+             make_double2(p.eps_e[0], p.eps_e[1]), make_double2(p.mu_e[0], p.mu_e[1]),
+             make_double2(p.eps_i[0], p.eps_i[1]), make_double2(p.mu_i[0], p.mu_i[1]),
+             {make_double2(p.kappa[0], p.kappa[1]), make_double2(p.kappa[2], p.kappa[3])},
+             p.omega, reinterpret_cast<double2*>(out)};
+  assemble_kernel<<<p.n_patches, threads, sizeof(double2) * 16 * n2, st>>>(aa);
+  p.launches += 1;
+  IFGFB_CUDA(cudaGetLastError());
+  return IFGFB_OK;
+}
+
+// ------------------------------------------------------------- GMRES -----
+__global__ void zdotc_kernel(const double2* __restrict__ x, const double2* __restrict__ y,
+                             int64_t n, double2* __restrict__ partial) {
+  double re = 0, im = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 a = x[i], b = y[i];
+    re += a.x * b.x + a.y * b.y;
+    im += a.x * b.y - a.y * b.x;
+  }
+  __shared__ double sr[32], si[32];
+  re = warp_sum(re);
+  im = warp_sum(im);
+  if ((threadIdx.x & 31) == 0) { sr[threadIdx.x >> 5] = re; si[threadIdx.x >> 5] = im; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    re = threadIdx.x < nw ? sr[threadIdx.x] : 0.0;
+    im = threadIdx.x < nw ? si[threadIdx.x] : 0.0;
+    re = warp_sum(re);
+    im = warp_sum(im);
+    if (threadIdx.x == 0) partial[blockIdx.x] = make_double2(re, im);
+  }
+}
+
+__global__ void finish_sum(const double2* __restrict__ partial, int nb, double2* out) {
+  double re = 0, im = 0;
+  for (int i = threadIdx.x; i < nb; i += 32) { re += partial[i].x; im += partial[i].y; }
+  re = warp_sum(re);
+  im = warp_sum(im);
+  if (threadIdx.x == 0) *out = make_double2(re, im);
+}
+
+__global__ void zaxpy_kernel(double2 alpha, const double2* __restrict__ x,
+                             double2* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = cadd(y[i], cmul(alpha, x[i]));
+}
+
+__global__ void zdiv_kernel(double2* __restrict__ y, const double2* __restrict__ x,
+                            double denom, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = make_double2(x[i].x / denom, x[i].y / denom);
+}
+
+static double2* g_red = nullptr;
+static double2* g_red_host = nullptr;
+
+static int reduce_buffers() {
+  if (!g_red) {
+    IFGFB_CUDA(cudaMalloc(&g_red, sizeof(double2) * 1025));
+    IFGFB_CUDA(cudaMallocHost(&g_red_host, sizeof(double2)));
+  }
+  return IFGFB_OK;
+}
+
+}  // namespace ifgfb
+
+using namespace ifgfb;
+#define CHECK_ARG IFGFB_CHECK_ARG
+#define RC IFGFB_RC
+
+extern "C" {
+
+int ifgfb_plan_set_surface(ifgfb_plan* h, const ifgfb_surface_desc* d) {
+  CHECK_ARG(h && d, "null argument");
+  Plan& p = h->p;
+  CHECK_ARG(!p.finalized, "plan already finalized");
+  CHECK_ARG(d->n_c >= 2 && d->n_c <= MAXNC, "n_c out of supported range [2,16]");
+  CHECK_ARG((int64_t)d->n_patches * d->n_c * d->n_c == p.n,
+            "n_patches * n_c^2 != number of points");
+  p.n_patches = d->n_patches;
+  p.n_c = d->n_c;
+  const size_t n = p.n, n2 = (size_t)d->n_c * d->n_c;
+  RC(dev_upload(p, &p.pts, d->points, 3 * n));
+  RC(dev_upload(p, &p.nrm, d->normals, 3 * n));
+  RC(dev_upload(p, &p.wq, d->weights, n));
+  RC(dev_upload(p, &p.jac, d->jacobians, n));
+  RC(dev_upload(p, &p.eu, d->e_u, 3 * n));
+  RC(dev_upload(p, &p.ev, d->e_v, 3 * n));
+  RC(dev_upload(p, &p.t1, d->tangent1, 3 * n));
+  RC(dev_upload(p, &p.t2, d->tangent2, 3 * n));
+  RC(dev_upload(p, &p.dmat, d->diff_matrix, n2));
+  RC(dev_upload(p, &p.cmat, d->coeff_matrix, n2));
+  for (int i = 0; i < 2; ++i) {
+    p.eps_e[i] = d->eps_e[i];
+    p.mu_e[i] = d->mu_e[i];
+    p.eps_i[i] = d->eps_i[i];
+    p.mu_i[i] = d->mu_i[i];
+  }
+  for (int i = 0; i < 4; ++i) p.kappa[i] = d->kappas[i];
+  p.omega = d->omega;
+  p.fd_step = d->fd_step;
+  RC(dev_upload<double>(p, &p.phi, nullptr, 16 * n));
+  RC(dev_upload<double>(p, &p.phiw, nullptr, 16 * n));
+  RC(dev_upload<double>(p, &p.pcoef, nullptr, 16 * n));
+  RC(dev_upload<double>(p, &p.far_out, nullptr, 32 * n));
+  RC(dev_upload<double>(p, &p.far_disp, nullptr, 32 * n));
+  RC(dev_upload<double>(p, &p.s_val, nullptr, 32 * n));
+  RC(dev_upload<double>(p, &p.d_val, nullptr, 24 * n));
+  RC(dev_upload<double>(p, &p.dev_y, nullptr, 8 * n));
+  RC(dev_upload<double>(p, &p.dev_out, nullptr, 8 * n));
+  IFGFB_CUDA(cudaMallocHost(&p.host_stage, sizeof(double) * 16 * n));
+  p.has_surface = true;
+  return IFGFB_OK;
+}
+
+int ifgfb_plan_set_near(ifgfb_plan* h, const ifgfb_near_desc* d) {
+  CHECK_ARG(h && d, "null argument");
+  Plan& p = h->p;
+  CHECK_ARG(p.has_surface, "set_surface must precede set_near");
+  const int n = p.n, n2 = p.n_c * p.n_c;
+  std::vector<int> tmp(n + 1);
+  for (int i = 0; i <= n; ++i) tmp[i] = (int)d->mom_off[i];
+  CHECK_ARG(d->mom_off[n] == d->n_mom, "mom_off end != n_mom");
+  RC(dev_upload(p, &p.mom_off, tmp.data(), tmp.size()));
+  std::vector<int> pt(d->n_mom);
+  for (int64_t i = 0; i < d->n_mom; ++i) {
+    CHECK_ARG(d->mom_patch[i] >= 0 && d->mom_patch[i] < p.n_patches, "moment patch out of range");
+    pt[i] = (int)d->mom_patch[i];
+  }
+  RC(dev_upload(p, &p.mom_patch, pt.data(), pt.size()));
+  RC(dev_upload(p, &p.moments, d->moments, (size_t)d->n_mom * 4 * n2 * 2));
+  for (int i = 0; i <= n; ++i) tmp[i] = (int)d->dir_off[i];
+  CHECK_ARG(d->dir_off[n] == d->n_direct, "dir_off end != n_direct");
+  RC(dev_upload(p, &p.dir_off, tmp.data(), tmp.size()));
+  std::vector<int> ds(d->n_direct);
+  for (int64_t i = 0; i < d->n_direct; ++i) {
+    const int64_t c = d->dir_src[i];
+    CHECK_ARG(c >= -(int64_t)n && c < n, "direct source out of range");
+    ds[i] = (int)c;
+  }
+  RC(dev_upload(p, &p.dir_src, ds.data(), ds.size()));
+  p.n_mom = d->n_mom;
+  p.n_direct = d->n_direct;
+  p.has_near = true;
+  return IFGFB_OK;
+}
+
+int ifgfb_potentials(ifgfb_plan* h, const double* phi, double* s_val,
+                     double* d_val, void* stream) {
+  CHECK_ARG(h && phi && s_val && d_val, "null argument");
+  Plan& p = h->p;
+  if (!p.finalized || !p.has_near) {
+    set_error("plan has no surface/near-field data");
+    return IFGFB_ERR_STATE;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  p.launches = 0;
+  RC(pack_launch(p, nullptr, phi, st));
+  RC(potentials_from_phi(p, st));
+  IFGFB_CUDA(cudaMemcpyAsync(s_val, p.s_val, sizeof(double2) * 16 * (size_t)p.n,
+                             cudaMemcpyDeviceToDevice, st));
+  IFGFB_CUDA(cudaMemcpyAsync(d_val, p.d_val, sizeof(double2) * 12 * (size_t)p.n,
+                             cudaMemcpyDeviceToDevice, st));
+  return IFGFB_OK;
+}
+
+int ifgfb_muller_apply(ifgfb_plan* h, const double* y, double* out, void* stream) {
+  CHECK_ARG(h && y && out, "null argument");
+  Plan& p = h->p;
+  if (!p.finalized || !p.has_near) {
+    set_error("plan has no surface/near-field data");
+    return IFGFB_ERR_STATE;
+  }
+  return muller_apply(p, y, out, static_cast<cudaStream_t>(stream));
+}
+
+int ifgfb_muller_apply_host(ifgfb_plan* h, const double* y_host, double* out_host,
+                            void* stream) {
+  CHECK_ARG(h && y_host && out_host, "null argument");
+  Plan& p = h->p;
+  if (!p.finalized || !p.has_near) {
+    set_error("plan has no surface/near-field data");
+    return IFGFB_ERR_STATE;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t bytes = sizeof(double) * 8 * (size_t)p.n;
+  memcpy(p.host_stage, y_host, bytes);
+  IFGFB_CUDA(cudaMemcpyAsync(p.dev_y, p.host_stage, bytes, cudaMemcpyHostToDevice, st));
+  RC(muller_apply(p, p.dev_y, p.dev_out, st));
+  IFGFB_CUDA(cudaMemcpyAsync(p.host_stage + 8 * (size_t)p.n, p.dev_out, bytes,
+                             cudaMemcpyDeviceToHost, st));
+  IFGFB_CUDA(cudaStreamSynchronize(st));
+  memcpy(out_host, p.host_stage + 8 * (size_t)p.n, bytes);
+  return IFGFB_OK;
+}
+
+int ifgfb_zdotc(const double* x, const double* y, int64_t n, double* result,
+                void* stream) {
+  CHECK_ARG(x && y && result && n >= 0, "bad argument");
+  RC(reduce_buffers());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nb = (int)std::min<int64_t>(1024, std::max<int64_t>(1, (n + 255) / 256));
+  zdotc_kernel<<<nb, 256, 0, st>>>(reinterpret_cast<const double2*>(x),
+                                   reinterpret_cast<const double2*>(y), n, g_red);
+  finish_sum<<<1, 32, 0, st>>>(g_red, nb, g_red + 1024);
+  IFGFB_CUDA(cudaMemcpyAsync(g_red_host, g_red + 1024, sizeof(double2),
+                             cudaMemcpyDeviceToHost, st));
+  IFGFB_CUDA(cudaStreamSynchronize(st));
+  result[0] = g_red_host->x;
+  result[1] = g_red_host->y;
+  return IFGFB_OK;
+}
+
+int ifgfb_dznrm2(const double* x, int64_t n, double* result, void* stream) {
+  double v[2];
+  RC(ifgfb_zdotc(x, x, n, v, stream));
+  *result = sqrt(v[0]);
+  return IFGFB_OK;
+}
+
+int ifgfb_zaxpy(const double* alpha, const double* x, double* y, int64_t n,
+                void* stream) {
+  CHECK_ARG(alpha && x && y && n >= 0, "bad argument");
+  const int nb = (int)std::min<int64_t>(4096, std::max<int64_t>(1, (n + 255) / 256));
+  zaxpy_kernel<<<nb, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      make_double2(alpha[0], alpha[1]), reinterpret_cast<const double2*>(x),
+      reinterpret_cast<double2*>(y), n);
+  IFGFB_CUDA(cudaGetLastError());
+  return IFGFB_OK;
+}
+
+int ifgfb_zscal_div(double* y, const double* x, double denom, int64_t n,
+                    void* stream) {
+  CHECK_ARG(x && y && n >= 0, "bad argument");
+  const int nb = (int)std::min<int64_t>(4096, std::max<int64_t>(1, (n + 255) / 256));
+  zdiv_kernel<<<nb, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<double2*>(y), reinterpret_cast<const double2*>(x), denom, n);
+  IFGFB_CUDA(cudaGetLastError());
+  return IFGFB_OK;
+}
+
+}  // extern "C"

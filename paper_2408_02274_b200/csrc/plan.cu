@@ -16,24 +16,6 @@ void set_error(const std::string& msg) { g_err = msg; }
 
 int far_setup_kernels();
 
-template <typename T>
-static int dev_upload(Plan& p, T** dst, const T* src, size_t n) {
-  *dst = nullptr;
-  if (n == 0) return IFGFB_OK;
-  void* ptr = nullptr;
-  IFGFB_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
-  p.allocations.push_back(ptr);
-  p.bytes += n * sizeof(T);
-  if (src) IFGFB_CUDA(cudaMemcpy(ptr, src, n * sizeof(T), cudaMemcpyHostToDevice));
-  *dst = static_cast<T*>(ptr);
-  return IFGFB_OK;
-}
-
-template <typename T>
-static int dev_alloc(Plan& p, T** dst, size_t n) {
-  return dev_upload<T>(p, dst, nullptr, n);
-}
-
 static bool to_i32(const int64_t* src, size_t n, std::vector<int>& out,
                    const char* what) {
   out.resize(n);
@@ -47,27 +29,12 @@ static bool to_i32(const int64_t* src, size_t n, std::vector<int>& out,
   return true;
 }
 
-#define CHECK_ARG(cond, msg)             \
-  do {                                   \
-    if (!(cond)) {                       \
-      set_error(msg);                    \
-      return IFGFB_ERR_ARG;              \
-    }                                    \
-  } while (0)
-
-#define RC(x)                  \
-  do {                         \
-    int rc_ = (x);             \
-    if (rc_ != IFGFB_OK) return rc_; \
-  } while (0)
+#define CHECK_ARG IFGFB_CHECK_ARG
+#define RC IFGFB_RC
 
 }  // namespace ifgfb
 
 using namespace ifgfb;
-
-struct ifgfb_plan {
-  Plan p;
-};
 
 extern "C" {
 
