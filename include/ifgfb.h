@@ -207,6 +207,17 @@ int ifgfb_zaxpy(const double* alpha, const double* x, double* y, int64_t n,
 int ifgfb_zscal_div(double* y, const double* x, double denom, int64_t n,
                     void* stream);          /* y = x / denom (real)       */
 
+/* One modified Gram-Schmidt Arnoldi step (reference solver.py:61-67) on a
+ * device basis V (vectors of n complex, stride ld complex between vectors):
+ *   for i in 0..k: h[i] = vdot(V[i], w); w -= h[i] V[i]
+ *   h[k+1] = ||w||;  V[k+1] = w / h[k+1]  (skipped when h[k+1] == 0)
+ * h is a device array of >= k+2 complex; nothing is synchronised. */
+int ifgfb_arnoldi_mgs(double* basis, int64_t ld, int k, int64_t n, double* w,
+                      double* h, void* stream);
+/* x = sum_{j<k} y[j] V[j]   (reference solver.py:92), y device k complex */
+int ifgfb_basis_combine(const double* basis, int64_t ld, int k, int64_t n,
+                        const double* y, double* x, void* stream);
+
 /* Number of kernels launched by the last apply on this plan. */
 int64_t ifgfb_plan_last_launches(const ifgfb_plan* plan);
 

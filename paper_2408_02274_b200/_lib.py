@@ -98,6 +98,10 @@ EXPORTS = {
     "ifgfb_dznrm2": ([C.c_void_p, C.c_int64, _dp, C.c_void_p], C.c_int),
     "ifgfb_zaxpy": ([_dp, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
                     C.c_int),
+    "ifgfb_arnoldi_mgs": ([C.c_void_p, C.c_int64, C.c_int, C.c_int64,
+                           C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "ifgfb_basis_combine": ([C.c_void_p, C.c_int64, C.c_int, C.c_int64,
+                             C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_zscal_div": ([C.c_void_p, C.c_void_p, C.c_double, C.c_int64,
                          C.c_void_p], C.c_int),
 }

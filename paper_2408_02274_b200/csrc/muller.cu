@@ -145,11 +145,6 @@ struct NearArgs {
   double2* s_val; double2* d_val;
 };
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 // S kernel e^{i k r}/(4 pi r) and its target-normal derivative factor.
 __device__ __forceinline__ void kernel_pair(double kr, double ki, double r,
@@ -468,64 +463,6 @@ int muller_apply(Plan& p, const double* y, double* out, cudaStream_t st) {
   return IFGFB_OK;
 }
 
-// ------------------------------------------------------------- GMRES -----
-__global__ void zdotc_kernel(const double2* __restrict__ x, const double2* __restrict__ y,
-                             int64_t n, double2* __restrict__ partial) {
-  double re = 0, im = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double2 a = x[i], b = y[i];
-    re += a.x * b.x + a.y * b.y;
-    im += a.x * b.y - a.y * b.x;
-  }
-  __shared__ double sr[32], si[32];
-  re = warp_sum(re);
-  im = warp_sum(im);
-  if ((threadIdx.x & 31) == 0) { sr[threadIdx.x >> 5] = re; si[threadIdx.x >> 5] = im; }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int nw = blockDim.x >> 5;
-    re = threadIdx.x < nw ? sr[threadIdx.x] : 0.0;
-    im = threadIdx.x < nw ? si[threadIdx.x] : 0.0;
-    re = warp_sum(re);
-    im = warp_sum(im);
-    if (threadIdx.x == 0) partial[blockIdx.x] = make_double2(re, im);
-  }
-}
-
-__global__ void finish_sum(const double2* __restrict__ partial, int nb, double2* out) {
-  double re = 0, im = 0;
-  for (int i = threadIdx.x; i < nb; i += 32) { re += partial[i].x; im += partial[i].y; }
-  re = warp_sum(re);
-  im = warp_sum(im);
-  if (threadIdx.x == 0) *out = make_double2(re, im);
-}
-
-__global__ void zaxpy_kernel(double2 alpha, const double2* __restrict__ x,
-                             double2* __restrict__ y, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = cadd(y[i], cmul(alpha, x[i]));
-}
-
-__global__ void zdiv_kernel(double2* __restrict__ y, const double2* __restrict__ x,
-                            double denom, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = make_double2(x[i].x / denom, x[i].y / denom);
-}
-
-static double2* g_red = nullptr;
-static double2* g_red_host = nullptr;
-
-static int reduce_buffers() {
-  if (!g_red) {
-    IFGFB_CUDA(cudaMalloc(&g_red, sizeof(double2) * 1025));
-    IFGFB_CUDA(cudaMallocHost(&g_red_host, sizeof(double2)));
-  }
-  return IFGFB_OK;
-}
-
 }  // namespace ifgfb
 
 using namespace ifgfb;
@@ -655,51 +592,6 @@ int ifgfb_muller_apply_host(ifgfb_plan* h, const double* y_host, double* out_hos
                              cudaMemcpyDeviceToHost, st));
   IFGFB_CUDA(cudaStreamSynchronize(st));
   memcpy(out_host, p.host_stage + 8 * (size_t)p.n, bytes);
-  return IFGFB_OK;
-}
-
-int ifgfb_zdotc(const double* x, const double* y, int64_t n, double* result,
-                void* stream) {
-  CHECK_ARG(x && y && result && n >= 0, "bad argument");
-  RC(reduce_buffers());
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int nb = (int)std::min<int64_t>(1024, std::max<int64_t>(1, (n + 255) / 256));
-  zdotc_kernel<<<nb, 256, 0, st>>>(reinterpret_cast<const double2*>(x),
-                                   reinterpret_cast<const double2*>(y), n, g_red);
-  finish_sum<<<1, 32, 0, st>>>(g_red, nb, g_red + 1024);
-  IFGFB_CUDA(cudaMemcpyAsync(g_red_host, g_red + 1024, sizeof(double2),
-                             cudaMemcpyDeviceToHost, st));
-  IFGFB_CUDA(cudaStreamSynchronize(st));
-  result[0] = g_red_host->x;
-  result[1] = g_red_host->y;
-  return IFGFB_OK;
-}
-
-int ifgfb_dznrm2(const double* x, int64_t n, double* result, void* stream) {
-  double v[2];
-  RC(ifgfb_zdotc(x, x, n, v, stream));
-  *result = sqrt(v[0]);
-  return IFGFB_OK;
-}
-
-int ifgfb_zaxpy(const double* alpha, const double* x, double* y, int64_t n,
-                void* stream) {
-  CHECK_ARG(alpha && x && y && n >= 0, "bad argument");
-  const int nb = (int)std::min<int64_t>(4096, std::max<int64_t>(1, (n + 255) / 256));
-  zaxpy_kernel<<<nb, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      make_double2(alpha[0], alpha[1]), reinterpret_cast<const double2*>(x),
-      reinterpret_cast<double2*>(y), n);
-  IFGFB_CUDA(cudaGetLastError());
-  return IFGFB_OK;
-}
-
-int ifgfb_zscal_div(double* y, const double* x, double denom, int64_t n,
-                    void* stream) {
-  CHECK_ARG(x && y && n >= 0, "bad argument");
-  const int nb = (int)std::min<int64_t>(4096, std::max<int64_t>(1, (n + 255) / 256));
-  zdiv_kernel<<<nb, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<double2*>(y), reinterpret_cast<const double2*>(x), denom, n);
-  IFGFB_CUDA(cudaGetLastError());
   return IFGFB_OK;
 }
 
