@@ -506,6 +506,7 @@ class AccumulationPlan:
     sig_off: np.ndarray
     group_bounds: np.ndarray      # flat, per group: start slot (len n_groups)
     group_end: np.ndarray
+    group_sigma: np.ndarray       # child segment id of each group
     scatter: np.ndarray
     xs: np.ndarray
     xt: np.ndarray
@@ -596,6 +597,7 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy,
     plan = AccumulationPlan(
         level=d, n_types=n_t, type_gamma=gamma, type_octant=toct,
         sig_off=sig_off, group_bounds=g_start, group_end=g_end,
+        group_sigma=g_sigma,
         scatter=order_all, xs=geo["xs"], xt=geo["xt"], xp=geo["xp"],
         r_parent=geo["rp"], r_child=geo["rc"],
         inst_off=_offsets_from_owner(prow, pcl.n_segments),

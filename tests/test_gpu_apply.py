@@ -1,0 +1,131 @@
+"""GPU N-Muller apply / potentials / GMRES against the unmodified reference
+(golden), the oracle on this host, and the reference's operator and solver
+tests (tests/test_operators.py, tests/test_solver.py) restated.
+
+Tolerances (north star): apply(y) <= 1e-10 relative l2 (the reference's own
+vec/seq floor is 2.8e-11 at cfg 1, 5.0e-11 at s1); raw far-field outputs <=
+1e-13; GMRES residual history <= 1e-8 relative per entry.  D alone is NOT
+held to 1e-10: the reference's own vec/seq runs differ by 2.2e-10 there
+(finite difference with h = 1e-6)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from _support import golden, inputs, plan_matches_golden, rel
+from paper_2408_02274_b200.fields import plane_wave
+from paper_2408_02274_b200.operator import (DensityBlock, MullerOperator,
+                                            build_muller_operator)
+from paper_2408_02274_b200.solver import gmres
+
+pytestmark = pytest.mark.gpu
+
+_OPS = {}
+
+
+def device_op(name) -> MullerOperator:
+    if name not in _OPS:
+        inp = inputs(name)
+        _OPS[name] = MullerOperator(
+            inp["disc"], inp["mats"], inp["smap"], inp["moments"],
+            (inp["corr"].ell_idx, inp["corr"].src_idx), tree=inp["tree"],
+            hierarchy=inp["hier"])
+    return _OPS[name]
+
+
+@pytest.mark.parametrize("name", ["s1", "c1"])
+def test_apply_vs_reference_golden(name):
+    if not plan_matches_golden(name):
+        pytest.skip("host numpy produced a different plan than the golden host")
+    z = golden(name)
+    op = device_op(name)
+    out = op.apply(z["y"])
+    assert rel(out, z["apply_y"]) < 1e-10
+
+
+@pytest.mark.parametrize("name", ["s1", "c1"])
+def test_potentials_vs_reference_golden(name):
+    if not plan_matches_golden(name):
+        pytest.skip("host numpy produced a different plan than the golden host")
+    z = golden(name)
+    op = device_op(name)
+    m, j = op.decode(z["y"])
+    s, d = op.potentials(DensityBlock.from_currents(op.disc, j, m))
+    assert rel(s, z["s_val"]) < 1e-13
+    assert rel(d, z["d_val"]) < 1e-9
+
+
+def test_apply_vs_oracle_on_host():
+    inp = inputs("s1")
+    op = device_op("s1")
+    y = np.random.default_rng(9).normal(size=(op.n_unknowns, 2)) @ [1, 1j]
+    ref = oracle.muller_apply(oracle.OperatorData(
+        inp["disc"], inp["mats"], inp["smap"], inp["moments"],
+        inp["corr"].ell_idx, inp["corr"].src_idx, inp["tree"], inp["hier"]), y)
+    assert rel(op.apply(y), ref) < 1e-10
+
+
+def test_device_and_host_paths_bitwise_equal_and_deterministic():
+    op = device_op("c1")
+    y = golden("c1")["y"]
+    a = op.apply(y)
+    b = op.apply(y)
+    yd = torch.from_numpy(y).cuda()
+    c = op.apply_device(yd).cpu().numpy()
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+def test_apply_linearity():
+    op = device_op("c1")
+    rng = np.random.default_rng(2)
+    n = op.n_unknowns
+    y1 = rng.normal(size=n) + 1j * rng.normal(size=n)
+    y2 = rng.normal(size=n) + 1j * rng.normal(size=n)
+    lhs = op.apply(0.7 * y1 - 1.3j * y2)
+    rhs = 0.7 * op.apply(y1) - 1.3j * op.apply(y2)
+    # reference's own linearity residual here is 5.4e-11 (golden floor)
+    assert rel(lhs, rhs) < 2e-10
+
+
+def test_apply_rejects_wrong_length():
+    op = device_op("s1")
+    with pytest.raises(ValueError):
+        op.apply(np.zeros(op.n_unknowns + 1, complex))
+
+
+def test_gmres_matches_reference_history():
+    if not plan_matches_golden("c1"):
+        pytest.skip("host numpy produced a different plan than the golden host")
+    z = golden("c1_gmres")
+    op = device_op("c1")
+    k0 = 2 * np.pi
+    b = op.rhs(plane_wave(k0, direction=(0.0, 0.0, 1.0),
+                          polarization=(1.0, 0.0, 0.0), omega=k0))
+    assert np.array_equal(b, z["b"])
+    x, rep = gmres(op, b, tol=1e-6, max_iter=300)
+    ref = z["residuals"]
+    assert rep.converged and rep.iterations == int(z["iterations"]) == 38
+    r = np.array(rep.residuals)
+    assert np.max(np.abs(r - ref) / ref) < 1e-8
+    assert rel(x, z["x"]) < 1e-8
+    assert np.linalg.norm(b - op.apply(x)) / np.linalg.norm(b) <= 2e-6
+
+
+def test_gmres_generic_callables():
+    rng = np.random.default_rng(1)
+    b = rng.normal(size=20) + 1j * rng.normal(size=20)
+    x, rep = gmres(lambda v: v, b, tol=1e-12)
+    assert rep.iterations == 1 and rep.converged and np.abs(x - b).max() < 1e-12
+    x, rep = gmres(lambda v: 2 * v, np.zeros(10, complex), tol=1e-10)
+    assert rep.iterations == 0 and rep.converged and not x.any()
+    n = 60
+    a = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n)) + 5 * np.eye(n)
+    b = rng.normal(size=n) + 1j * rng.normal(size=n)
+    x, rep = gmres(lambda v: a @ v, b, tol=1e-10, max_iter=n)
+    assert np.all(np.diff(rep.residuals) <= 1e-14)
+    assert np.abs(x - np.linalg.solve(a, b)).max() < 1e-8
+    x, rep = gmres(lambda v: a @ v, b, tol=1e-30, max_iter=5)
+    assert not rep.converged and rep.iterations == 5
+    with pytest.raises(ValueError):
+        gmres(lambda v: v, b, tol=0.0)

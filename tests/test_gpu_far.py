@@ -1,0 +1,145 @@
+"""GPU far field (ifgfb_far_apply through the drop-in ``ifgf_apply``) against
+the reference golden vectors, the oracle run on this host, and the
+reference's own far-field tests (tests/test_ifgf.py:225-389) restated."""
+
+import numpy as np
+import pytest
+
+import oracle
+from _support import golden, inputs, plan_matches_golden, rel
+from paper_2408_02274_b200 import surface
+from paper_2408_02274_b200.engine import ifgf_apply
+from paper_2408_02274_b200.octree import build_box_tree, build_cone_hierarchy
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["rand_ifgf", "s1", "c1"])
+def test_far_field_vs_reference_golden(name):
+    if name != "rand_ifgf" and not plan_matches_golden(name):
+        pytest.skip("host numpy produced a different plan than the golden host")
+    z, inp = golden(name), inputs(name)
+    out, od = ifgf_apply(inp["tree"], inp["hier"], z["weights"], inp["kappas"],
+                         displaced_normals=inp["disc"].normals,
+                         displaced_step=1e-6)
+    # reference floor for ifgf outputs: vec vs seq 9.6e-16
+    assert rel(out, z["far"]) < 1e-13
+    assert rel(od, z["far_disp"]) < 1e-13
+
+
+def test_far_field_vs_oracle_on_host():
+    z, inp = golden("rand_ifgf"), inputs("rand_ifgf")
+    w = np.random.default_rng(11).normal(size=(3, inp["disc"].n_points)) * (1 + 0.5j)
+    got, gd = ifgf_apply(inp["tree"], inp["hier"], w, inp["kappas"],
+                         displaced_normals=inp["disc"].normals)
+    ref, rd = oracle.far_field(inp["tree"], inp["hier"], w, inp["kappas"],
+                               inp["disc"].normals, 1e-6)
+    assert rel(got, ref) < 1e-13 and rel(gd, rd) < 1e-13
+
+
+def test_channel_independence_and_linearity():
+    disc = surface.make_sphere_surface(1, 10)
+    kap = (np.pi, 1.3 * np.pi)
+    tree = build_box_tree(disc.points, max(kap))
+    hier = build_cone_hierarchy(tree)
+    n = disc.n_points
+    rng = np.random.default_rng(6)
+    w = np.zeros((4, n), dtype=complex)
+    w[2] = rng.normal(size=n) + 1j * rng.normal(size=n)
+    out, _ = ifgf_apply(tree, hier, w, kap)
+    assert np.abs(out[[0, 1, 3]]).max() == 0.0
+    assert np.abs(out[2]).max() > 0.0
+    w2 = np.zeros_like(w)
+    w2[2] = rng.normal(size=n)
+    a, _ = ifgf_apply(tree, hier, w + 0.5j * w2, kap)
+    b, _ = ifgf_apply(tree, hier, w, kap)
+    c, _ = ifgf_apply(tree, hier, w2, kap)
+    assert np.abs(a - b - 0.5j * c).max() < 1e-12 * np.abs(a).max()
+
+
+def test_vec_seq_identical_and_deterministic():
+    disc = surface.make_sphere_surface(2, 8)
+    kap = (np.pi, 2 * np.pi)
+    tree = build_box_tree(disc.points, max(kap))
+    hier = build_cone_hierarchy(tree)
+    w = np.random.default_rng(7).normal(size=(3, disc.n_points)) * (1 - 1j)
+    v, _ = ifgf_apply(tree, hier, w, kap, mode="vec")
+    s, _ = ifgf_apply(tree, hier, w, kap, mode="seq")
+    v2, _ = ifgf_apply(tree, hier, w, kap, mode="vec")
+    assert np.abs(v - s).max() < 1e-12 * np.abs(v).max()
+    assert np.array_equal(v, v2)          # bitwise run-to-run
+    with pytest.raises(ValueError):
+        ifgf_apply(tree, hier, w, kap, mode="bogus")
+
+
+def test_many_channels_and_three_kernels():
+    """nch*nk > 16 columns: processed as column groups on device."""
+    inp = inputs("rand_ifgf")
+    n = inp["disc"].n_points
+    rng = np.random.default_rng(3)
+    w = rng.normal(size=(11, n)) + 1j * rng.normal(size=(11, n))
+    kap = (2 * np.pi, 3 * np.pi, 2.5 * np.pi)
+    got, _ = ifgf_apply(inp["tree"], inp["hier"], w, kap)
+    ref, _ = oracle.far_field(inp["tree"], inp["hier"], w, kap)
+    assert got.shape == (11, 3, n)
+    assert rel(got, ref) < 1e-13
+
+
+def test_self_interaction_excluded():
+    pts = np.array([[0.05, 0.05, 0.05], [0.95, 0.95, 0.95]])
+    tree = build_box_tree(pts, 40.0)
+    hier = build_cone_hierarchy(tree)
+    out, _ = ifgf_apply(tree, hier, np.array([[1.0 + 0j, 0.0]]), (40.0,))
+    r = np.linalg.norm(pts[1] - pts[0])
+    assert abs(out[0, 0, 0]) < 1e-12
+    assert out[0, 0, 1] == pytest.approx(np.exp(1j * 40 * r) / (4 * np.pi * r), rel=2e-4)
+
+
+def test_shallow_tree_gives_zero_far_field():
+    pts = np.random.default_rng(1).normal(size=(30, 3)) * 0.01
+    tree = build_box_tree(pts, 1.0)
+    hier = build_cone_hierarchy(tree)
+    out, od = ifgf_apply(tree, hier, np.ones((2, 30)), (1.0, 2.0),
+                         displaced_normals=np.ones((30, 3)))
+    assert out.shape == (2, 2, 30) and not out.any() and not od.any()
+
+
+def test_sphere_accuracy_vs_naive_far_sums():
+    from test_oracle import naive_far
+    disc = surface.make_sphere_surface(2, 12)
+    kap = (2 * np.pi, 3 * np.pi)
+    tree = build_box_tree(disc.points, max(kap))
+    hier = build_cone_hierarchy(tree)
+    rng = np.random.default_rng(5)
+    w = rng.normal(size=(2, disc.n_points)) + 1j * rng.normal(size=(2, disc.n_points))
+    out, _ = ifgf_apply(tree, hier, w, kap)
+    idx = rng.choice(disc.n_points, 150, replace=False)
+    sub = np.zeros(disc.n_points, bool)
+    sub[idx] = True
+    ref = naive_far(tree, w, kap)
+    assert rel(out[:, :, idx], ref[:, :, idx]) < 1.5e-4
+
+
+def test_displaced_outputs_fd_vs_analytic():
+    disc = surface.make_sphere_surface(1, 10)
+    kappa = np.pi
+    tree = build_box_tree(disc.points, kappa)
+    hier = build_cone_hierarchy(tree)
+    rng = np.random.default_rng(8)
+    w = rng.normal(size=(1, disc.n_points)) + 1j * rng.normal(size=(1, disc.n_points))
+    h = 1e-6
+    out, od = ifgf_apply(tree, hier, w, (kappa,), displaced_normals=disc.normals,
+                         displaced_step=h)
+    fd = (od - out) / h
+    d = tree.depth
+    coords = tree.level(d).coords[tree.point_boxes(d)]
+    wt = w[:, tree.perm]
+    for ell in rng.choice(disc.n_points, 30, replace=False):
+        t = tree.iperm[ell]
+        far = np.abs(coords - coords[t]).max(axis=1) >= 2
+        dx = tree.points[t] - tree.points[far]
+        r = np.linalg.norm(dx, axis=1)
+        q = (dx @ disc.normals[ell]) * (1j * kappa * r - 1) * np.exp(1j * kappa * r) / (4 * np.pi * r**3)
+        ref = (q * wt[0, far]).sum()
+        if abs(ref) > 1e-3:
+            assert fd[0, 0, ell] == pytest.approx(ref, rel=2e-3)

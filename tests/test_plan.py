@@ -1,0 +1,139 @@
+"""Plan builder: bit-exact against the reference plan digests (golden, made
+by the unmodified reference) plus the reference's own structural tests
+(restated from reference tests/test_ifgf.py:41-222)."""
+
+import numpy as np
+import pytest
+
+from _support import framework_digests, golden_digests, inputs
+from paper_2408_02274_b200 import octree, surface
+from paper_2408_02274_b200.octree import (ETA, build_box_tree,
+                                          build_cone_hierarchy, cone_coords,
+                                          morton_decode, morton_encode)
+
+
+@pytest.mark.parametrize("name", ["s1", "c1"])
+def test_plan_digests_match_reference(name):
+    mine = framework_digests(inputs(name))
+    ref = golden_digests(name)
+    bad = [k for k in ref if str(mine[k]) != str(ref[k])]
+    assert not bad, f"plan arrays differ from the reference: {bad}"
+
+
+def test_accumulation_rows_exact_hits():
+    inp = inputs("c1")
+    for d in range(4, inp["tree"].depth + 1):
+        ap = octree.accumulation_plan(inp["tree"], inp["hier"], d)
+        assert ap.crow_misses == 0
+        assert ap.n_instances == ap.inst_off[-1]
+    for d in range(3, inp["tree"].depth + 1):
+        assert octree.emission_plan(inp["tree"], inp["hier"], d).row_misses == 0
+
+
+def test_plan_counts_cfg1():
+    """cfg-1 plan counts measured from the reference plan."""
+    inp = inputs("c1")
+    tree, hier = inp["tree"], inp["hier"]
+    assert tree.depth == 5
+    assert [tree.level(d).n_boxes for d in (3, 4, 5)] == [56, 248, 944]
+    assert [hier.level(d).n_segments for d in (3, 4, 5)] == [13244, 32136, 33280]
+    assert [(hier.level(d).n_s, hier.level(d).n_a) for d in (3, 4, 5)] == \
+        [(8, 16), (4, 8), (2, 4)]
+    assert [hier.level(d).cpt_idx.size for d in (3, 4, 5)] == \
+        [107664, 88848, 93072]
+    inst = [octree.accumulation_plan(tree, hier, d).n_instances for d in (4, 5)]
+    assert inst == [58976, 123896]
+
+
+def test_morton_round_trip():
+    rng = np.random.default_rng(0)
+    c = rng.integers(0, 2**15, size=(100, 3))
+    assert np.array_equal(morton_decode(morton_encode(c)), c)
+
+
+def test_tree_depth_rule():
+    disc = surface.make_sphere_surface(2, 8)
+    kappa = 2 * np.pi
+    tree = build_box_tree(disc.points, kappa)
+    q = 0.25 * 2 * np.pi / kappa
+    assert tree.side(tree.depth) <= q < tree.side(tree.depth - 1)
+
+
+def test_tree_single_cluster():
+    pts = np.random.default_rng(1).normal(size=(30, 3)) * 0.01
+    tree = build_box_tree(pts, 1.0)
+    assert tree.depth == 1 and tree.level(1).n_boxes == 1
+    assert np.array_equal(tree.level(1).neighbors(0), [0])
+
+
+def test_empty_points_rejected():
+    with pytest.raises(ValueError):
+        build_box_tree(np.zeros((0, 3)), 1.0)
+
+
+def test_partition_and_handoff():
+    disc = surface.make_sphere_surface(2, 8)
+    tree = build_box_tree(disc.points, 3 * np.pi)
+    for d in range(1, tree.depth + 1):
+        assert tree.level(d).pt_count.sum() == disc.n_points
+    for d in range(2, tree.depth + 1):
+        lvl, up = tree.level(d), tree.level(d - 1)
+        for b in range(0, lvl.n_boxes, max(1, lvl.n_boxes // 13)):
+            u = np.concatenate([tree.box_points(d, q) for q in lvl.neighbors(b)])
+            cz = lvl.cousins(b)
+            v = (np.concatenate([tree.box_points(d, q) for q in cz])
+                 if cz.size else np.empty(0, int))
+            pu = np.concatenate([tree.box_points(d - 1, q)
+                                 for q in up.neighbors(lvl.parent[b])])
+            assert np.array_equal(np.sort(np.concatenate([u, v])), np.sort(pu))
+            assert np.intersect1d(u, v).size == 0
+
+
+def test_cousins_within_eta_and_covered():
+    disc = surface.make_sphere_surface(2, 8)
+    tree = build_box_tree(disc.points, 2 * np.pi)
+    hier = build_cone_hierarchy(tree)
+    for d in range(3, tree.depth + 1):
+        cl, lvl = hier.level(d), tree.level(d)
+        for b in range(lvl.n_boxes):
+            tg = cl.cpt_idx[cl.cpt_off[b]:cl.cpt_off[b + 1]]
+            if tg.size == 0:
+                continue
+            s, th, ph, _ = cone_coords(tree.points[tg], lvl.centers[b], lvl.side)
+            assert s.max() <= ETA + 1e-12
+            f = cl.seg_index(s, th, ph)
+            own = cl.segs_of(b)
+            assert np.all(own[np.minimum(np.searchsorted(own, f), own.size - 1)] == f)
+
+
+def test_parent_nodes_covered():
+    disc = surface.make_sphere_surface(2, 8)
+    tree = build_box_tree(disc.points, 2 * np.pi)
+    hier = build_cone_hierarchy(tree)
+    for d in range(tree.depth, 3, -1):
+        cl, lvl = hier.level(d), tree.level(d)
+        pcl, up = hier.level(d - 1), tree.level(d - 1)
+        for b in range(lvl.n_boxes):
+            own, ps = cl.segs_of(b), pcl.segs_of(lvl.parent[b])
+            if own.size == 0 or ps.size == 0:
+                continue
+            xyz, _ = pcl.segment_nodes_xyz(ps, up.centers[lvl.parent[b]])
+            s, th, ph, _ = cone_coords(xyz.reshape(-1, 3), lvl.centers[b], lvl.side)
+            f = cl.seg_index(s, th, ph)
+            assert np.all(own[np.minimum(np.searchsorted(own, f), own.size - 1)] == f)
+
+
+def test_no_cones_without_cousins():
+    pts = np.random.default_rng(3).normal(size=(40, 3)) * 0.02
+    tree = build_box_tree(pts, 1.0)
+    assert not build_cone_hierarchy(tree).cone_levels
+
+
+def test_cone_count_doubling_follows_code():
+    """n_s doubles toward COARSER levels wherever kappa*H_d > 1/2 (reference
+    ifgf.py:426-429; the reference's own test_cone_counts_growth encodes the
+    other reading and fails)."""
+    inp = inputs("c1")
+    hier = inp["hier"]
+    ns = [hier.level(d).n_s for d in sorted(hier.cone_levels)]
+    assert ns == sorted(ns, reverse=True)
