@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark: IFGF-accelerated N-Muller matvec throughput on B200.
+
+metric  = unknowns * matvec / s  (4N unknowns per apply, BASELINE.json)
+value   = device throughput with y resident in HBM (CUDA events, L2 flushed
+          between steps)
+e2e     = same metric through the public host API (MullerOperator.apply on a
+          numpy vector: pinned staging, H2D, apply, D2H inside the timed call)
+
+Workload (BASELINE.json configs[1], cfg-2 family): unit dielectric sphere,
+eps_r = 2.25, 6 x n^2 patches on 10x10 Chebyshev grids, k0 = pi * n (fixed
+points per wavelength, reference cli.py:300-307), y ~ N(0,1) + i N(0,1)
+(seed 0), reference default IFGF parameters.  Default n = 4 (38,400
+unknowns).
+
+--impl reference: the reference algorithm's CPU implementation (the numpy
+oracle restatement, `oracle/`, since the reference is Python and cannot be
+compiled) on this host's cores, on a bounded sample of the same workload.
+
+Multi-GPU (torchrun, N > 1): every rank runs the full matvec of the same
+workload on its own GPU (replicas, no data-path collective); the timed
+region is barrier-bracketed and the max over ranks is reported.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FP64_PEAK_TFLOPS = 37.0   # DMMA m8n8k4 f64, measured (profiles/fp64_peak_r01.txt)
+W_PROP = 75 * 75 * 16 * 4          # FLOP per (parent segment, child) instance
+W_COEF = 16 * (3 * 3 * 25 + 5 * 5 * 15 + 5 * 5 * 15) * 4   # K3 per segment
+W_EMIT = 2 * 75 * 16 * 4           # per (box, target) pair, x and x + h n
+W_LEAF = 128                       # per (node, source) pair (2 kernels x 8 ch)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--n-refine", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gmres", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload(n_refine):
+    import numpy as np
+    from paper_2408_02274_b200 import surface
+    from paper_2408_02274_b200.operator import MaterialPair
+    disc = surface.make_sphere_surface(n_refine, 10)
+    k0 = np.pi * n_refine
+    mats = MaterialPair(1.0, 1.0, 2.25, 1.0, k0)
+    n = disc.n_points
+    rng = np.random.default_rng(0)
+    y = rng.normal(size=4 * n) + 1j * rng.normal(size=4 * n)
+    name = f"sphere(n_refine={n_refine}, n_c=10) k0={n_refine}pi eps_r=2.25"
+    return disc, mats, y, name
+
+
+def plan_inputs(disc, mats):
+    from paper_2408_02274_b200 import nearfield, octree
+    kmax = max(abs(mats.kappa_e), abs(mats.kappa_i))
+    tree = octree.build_box_tree(disc.points, kmax)
+    hier = octree.build_cone_hierarchy(tree)
+    smap = nearfield.classify_targets(disc)
+    mom = nearfield.compute_moments(disc, smap, nearfield.SingularQuadratureConfig(),
+                                    mats.kappas)
+    cp = nearfield.correction_pairs(disc, tree, smap)
+    return tree, hier, smap, mom, cp
+
+
+def work_counts(tree, hier):
+    """Algorithmic FLOP per matvec from the plan."""
+    from paper_2408_02274_b200 import octree
+    D = tree.depth
+    prop = {}
+    for d in range(4, D + 1):
+        ap = octree.accumulation_plan(tree, hier, d)
+        prop[d] = W_PROP * ap.n_instances + W_COEF * hier.level(d - 1).n_segments
+    cl, lvl = hier.level(D), tree.level(D)
+    leaf = W_LEAF * 75 * int((cl.seg_off[1:] - cl.seg_off[:-1]) @ lvl.pt_count)
+    emit = W_EMIT * sum(hier.level(d).cpt_idx.size for d in range(3, D + 1))
+    return {"prop_by_level": prop, "prop": sum(prop.values()), "leaf": leaf,
+            "leaf_coef": W_COEF * cl.n_segments, "emit": emit,
+            "total": sum(prop.values()) + leaf + W_COEF * cl.n_segments + emit}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = ROOT / "gpurun_out" / f"clocks_{index}_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.path.parent.mkdir(exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 8:
+                rows.append(parts)
+        try:
+            self.path.unlink()
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_baseline(disc, mats, y, inputs, budget_s, counts):
+    """The oracle (numpy restatement of the reference) on a bounded sample:
+    far field on every k-th box per level (scaled x k), near field and
+    assembly in full."""
+    import numpy as np
+    import oracle
+    tree, hier, smap, mom, cp = inputs
+    k = max(1, int(round(counts["total"] / 4.0e9 / budget_s)))
+    op = oracle.OperatorData(disc, mats, smap, mom, cp.ell_idx, cp.src_idx, tree, hier)
+    t0 = time.perf_counter()
+    import oracle.muller_oracle as mo
+    orig = mo.far_field
+    far_t = [0.0]
+
+    def sampled(*a, **kw):
+        kw["box_stride"] = k
+        t = time.perf_counter()
+        r = orig(*a, **kw)
+        far_t[0] += time.perf_counter() - t
+        return r
+
+    mo.far_field = sampled
+    try:
+        mo.muller_apply(op, y)
+    finally:
+        mo.far_field = orig
+    total = time.perf_counter() - t0
+    est = (total - far_t[0]) + far_t[0] * k
+    cores = os.cpu_count()
+    return {"value": 4 * disc.n_points / est, "unit": "unknowns*matvec/s",
+            "cores": cores, "kind": "port",
+            "sample": (f"oracle/ (numpy restatement of the reference) full near field + "
+                       f"assembly, far field on every {k}-th box of each level "
+                       f"(leaf, emission, propagation), far time scaled x{k}; "
+                       f"sample wall {total:.1f}s, estimated full matvec {est:.1f}s; "
+                       f"OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', cores)}")}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    disc, mats, y, name = workload(args.n_refine)
+    inputs = plan_inputs(disc, mats)
+    counts = work_counts(inputs[0], inputs[1])
+    per_step = min(15.0, 150.0 / max(1, args.steps + args.warmup))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(disc, mats, y, inputs, per_step, counts)
+        if i >= args.warmup:
+            vals.append(cb)
+    v = statistics.mean(c["value"] for c in vals)
+    t_step = 4 * disc.n_points / v
+    line = {"impl": "reference", "metric": "IFGF N-Muller matvec unknowns*matvec/s",
+            "value": v, "unit": "unknowns*matvec/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128/f64", "data": "synthetic (seeded N(0,1) densities)",
+            "config": {"workload": name, "unknowns": 4 * disc.n_points,
+                       "parallelism": "cpu"},
+            "cpu_baseline": {**vals[-1], "value": v},
+            "e2e": {"value": v, "unit": "unknowns*matvec/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2408_02274_b200.build import build
+    from paper_2408_02274_b200.engine import kernel_times, set_kernel_timing
+    from paper_2408_02274_b200.operator import MullerOperator
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        build()
+    if world > 1:
+        dist.barrier()
+    disc, mats, y, name = workload(args.n_refine)
+    t0 = time.time()
+    inputs = plan_inputs(disc, mats)
+    tree, hier, smap, mom, cp = inputs
+    op = MullerOperator(disc, mats, smap, mom, (cp.ell_idx, cp.src_idx),
+                        tree=tree, hierarchy=hier)
+    t_plan = time.time() - t0
+    counts = work_counts(tree, hier)
+    dev = torch.device("cuda", local)
+    yd = torch.from_numpy(y).to(dev)
+    out = torch.empty_like(yd)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(max(args.warmup, 3)):
+        op.apply_device(yd, out)
+    torch.cuda.synchronize()
+    launches_per_step = op.last_launches()
+    # ---- timed device loop (events per step, L2 flushed between steps)
+    set_kernel_timing(op.plan, True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record()
+            op.apply_device(yd, out)
+            evs[i][1].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_steps = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(ms_steps) / len(ms_steps)
+    ktimes = kernel_times(op.plan)
+    set_kernel_timing(op.plan, False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    # ---- end to end through the host API
+    y_host = np.ascontiguousarray(y)
+    op.apply(y_host)
+    e2e_t = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        op.apply(y_host)
+        e2e_t.append(time.perf_counter() - t)
+    e2e_s = sum(e2e_t) / len(e2e_t)
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    clocks = clk.summary()
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    unknowns = 4 * disc.n_points
+    value = world * unknowns / (ms * 1e-3)
+    prop_ms, prop_n = ktimes["propagate"]
+    prop_flop = counts["prop"] * args.steps
+    achieved = prop_flop / (prop_ms * 1e-3) / 1e12 if prop_ms > 0 else None
+    traffic = None
+    tf = ROOT / "profiles" / f"traffic_n{args.n_refine}.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("propagate_bytes_per_launch")
+    kern = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+            for k, v in ktimes.items() if v[1]}
+    line = {
+        "metric": "IFGF N-Muller matvec unknowns*matvec/s", "value": value,
+        "unit": "unknowns*matvec/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128/f64",
+        "data": "synthetic (seeded N(0,1) densities; analytic sphere mesh)",
+        "config": {"workload": name, "unknowns": unknowns, "points": disc.n_points,
+                   "depth": tree.depth, "segments": int(sum(hier.level(d).n_segments
+                                                            for d in hier.cone_levels)),
+                   "algorithmic_gflop_per_matvec": counts["total"] / 1e9,
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "parallelism": "replicas" if world > 1 else "single-gpu",
+                   "plan_build_s": round(t_plan, 1)},
+        "roofline": {"kernel": "propagate (K4: child->parent re-interpolation on "
+                               "FP64 DMMA + fused K3)",
+                     "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": (achieved / FP64_PEAK_TFLOPS
+                                                 if achieved else None),
+                     "traffic": traffic,
+                     "flop_per_launch": counts["prop"] / max(1, prop_n // args.steps),
+                     "ms_per_launch": prop_ms / max(1, prop_n),
+                     "peak_source": "FP64 mma.sync m8n8k4 measured on B200 "
+                                    "(tools/fp64_peak.cu, profiles/fp64_peak_r01.txt); "
+                                    "MEASURED_PEAKS.json has no FP64 entry",
+                     "share_of_step": prop_ms / args.steps / ms},
+        "kernels": kern,
+        "e2e": {"value": world * unknowns / e2e_s, "unit": "unknowns*matvec/s",
+                "h2d_bytes_per_step": unknowns * 16, "d2h_bytes_per_step": unknowns * 16},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(disc, mats, y, inputs, 15.0, counts)
+    if world == 1 and not args.no_gmres:
+        line["gmres"] = gmres_cfg1()
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def gmres_cfg1():
+    """BASELINE cfg 1 GMRES: sphere (2,10), k0 = 2 pi, tol 1e-6, x-polarised
+    plane wave exp(i k0 z); reference: 38 iterations, 719-762 s on 8 cores."""
+    import numpy as np
+    from paper_2408_02274_b200 import surface
+    from paper_2408_02274_b200.fields import plane_wave
+    from paper_2408_02274_b200.operator import MaterialPair, build_muller_operator
+    from paper_2408_02274_b200.solver import gmres
+    disc = surface.make_sphere_surface(2, 10)
+    k0 = 2 * np.pi
+    op = build_muller_operator(disc, MaterialPair(1.0, 1.0, 2.25, 1.0, k0))
+    b = op.rhs(plane_wave(k0, direction=(0.0, 0.0, 1.0), polarization=(1.0, 0.0, 0.0),
+                          omega=k0))
+    gmres(op, b, tol=1e-6, max_iter=300)
+    x, rep = gmres(op, b, tol=1e-6, max_iter=300)
+    return {"config": "cfg1 sphere(2,10) k0=2pi eps_r=2.25, tol 1e-6", "iterations":
+            rep.iterations, "final_residual": rep.residuals[-1], "solve_s": rep.wall_time}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

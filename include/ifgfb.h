@@ -218,6 +218,15 @@ int ifgfb_arnoldi_mgs(double* basis, int64_t ld, int k, int64_t n, double* w,
 int ifgfb_basis_combine(const double* basis, int64_t ld, int k, int64_t n,
                         const double* y, double* x, void* stream);
 
+/* Per-kernel-class CUDA-event timing (recorded on the launching stream).
+ * Classes: 0 leaf (K2+K3), 1 propagation (K4+K3), 2 emission (K5),
+ * 3 emission reduce, 4 near field (K6), 5 density pack (K1),
+ * 6 assembly (K7), 7 other.  set_timing resets the accumulators;
+ * kernel_times synchronises and returns total ms and launch counts. */
+#define IFGFB_KERNEL_KINDS 8
+int ifgfb_plan_set_timing(ifgfb_plan* plan, int enable);
+int ifgfb_plan_kernel_times(ifgfb_plan* plan, double* ms, int64_t* counts);
+
 /* Number of kernels launched by the last apply on this plan. */
 int64_t ifgfb_plan_last_launches(const ifgfb_plan* plan);
 

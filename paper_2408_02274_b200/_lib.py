@@ -14,6 +14,9 @@ import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libifgfb200.so"
 
+KERNEL_KINDS = ("leaf", "propagate", "emit", "emit_reduce", "near",
+                "pack", "assemble", "other")
+
 IFGFB_OK = 0
 IFGFB_ERR_ARG = -1
 
@@ -85,6 +88,8 @@ EXPORTS = {
     "ifgfb_plan_destroy": ([C.c_void_p], C.c_int),
     "ifgfb_plan_device_bytes": ([C.c_void_p], C.c_int64),
     "ifgfb_plan_last_launches": ([C.c_void_p], C.c_int64),
+    "ifgfb_plan_set_timing": ([C.c_void_p, C.c_int], C.c_int),
+    "ifgfb_plan_kernel_times": ([C.c_void_p, _dp, _ip], C.c_int),
     "ifgfb_far_apply": ([C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int,
                          C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_potentials": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

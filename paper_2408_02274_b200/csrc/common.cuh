@@ -82,6 +82,60 @@ struct DevArray {
   size_t n = 0;
 };
 
+// ------------------------------------------------------- kernel timing --
+// Optional CUDA-event timing of every kernel class (enabled through
+// ifgfb_plan_set_timing); events are recorded on the launching stream.
+enum KernelKind {
+  K_LEAF = 0, K_ACCUM, K_EMIT, K_REDUCE, K_NEAR, K_PACK, K_ASSEMBLE, K_OTHER,
+  K_NKINDS
+};
+
+struct KTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<int> kinds;
+  double ms[K_NKINDS] = {};
+  int64_t count[K_NKINDS] = {};
+
+  cudaEvent_t next() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  // returns a token (index of the start event) or -1 when off
+  int begin(int kind, cudaStream_t st) {
+    if (!on) return -1;
+    const int tok = (int)used;
+    cudaEventRecord(next(), st);
+    kinds.push_back(kind);
+    return tok;
+  }
+  void end(int tok, cudaStream_t st) {
+    if (tok < 0) return;
+    cudaEventRecord(next(), st);
+  }
+  // fold recorded pairs into the accumulators (synchronises the events)
+  void collect() {
+    for (size_t i = 0; i < kinds.size(); ++i) {
+      float t = 0.f;
+      cudaEventSynchronize(pool[2 * i + 1]);
+      cudaEventElapsedTime(&t, pool[2 * i], pool[2 * i + 1]);
+      ms[kinds[i]] += t;
+      count[kinds[i]] += 1;
+    }
+    kinds.clear();
+    used = 0;
+  }
+  void reset() {
+    collect();
+    for (int k = 0; k < K_NKINDS; ++k) { ms[k] = 0; count[k] = 0; }
+  }
+};
+
 // ------------------------------------------------------------------ plan --
 struct Level {
   int d = 0, n_boxes = 0, n_s = 0, n_a = 0;
@@ -159,6 +213,7 @@ struct Plan {
   double* dev_y = nullptr;      // 4N complex
   double* dev_out = nullptr;    // 4N complex
   int64_t launches = 0;
+  KTimer timer;
   size_t bytes = 0;
   std::vector<void*> allocations;
 };

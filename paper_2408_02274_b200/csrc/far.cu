@@ -456,7 +456,9 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
                   reinterpret_cast<const double2*>(p.wt), {kr[0], kr[1]},
                   {ki[0], ki[1]}, p.coef[cur]};
       if (L.n_seg > 0) {
+        const int tk = p.timer.begin(K_LEAF, st);
         leaf_kernel<NK><<<L.n_seg, 128, 0, st>>>(la);
+        p.timer.end(tk, st);
         ++launches;
       }
     }
@@ -467,11 +469,15 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
                     out_disp ? L.geom_disp : nullptr, p.coef[cur],
                     {kr[0], kr[1]}, {ki[0], ki[1]},
                     reinterpret_cast<double2*>(p.partial)};
+        int tk = p.timer.begin(K_EMIT, st);
         emit_kernel<NK><<<(L.n_etiles + 3) / 4, 128, 0, st>>>(ea);
+        p.timer.end(tk, st);
+        tk = p.timer.begin(K_REDUCE, st);
         emit_reduce<<<(n * NCOL + threads - 1) / threads, threads, 0, st>>>(
             n, L.tgt_off, L.tgt_pairs, reinterpret_cast<const double2*>(p.partial),
             reinterpret_cast<double2*>(p.out_tree),
             out_disp ? reinterpret_cast<double2*>(p.out_disp_tree) : nullptr);
+        p.timer.end(tk, st);
         launches += 2;
       }
       if (d > 3 && L.has_accum) {
@@ -481,7 +487,9 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
                      L.groups, L.scatter, L.tgeom, p.coef[cur], p.coef[cur ^ 1],
                      {kr[0], kr[1]}, {ki[0], ki[1]}};
           const size_t sm = sizeof(double2) * NN * NCOL * ACC_WARPS;
+          const int tk = p.timer.begin(K_ACCUM, st);
           accum_kernel<NK><<<U.n_seg, 128, sm, st>>>(aa);
+          p.timer.end(tk, st);
           ++launches;
         }
         cur ^= 1;

@@ -422,7 +422,9 @@ int potentials_from_phi(Plan& p, cudaStream_t st) {
               {p.kappa[0], p.kappa[2]}, {p.kappa[1], p.kappa[3]}, p.fd_step,
               reinterpret_cast<double2*>(p.s_val), reinterpret_cast<double2*>(p.d_val)};
   const int warps_per_block = 4;
+  const int tk = p.timer.begin(K_NEAR, st);
   near_kernel<<<(p.n + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(na);
+  p.timer.end(tk, st);
   p.launches += 1;
   IFGFB_CUDA(cudaGetLastError());
   return IFGFB_OK;
@@ -433,10 +435,12 @@ static int pack_launch(Plan& p, const double* y, const double* phi_in,
   const int n2 = p.n_c * p.n_c;
   const int threads = ((n2 + 31) / 32) * 32;
   const size_t sm = sizeof(double2) * 20 * n2;
+  const int tk = p.timer.begin(K_PACK, st);
   pack_kernel<<<p.n_patches, threads, sm, st>>>(
       surf(p), reinterpret_cast<const double2*>(y),
       reinterpret_cast<const double2*>(phi_in), reinterpret_cast<double2*>(p.phi),
       reinterpret_cast<double2*>(p.phiw), reinterpret_cast<double2*>(p.pcoef));
+  p.timer.end(tk, st);
   p.launches += 1;
   IFGFB_CUDA(cudaGetLastError());
   return IFGFB_OK;
@@ -457,7 +461,9 @@ int muller_apply(Plan& p, const double* y, double* out, cudaStream_t st) {
              make_double2(p.eps_i[0], p.eps_i[1]), make_double2(p.mu_i[0], p.mu_i[1]),
              {make_double2(p.kappa[0], p.kappa[1]), make_double2(p.kappa[2], p.kappa[3])},
              p.omega, reinterpret_cast<double2*>(out)};
+  const int tk = p.timer.begin(K_ASSEMBLE, st);
   assemble_kernel<<<p.n_patches, threads, sizeof(double2) * 16 * n2, st>>>(aa);
+  p.timer.end(tk, st);
   p.launches += 1;
   IFGFB_CUDA(cudaGetLastError());
   return IFGFB_OK;

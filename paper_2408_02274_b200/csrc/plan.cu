@@ -272,6 +272,23 @@ int64_t ifgfb_plan_device_bytes(const ifgfb_plan* h) {
   return h ? (int64_t)h->p.bytes : 0;
 }
 
+int ifgfb_plan_set_timing(ifgfb_plan* h, int enable) {
+  CHECK_ARG(h, "null argument");
+  h->p.timer.reset();
+  h->p.timer.on = enable != 0;
+  return IFGFB_OK;
+}
+
+int ifgfb_plan_kernel_times(ifgfb_plan* h, double* ms, int64_t* counts) {
+  CHECK_ARG(h && ms && counts, "null argument");
+  h->p.timer.collect();
+  for (int k = 0; k < K_NKINDS; ++k) {
+    ms[k] = h->p.timer.ms[k];
+    counts[k] = h->p.timer.count[k];
+  }
+  return IFGFB_OK;
+}
+
 int64_t ifgfb_plan_last_launches(const ifgfb_plan* h) {
   return h ? h->p.launches : 0;
 }

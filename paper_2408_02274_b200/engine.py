@@ -238,3 +238,18 @@ def ifgf_apply(tree, hier, weights, kappas, mode: str | None = None,
         if od is not None:
             od[c0:c1] = o_d.cpu().numpy()
     return out, od
+
+
+def set_kernel_timing(plan: FarFieldPlan, enable: bool = True) -> None:
+    _lib.check(_lib.load().ifgfb_plan_set_timing(plan.handle, int(enable)),
+               "ifgfb_plan_set_timing")
+
+
+def kernel_times(plan: FarFieldPlan) -> dict:
+    """{kind: (total_ms, launches)} since the last set_kernel_timing."""
+    ms = np.zeros(len(_lib.KERNEL_KINDS))
+    cnt = np.zeros(len(_lib.KERNEL_KINDS), dtype=np.int64)
+    _lib.check(_lib.load().ifgfb_plan_kernel_times(
+        plan.handle, _lib.dptr(ms), _lib.iptr(cnt)), "ifgfb_plan_kernel_times")
+    return {k: (float(ms[i]), int(cnt[i]))
+            for i, k in enumerate(_lib.KERNEL_KINDS)}
