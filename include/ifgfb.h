@@ -99,19 +99,20 @@ typedef struct {
 
 /* ---- propagation child level d -> parent level d-1 (reference _AccumType /
  *      _accum_types / _accumulate_level, ifgf.py:676-785), regrouped per
- *      parent segment row (owner computes). */
+ *      parent segment row (owner computes).  Each CTA owns one parent
+ *      segment; warp w (0..4) owns the 15 parent nodes with theta index
+ *      b == w.  Per type (parent segment id, child octant) and warp, its
+ *      owned nodes are grouped by child segment into MMA row tiles of <= 8. */
 typedef struct {
   int32_t level;             /* child level d */
   int64_t n_types;
-  const int64_t* sig_off;    /* n_types+1 into the group arrays */
-  const int64_t* group_start;/* per group: first sorted node slot (0..74) */
-  const int64_t* group_end;  /* per group: one past last slot */
-  const int64_t* scatter;    /* n_types*nn: parent node slot of sorted node */
-  const double* xs;          /* n_types*nn local coords in the child segment */
-  const double* xt;
-  const double* xp;
-  const double* r_parent;    /* n_types*nn */
-  const double* r_child;     /* n_types*nn */
+  const int64_t* tile_off;   /* n_types*5+1: tiles of (type, warp) */
+  int64_t n_tiles;
+  const uint8_t* tiles;      /* n_tiles*16: [local sigma group, n_rows,
+                                slot0..slot7 (a*5+c, 0xFF pad), 6 pad] */
+  const double* node_geom;   /* n_types*75*3: xs, xt, xp of each parent node
+                                in its child segment (parent node order) */
+  const double* node_r;      /* n_types*75*2: r_parent, r_child */
   int64_t n_parent_rows;     /* segments of level d-1 */
   const int64_t* inst_off;   /* n_parent_rows+1 */
   int64_t n_instances;

@@ -49,12 +49,11 @@ class EmitDesc(C.Structure):
 
 class AccumDesc(C.Structure):
     _fields_ = [("level", C.c_int32), ("n_types", C.c_int64),
-                ("sig_off", _ip), ("group_start", _ip), ("group_end", _ip),
-                ("scatter", _ip), ("xs", _dp), ("xt", _dp), ("xp", _dp),
-                ("r_parent", _dp), ("r_child", _dp),
-                ("n_parent_rows", C.c_int64), ("inst_off", _ip),
-                ("n_instances", C.c_int64), ("inst_type", _ip),
-                ("inst_crow_off", _ip), ("crow", _ip)]
+                ("tile_off", _ip), ("n_tiles", C.c_int64),
+                ("tiles", C.POINTER(C.c_uint8)), ("node_geom", _dp),
+                ("node_r", _dp), ("n_parent_rows", C.c_int64),
+                ("inst_off", _ip), ("n_instances", C.c_int64),
+                ("inst_type", _ip), ("inst_crow_off", _ip), ("crow", _ip)]
 
 
 class SurfaceDesc(C.Structure):

@@ -14,7 +14,14 @@ constexpr int PA = 5;          // angular interpolation order
 constexpr int NN = PS * PA * PA;  // 75 nodes per cone segment
 constexpr int NCOL = 16;       // complex columns carried per traversal
 constexpr int NRCOL = 2 * NCOL;   // 32 real columns
-constexpr int SEG_DOUBLES = NN * NRCOL;  // 2400 doubles = 19.2 KB per segment
+// Coefficients of one segment are stored in DMMA B-fragment order:
+// [ks 0..19][lane 0..31][column tile 0..3] doubles, ks = 5q + c covering the
+// coefficient rows i = (4q + (lane&3))*5 + c (zero when 4q + (lane&3) >= 15),
+// column = 8*tile + (lane>>2) of the 32 real columns (re/im of 16 complex).
+constexpr int KSTEPS = 20;
+constexpr int SEG_DOUBLES = KSTEPS * 32 * 4;  // 2560 doubles = 20 KB per segment
+constexpr int WARP_PARTS = 5;                 // propagation: node owners per CTA
+constexpr int PART_NODES = NN / WARP_PARTS;   // 15 parent nodes per warp
 
 void set_error(const std::string& msg);
 
@@ -160,10 +167,11 @@ struct Level {
   // accumulation from this level (as child) into level d-1
   bool has_accum = false;
   int64_t n_types = 0;
-  int* sig_off = nullptr;      // n_types+1
-  int2* groups = nullptr;      // (start, end)
-  unsigned char* scatter = nullptr;  // n_types*NN
-  double* tgeom = nullptr;     // n_types*NN*5 : xs, xt, xp, rp, rc
+  int* tile_off = nullptr;     // n_types*WARP_PARTS+1
+  uint4* tiles = nullptr;      // 16-byte tile records
+  double* node_geom = nullptr; // n_types*NN*3 (parent node order)
+  double* node_r = nullptr;    // n_types*NN*2 (r_parent, r_child)
+  double* ratio = nullptr;     // workspace n_types*NN*2 complex
   int* inst_off = nullptr;     // parent rows + 1
   int* inst_type = nullptr;
   int* inst_crow_off = nullptr;

@@ -103,10 +103,23 @@ __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
   __syncthreads();
 }
 
+// Write one segment's coefficients V[i][m] (node-major complex) in DMMA
+// B-fragment order (see SEG_DOUBLES): coalesced stores, padding zeroed.
 __device__ __forceinline__ void store_segment(double* dst, const double2* V,
                                               int tid, int nthr) {
-  double2* d2 = reinterpret_cast<double2*>(dst);
-  for (int i = tid; i < NN * NCOL; i += nthr) d2[i] = V[i];
+  for (int idx = tid; idx < SEG_DOUBLES; idx += nthr) {
+    const int ks = idx >> 7, lane = (idx >> 2) & 31, nt = idx & 3;
+    const int q = ks / PA, c = ks - PA * q;
+    const int ab = 4 * q + (lane & 3);
+    double v = 0.0;
+    if (ab < PS * PA) {
+      const int i = ab * PA + c;
+      const int col = 8 * nt + (lane >> 2);
+      const double2 z = V[i * NCOL + (col >> 1)];
+      v = (col & 1) ? z.y : z.x;
+    }
+    dst[idx] = v;
+  }
 }
 
 // ------------------------------------------------------------ weights ----
@@ -233,113 +246,120 @@ __device__ __forceinline__ BasisA make_basis(double xs, double xt, double xp,
   return B;
 }
 
-// acc[nt] (+)= sum_i basis_i * C[i][8nt + grp] over the 80-padded K range.
+// acc[nt] (+)= sum_i basis_i * C[i][8nt + grp]: 20 k-steps x 4 column tiles
+// of DMMA; the B fragments of a k-step are one coalesced 32-byte load per
+// lane from the fragment-ordered segment.
 template <bool EXACT>
 __device__ __forceinline__ void basis_times_block(const BasisA& B,
                                                   const double* __restrict__ C,
-                                                  int grp, int tig,
-                                                  double (&c0)[4],
+                                                  int lane, double (&c0)[4],
                                                   double (&c1)[4]) {
+  const double4* F = reinterpret_cast<const double4*>(C) + lane;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const bool ok = (4 * q + tig) < PS * PA;
 #pragma unroll
     for (int c = 0; c < PA; ++c) {
+      const double4 b = F[(5 * q + c) * 32];
       const double av = EXACT ? mul_rn(B.tst[q], B.tp[c]) : B.tst[q] * B.tp[c];
-      const int i = (4 * q + tig) * PA + c;
-      const double* src = C + i * NRCOL + grp;
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const double bv = ok ? __ldg(src + 8 * nt) : 0.0;
-        dmma(c0[nt], c1[nt], av, bv);
-      }
+      dmma(c0[0], c1[0], av, b.x);
+      dmma(c0[1], c1[1], av, b.y);
+      dmma(c0[2], c1[2], av, b.z);
+      dmma(c0[3], c1[3], av, b.w);
     }
   }
 }
 
 // ---------------------------------------------------------------- K4 ----
+// ratio[t][j][k] = (r_p / r_c) exp(i kappa_k (r_c - r_p)) per type and parent
+// node (reference ifgf.py:772-773), tabulated once per apply and level.
+template <int NK>
+__global__ void ratio_kernel(int64_t n, const double* __restrict__ node_r,
+                             double kr0, double ki0, double kr1, double ki1,
+                             double2* __restrict__ ratio) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  const double rp = node_r[2 * idx], rc = node_r[2 * idx + 1];
+  const double q = rp / rc;
+  const double2 e0 = cexp_ikx(kr0, ki0, rc - rp);
+  ratio[idx * NK] = make_double2(q * e0.x, q * e0.y);
+  if (NK > 1) {
+    const double2 e1 = cexp_ikx(kr1, ki1, rc - rp);
+    ratio[idx * NK + 1] = make_double2(q * e1.x, q * e1.y);
+  }
+}
+
 struct AccArgs {
   const int* inst_off; const int* inst_type; const int* inst_crow_off;
-  const int* crow; const int* sig_off; const int2* groups;
-  const unsigned char* scatter; const double* tgeom;
+  const int* crow; const int* tile_off; const uint4* tiles;
+  const double* node_geom; const double2* ratio;
   const double* coef_child; double* coef_parent;
-  double kr[2], ki[2];
 };
 
-constexpr int ACC_WARPS = 4;
-
-// One CTA per parent segment row (owner computes, no atomics): every
-// (parent segment, child box) instance re-interpolates the child's
-// coefficients at the parent's 75 nodes (tiles of 8 nodes sharing a child
-// segment sigma, 20 k-steps x 4 column tiles of DMMA), multiplies by the
-// re-centering ratio (r_p/r_c) exp(i kappa (r_c - r_p)) and accumulates into
-// a per-warp shared buffer; the 4 buffers are summed in fixed order (bitwise
-// deterministic), transformed to coefficients (K3) and written once.
+// One CTA (5 warps) per parent segment row, owner computes: warp w owns the
+// 15 parent nodes with theta index b == w and keeps their 16-column
+// accumulators in its own shared slice (no atomics, no inter-warp hazards,
+// every warp walks every (parent segment, child) instance -> balanced).
+// Per instance each warp re-interpolates the child's coefficients at its
+// nodes: row tiles of <= 8 nodes sharing a child segment sigma, 20 k-steps x
+// 4 column tiles of FP64 DMMA, times the re-centering ratio.  The summed
+// values are transformed to coefficients (K3) and written once.
 template <int NK>
-__global__ void __launch_bounds__(128, 2) accum_kernel(AccArgs a) {
-  extern __shared__ double2 smem[];
+__global__ void __launch_bounds__(160, 3) accum_kernel(AccArgs a) {
+  __shared__ double2 acc[WARP_PARTS * PART_NODES * NCOL];   // 19.2 KB
+  __shared__ double2 V[NN * NCOL];                          // 19.2 KB
   const int p = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, tig = lane & 3;
-  double2* acc = smem + warp * NN * NCOL;
-  for (int i = lane; i < NN * NCOL; i += 32) acc[i] = make_double2(0.0, 0.0);
+  double2* mine = acc + warp * PART_NODES * NCOL;
+  for (int i = lane; i < PART_NODES * NCOL; i += 32) mine[i] = make_double2(0.0, 0.0);
   __syncwarp();
   const int i0 = a.inst_off[p], i1 = a.inst_off[p + 1];
-  int tau = 0;
   for (int inst = i0; inst < i1; ++inst) {
     const int t = a.inst_type[inst];
-    const int g0 = a.sig_off[t], g1 = a.sig_off[t + 1];
-    const int cb = a.inst_crow_off[inst];
-    const double* tg = a.tgeom + (size_t)t * NN * 5;
-    const unsigned char* sc = a.scatter + (size_t)t * NN;
-    for (int g = g0; g < g1; ++g) {
-      const int2 se = a.groups[g];
-      const double* C = a.coef_child + (size_t)a.crow[cb + g - g0] * SEG_DOUBLES;
-      for (int r0 = se.x; r0 < se.y; r0 += 8, ++tau) {
-        if ((tau % ACC_WARPS) != warp) continue;
-        const int row = r0 + grp;
-        const bool valid = row < se.y;
-        const int j = valid ? row : se.y - 1;
-        const BasisA B = make_basis<false>(tg[j], tg[NN + j], tg[2 * NN + j], tig);
-        double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
-        basis_times_block<false>(B, C, grp, tig, c0, c1);
-        const double rp = tg[3 * NN + j], rc = tg[4 * NN + j];
-        const double q = rp / rc;
-        double2 ratio[NK];
+    const int* cr = a.crow + a.inst_crow_off[inst];
+    const int k0 = a.tile_off[t * WARP_PARTS + warp];
+    const int k1 = a.tile_off[t * WARP_PARTS + warp + 1];
+    for (int k = k0; k < k1; ++k) {
+      const uint4 tl = a.tiles[k];
+      const int g = tl.x & 0xff, nrows = (tl.x >> 8) & 0xff;
+      const int byte = 2 + grp;                    // slot byte of this row
+      const unsigned word = byte < 4 ? tl.x : byte < 8 ? tl.y : tl.z;
+      const int slot0 = (tl.x >> 16) & 0xff;
+      const bool valid = grp < nrows;
+      const int slot = valid ? (int)((word >> (8 * (byte & 3))) & 0xff) : slot0;
+      const int node = (slot / PA) * PA * PA + warp * PA + slot % PA;
+      const double* ng = a.node_geom + ((size_t)t * NN + node) * 3;
+      const BasisA B = make_basis<false>(ng[0], ng[1], ng[2], tig);
+      double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+      basis_times_block<false>(B, a.coef_child + (size_t)cr[g] * SEG_DOUBLES, lane,
+                               c0, c1);
+      if (valid) {
+        const double2* rt = a.ratio + ((size_t)t * NN + node) * NK;
+        const double2 r0 = rt[0];
+        const double2 r1 = NK > 1 ? rt[NK - 1] : r0;
+        double2* dst = mine + slot * NCOL;
 #pragma unroll
-        for (int k = 0; k < NK; ++k) {
-          const double2 e = cexp_ikx(a.kr[k], a.ki[k], rc - rp);
-          ratio[k] = make_double2(q * e.x, q * e.y);
+        for (int nt = 0; nt < 4; ++nt) {
+          const int m = 4 * nt + tig;
+          const double2 v = cmul(make_double2(c0[nt], c1[nt]),
+                                 (NK > 1 && (tig & 1)) ? r1 : r0);
+          dst[m].x += v.x;
+          dst[m].y += v.y;
         }
-        if (valid) {
-          double2* dst = acc + sc[j] * NCOL;
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt) {
-            const int m = 4 * nt + tig;
-            const double2 v = cmul(make_double2(c0[nt], c1[nt]),
-                                   (NK > 1 && (tig & 1)) ? ratio[NK - 1] : ratio[0]);
-            dst[m].x += v.x;
-            dst[m].y += v.y;
-          }
-        }
-        __syncwarp();
       }
+      __syncwarp();
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < NN * NCOL; i += blockDim.x) {
-    double2 s = smem[i];
-#pragma unroll
-    for (int w = 1; w < ACC_WARPS; ++w) {
-      const double2 v = smem[w * NN * NCOL + i];
-      s.x += v.x;
-      s.y += v.y;
-    }
-    smem[i] = s;
+  for (int idx = threadIdx.x; idx < NN * NCOL; idx += blockDim.x) {
+    const int node = idx / NCOL, m = idx - node * NCOL;
+    const int b = (node / PA) % PA;
+    const int slot = (node / (PA * PA)) * PA + node % PA;
+    V[idx] = acc[(b * PART_NODES + slot) * NCOL + m];
   }
   __syncthreads();
-  to_coeffs_smem(smem, threadIdx.x, blockDim.x);
-  store_segment(a.coef_parent + (size_t)p * SEG_DOUBLES, smem, threadIdx.x,
+  to_coeffs_smem(V, threadIdx.x, blockDim.x);
+  store_segment(a.coef_parent + (size_t)p * SEG_DOUBLES, V, threadIdx.x,
                 blockDim.x);
 }
 
@@ -371,7 +391,7 @@ __global__ void __launch_bounds__(128) emit_kernel(EmitArgs a) {
   const double4 gm = (pt && has_disp) ? a.geom_disp[pos] : a.geom[pos];
   const BasisA B = make_basis<true>(gm.x, gm.y, gm.z, tig);
   double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
-  basis_times_block<true>(B, a.coef + (size_t)td.x * SEG_DOUBLES, grp, tig, c0, c1);
+  basis_times_block<true>(B, a.coef + (size_t)td.x * SEG_DOUBLES, lane, c0, c1);
   if (!valid) return;
   const double r = gm.w;
   const double den = mul_rn(4.0 * M_PI, r);
@@ -483,14 +503,19 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
       if (d > 3 && L.has_accum) {
         Level& U = p.levels[d - 1];
         if (U.n_seg > 0) {
-          AccArgs aa{L.inst_off, L.inst_type, L.inst_crow_off, L.crow, L.sig_off,
-                     L.groups, L.scatter, L.tgeom, p.coef[cur], p.coef[cur ^ 1],
-                     {kr[0], kr[1]}, {ki[0], ki[1]}};
-          const size_t sm = sizeof(double2) * NN * NCOL * ACC_WARPS;
-          const int tk = p.timer.begin(K_ACCUM, st);
-          accum_kernel<NK><<<U.n_seg, 128, sm, st>>>(aa);
+          const int64_t nr = L.n_types * NN;
+          int tk = p.timer.begin(K_OTHER, st);
+          ratio_kernel<NK><<<(unsigned)((nr + 255) / 256), 256, 0, st>>>(
+              nr, L.node_r, kr[0], ki[0], kr[1], ki[1],
+              reinterpret_cast<double2*>(L.ratio));
           p.timer.end(tk, st);
-          ++launches;
+          AccArgs aa{L.inst_off, L.inst_type, L.inst_crow_off, L.crow, L.tile_off,
+                     L.tiles, L.node_geom, reinterpret_cast<const double2*>(L.ratio),
+                     p.coef[cur], p.coef[cur ^ 1]};
+          tk = p.timer.begin(K_ACCUM, st);
+          accum_kernel<NK><<<U.n_seg, 32 * WARP_PARTS, 0, st>>>(aa);
+          p.timer.end(tk, st);
+          launches += 2;
         }
         cur ^= 1;
       }
@@ -512,16 +537,7 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
   return IFGFB_OK;
 }
 
-int far_setup_kernels() {
-  int rc = init_constants();
-  if (rc) return rc;
-  const int sm = sizeof(double2) * NN * NCOL * ACC_WARPS;
-  IFGFB_CUDA(cudaFuncSetAttribute(accum_kernel<1>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  IFGFB_CUDA(cudaFuncSetAttribute(accum_kernel<2>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  return IFGFB_OK;
-}
+int far_setup_kernels() { return init_constants(); }
 
 int far_apply(Plan& p, const double* w, int nch, const double* kappas, int nk,
               double* out, double* out_disp, cudaStream_t st) {

@@ -191,37 +191,24 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
   const int64_t nt = a->n_types;
   L.n_types = nt;
   std::vector<int> tmp;
-  if (!to_i32(a->sig_off, nt + 1, tmp, "sig_off")) return IFGFB_ERR_ARG;
-  RC(dev_upload(p, &L.sig_off, tmp.data(), tmp.size()));
-  const int64_t ng = a->sig_off[nt];
-  std::vector<int2> grp(ng);
-  for (int64_t g = 0; g < ng; ++g) {
-    CHECK_ARG(a->group_start[g] >= 0 && a->group_end[g] <= NN &&
-                  a->group_start[g] < a->group_end[g], "bad sigma group bounds");
-    grp[g] = make_int2((int)a->group_start[g], (int)a->group_end[g]);
+  if (!to_i32(a->tile_off, nt * WARP_PARTS + 1, tmp, "tile_off")) return IFGFB_ERR_ARG;
+  CHECK_ARG(a->tile_off[nt * WARP_PARTS] == a->n_tiles, "tile_off end != n_tiles");
+  RC(dev_upload(p, &L.tile_off, tmp.data(), tmp.size()));
+  for (int64_t i = 0; i < a->n_tiles; ++i) {
+    const uint8_t* t = a->tiles + 16 * i;
+    CHECK_ARG(t[1] >= 1 && t[1] <= 8, "tile row count out of range");
+    for (int r = 0; r < t[1]; ++r)
+      CHECK_ARG(t[2 + r] < PART_NODES, "tile slot out of range");
   }
-  RC(dev_upload(p, &L.groups, grp.data(), grp.size()));
-  std::vector<unsigned char> sc(nt * NN);
-  for (int64_t i = 0; i < nt * NN; ++i) {
-    CHECK_ARG(a->scatter[i] >= 0 && a->scatter[i] < NN, "scatter slot out of range");
-    sc[i] = (unsigned char)a->scatter[i];
-  }
-  RC(dev_upload(p, &L.scatter, sc.data(), sc.size()));
-  std::vector<double> geo(nt * NN * 5);
-  for (int64_t t = 0; t < nt; ++t)
-    for (int j = 0; j < NN; ++j) {
-      const int64_t src = t * NN + j;
-      double* dst = geo.data() + t * NN * 5;
-      dst[j] = a->xs[src];
-      dst[NN + j] = a->xt[src];
-      dst[2 * NN + j] = a->xp[src];
-      dst[3 * NN + j] = a->r_parent[src];
-      dst[4 * NN + j] = a->r_child[src];
-    }
-  RC(dev_upload(p, &L.tgeom, geo.data(), geo.size()));
+  RC(dev_upload(p, &L.tiles, reinterpret_cast<const uint4*>(a->tiles), (size_t)a->n_tiles));
+  RC(dev_upload(p, &L.node_geom, a->node_geom, (size_t)nt * NN * 3));
+  RC(dev_upload(p, &L.node_r, a->node_r, (size_t)nt * NN * 2));
+  RC(dev_alloc(p, &L.ratio, (size_t)nt * NN * 4));
   if (!to_i32(a->inst_off, a->n_parent_rows + 1, tmp, "inst_off")) return IFGFB_ERR_ARG;
   RC(dev_upload(p, &L.inst_off, tmp.data(), tmp.size()));
   L.n_instances = a->n_instances;
+  for (int64_t i = 0; i < a->n_instances; ++i)
+    CHECK_ARG(a->inst_type[i] >= 0 && a->inst_type[i] < nt, "inst_type out of range");
   if (!to_i32(a->inst_type, a->n_instances, tmp, "inst_type")) return IFGFB_ERR_ARG;
   RC(dev_upload(p, &L.inst_type, tmp.data(), tmp.size()));
   if (!to_i32(a->inst_crow_off, a->n_instances + 1, tmp, "inst_crow_off")) return IFGFB_ERR_ARG;

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .octree import accumulation_plan, emission_plan
+from .octree import accumulation_plan, emission_plan, warp_tiles
 
 __all__ = ["FarFieldPlan", "ifgf_apply", "device_stream"]
 
@@ -107,31 +107,27 @@ class FarFieldPlan:
 
     def _add_accum(self, lib, d):
         ap = accumulation_plan(self.tree, self.hier, d)
-        if ap.crow_misses:
-            # the reference silently uses the neighbouring row in that case
-            # (searchsorted, ifgf.py:743-746); we reproduce the same rows.
-            pass
-        a = dict(sig_off=_c(ap.sig_off, np.int64),
-                 gs=_c(ap.group_bounds, np.int64),
-                 ge=_c(ap.group_end, np.int64),
-                 sc=_c(ap.scatter, np.int64), xs=_c(ap.xs, np.float64),
-                 xt=_c(ap.xt, np.float64), xp=_c(ap.xp, np.float64),
-                 rp=_c(ap.r_parent, np.float64), rc=_c(ap.r_child, np.float64),
+        # crow rows are reproduced exactly as the reference's searchsorted
+        # picks them (ifgf.py:743-746), including any inexact hit.
+        tile_off, tiles, node_geom, node_r = warp_tiles(ap)
+        a = dict(to=_c(tile_off, np.int64), tl=np.ascontiguousarray(tiles),
+                 ng=_c(node_geom, np.float64), nr=_c(node_r, np.float64),
                  io=_c(ap.inst_off, np.int64), it=_c(ap.inst_type, np.int64),
                  ico=_c(ap.inst_crow_off, np.int64), cr=_c(ap.crow, np.int64))
         self._hold(*a.values())
         desc = _lib.AccumDesc(
-            d, ap.n_types, _lib.iptr(a["sig_off"]), _lib.iptr(a["gs"]),
-            _lib.iptr(a["ge"]), _lib.iptr(a["sc"]), _lib.dptr(a["xs"]),
-            _lib.dptr(a["xt"]), _lib.dptr(a["xp"]), _lib.dptr(a["rp"]),
-            _lib.dptr(a["rc"]), self.hier.level(d - 1).n_segments,
-            _lib.iptr(a["io"]), ap.n_instances, _lib.iptr(a["it"]),
-            _lib.iptr(a["ico"]), _lib.iptr(a["cr"]))
+            d, ap.n_types, _lib.iptr(a["to"]), tiles.shape[0],
+            a["tl"].ctypes.data_as(__import__("ctypes").POINTER(
+                __import__("ctypes").c_uint8)),
+            _lib.dptr(a["ng"]), _lib.dptr(a["nr"]),
+            self.hier.level(d - 1).n_segments, _lib.iptr(a["io"]),
+            ap.n_instances, _lib.iptr(a["it"]), _lib.iptr(a["ico"]),
+            _lib.iptr(a["cr"]))
         _lib.check(lib.ifgfb_plan_add_accum(self._h, desc),
                    f"ifgfb_plan_add_accum({d})")
         st = self.stats["levels"].setdefault(d, {})
         st.update(types=int(ap.n_types), instances=int(ap.n_instances),
-                  crow_misses=int(ap.crow_misses))
+                  crow_misses=int(ap.crow_misses), tiles=int(tiles.shape[0]))
 
     def _add_emission(self, lib, d, disp_t):
         ep = emission_plan(self.tree, self.hier, d, disp_t)

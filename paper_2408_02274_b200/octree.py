@@ -607,6 +607,85 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy,
     return plan
 
 
+WARP_PARTS = 5          # parent nodes owned per warp: fixed theta index b
+
+
+def warp_tiles(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5):
+    """Device tiling of every propagation type for the node-owner kernel.
+
+    The 75 parent nodes (a, b, c) are split into 5 fixed sets by the theta
+    index b (warp w owns the 15 nodes with b == w).  Per type and warp the
+    owned nodes are grouped by child segment (sigma group) and chunked into
+    MMA row tiles of <= 8 nodes.  Returns
+
+      tile_off   (n_types*5 + 1,) int64  tile range of (type, warp)
+      tiles      (n_tiles, 16)    uint8  [local group, n_rows, slot0..7, pad]
+                                         slot = a*p_a + c (0..14), 0xFF = pad
+      node_geom  (n_types, 75, 3) f64    xs, xt, xp in PARENT node order
+      node_r     (n_types, 75, 2) f64    r_parent, r_child in parent order
+    """
+    nn = p_s * p_a * p_a
+    nt = ap.n_types
+    gid = np.empty((nt, nn), dtype=np.int64)
+    node_geom = np.empty((nt, nn, 3))
+    node_r = np.empty((nt, nn, 2))
+    rows = np.arange(nt)[:, None]
+    # sorted slot j of type t holds parent node scatter[t, j]
+    gsorted = np.repeat(np.arange(ap.group_sigma.size) -
+                        np.repeat(ap.sig_off[:-1], np.diff(ap.sig_off)),
+                        ap.group_end - ap.group_bounds)
+    gid[rows, ap.scatter] = gsorted.reshape(nt, nn)
+    for k, arr in enumerate((ap.xs, ap.xt, ap.xp)):
+        node_geom[rows, ap.scatter, k] = arr
+    node_r[rows, ap.scatter, 0] = ap.r_parent
+    node_r[rows, ap.scatter, 1] = ap.r_child
+    b_of = (np.arange(nn) // p_a) % p_a
+    slot_of = (np.arange(nn) // (p_a * p_a)) * p_a + np.arange(nn) % p_a
+    tiles = []
+    counts = np.zeros(nt * WARP_PARTS, dtype=np.int64)
+    for w in range(WARP_PARTS):
+        nodes = np.nonzero(b_of == w)[0]               # parent order
+        g = gid[:, nodes]                              # (nt, 15)
+        order = np.argsort(g, axis=1, kind="stable")
+        gs = np.take_along_axis(g, order, axis=1)
+        sl = slot_of[nodes][order]                     # (nt, 15)
+        # run starts and positions inside each run
+        new = np.ones_like(gs, dtype=bool)
+        new[:, 1:] = gs[:, 1:] != gs[:, :-1]
+        run_id = np.cumsum(new, axis=1) - 1
+        start = np.zeros_like(gs)
+        idx = np.arange(gs.shape[1])[None, :].repeat(nt, 0)
+        start_pos = np.where(new, idx, 0)
+        start = np.maximum.accumulate(start_pos, axis=1)
+        pos = idx - start                              # position in run
+        tile_in_run = pos // 8
+        # tile key per element: (run_id, tile_in_run) -> consecutive ids
+        key = run_id * 2 + tile_in_run                 # runs are <= 15 long
+        newt = np.ones_like(key, dtype=bool)
+        newt[:, 1:] = key[:, 1:] != key[:, :-1]
+        tid = np.cumsum(newt, axis=1) - 1              # tile index per type
+        ntile = tid[:, -1] + 1
+        counts[np.arange(nt) * WARP_PARTS + w] = ntile
+        arr = np.full((nt, int(ntile.max()), 16), 0xFF, dtype=np.uint8)
+        arr[:, :, 1] = 0
+        tt, jj = np.nonzero(np.ones_like(gs, dtype=bool))
+        t_ = tid[tt, jj]
+        arr[tt, t_, 0] = gs[tt, jj].astype(np.uint8)      # local group
+        arr[tt, t_, 2 + (pos[tt, jj] % 8)] = sl[tt, jj].astype(np.uint8)
+        np.add.at(arr[:, :, 1], (tt, t_), 1)
+        tiles.append((arr, ntile))
+    # interleave into (type, warp)-major order
+    tile_off = np.zeros(nt * WARP_PARTS + 1, dtype=np.int64)
+    np.cumsum(counts, out=tile_off[1:])
+    out = np.empty((int(tile_off[-1]), 16), dtype=np.uint8)
+    for w, (arr, ntile) in enumerate(tiles):
+        m = np.arange(arr.shape[1])[None, :] < ntile[:, None]
+        t_idx, k_idx = np.nonzero(m)
+        dst = tile_off[t_idx * WARP_PARTS + w] + k_idx
+        out[dst] = arr[t_idx, k_idx]
+    return tile_off, out, node_geom, node_r
+
+
 # ---------------------------------------------------------------------------
 # emission plan (level d boxes -> their cousin points)
 # ---------------------------------------------------------------------------
