@@ -46,14 +46,25 @@ int init_constants() {
 }
 
 // ---------------------------------------------------------------- K3 ----
+// Node (a, b, c) -> row of a segment buffer in shared memory.  Standard
+// layout: (a*PA + b)*PA + c.  OWNER layout (propagation kernel): the 15 nodes
+// of theta index b are contiguous, b*15 + a*PA + c.
+template <bool OWNER>
+__device__ __forceinline__ int node_row(int a, int b, int c) {
+  return OWNER ? b * PS * PA + a * PA + c : (a * PA + b) * PA + c;
+}
+
 // In-place node values -> coefficients for one segment held in shared memory
-// V[node][NCOL] (node = (a*PA + b)*PA + c): three axis transforms.
+// (rows per node_row<OWNER>, NCOL complex columns): three axis transforms
+// (reference ifgf.py:502-522).
+template <bool OWNER>
 __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
   for (int task = tid; task < PA * PA * NCOL; task += nthr) {
     const int bc = task / NCOL, m = task % NCOL;
+    const int b = bc / PA, c = bc % PA;
     double2 v[PS];
 #pragma unroll
-    for (int a = 0; a < PS; ++a) v[a] = V[(a * PA * PA + bc) * NCOL + m];
+    for (int a = 0; a < PS; ++a) v[a] = V[node_row<OWNER>(a, b, c) * NCOL + m];
 #pragma unroll
     for (int a = 0; a < PS; ++a) {
       double2 s = make_double2(0.0, 0.0);
@@ -62,7 +73,7 @@ __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
         s.x += c_ms[a * PS + q] * v[q].x;
         s.y += c_ms[a * PS + q] * v[q].y;
       }
-      V[(a * PA * PA + bc) * NCOL + m] = s;
+      V[node_row<OWNER>(a, b, c) * NCOL + m] = s;
     }
   }
   __syncthreads();
@@ -71,7 +82,7 @@ __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
     const int a = ac / PA, c = ac % PA;
     double2 v[PA];
 #pragma unroll
-    for (int b = 0; b < PA; ++b) v[b] = V[((a * PA + b) * PA + c) * NCOL + m];
+    for (int b = 0; b < PA; ++b) v[b] = V[node_row<OWNER>(a, b, c) * NCOL + m];
 #pragma unroll
     for (int b = 0; b < PA; ++b) {
       double2 s = make_double2(0.0, 0.0);
@@ -80,15 +91,16 @@ __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
         s.x += c_ma[b * PA + q] * v[q].x;
         s.y += c_ma[b * PA + q] * v[q].y;
       }
-      V[((a * PA + b) * PA + c) * NCOL + m] = s;
+      V[node_row<OWNER>(a, b, c) * NCOL + m] = s;
     }
   }
   __syncthreads();
   for (int task = tid; task < PS * PA * NCOL; task += nthr) {
     const int ab = task / NCOL, m = task % NCOL;
+    const int a = ab / PA, b = ab % PA;
     double2 v[PA];
 #pragma unroll
-    for (int c = 0; c < PA; ++c) v[c] = V[(ab * PA + c) * NCOL + m];
+    for (int c = 0; c < PA; ++c) v[c] = V[node_row<OWNER>(a, b, c) * NCOL + m];
 #pragma unroll
     for (int c = 0; c < PA; ++c) {
       double2 s = make_double2(0.0, 0.0);
@@ -97,14 +109,15 @@ __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
         s.x += c_ma[c * PA + q] * v[q].x;
         s.y += c_ma[c * PA + q] * v[q].y;
       }
-      V[(ab * PA + c) * NCOL + m] = s;
+      V[node_row<OWNER>(a, b, c) * NCOL + m] = s;
     }
   }
   __syncthreads();
 }
 
-// Write one segment's coefficients V[i][m] (node-major complex) in DMMA
-// B-fragment order (see SEG_DOUBLES): coalesced stores, padding zeroed.
+// Write one segment's coefficients V[i][m] (rows per node_row<OWNER>) in
+// DMMA B-fragment order (see SEG_DOUBLES): coalesced stores, padding zeroed.
+template <bool OWNER>
 __device__ __forceinline__ void store_segment(double* dst, const double2* V,
                                               int tid, int nthr) {
   for (int idx = tid; idx < SEG_DOUBLES; idx += nthr) {
@@ -113,9 +126,8 @@ __device__ __forceinline__ void store_segment(double* dst, const double2* V,
     const int ab = 4 * q + (lane & 3);
     double v = 0.0;
     if (ab < PS * PA) {
-      const int i = ab * PA + c;
       const int col = 8 * nt + (lane >> 2);
-      const double2 z = V[i * NCOL + (col >> 1)];
+      const double2 z = V[node_row<OWNER>(ab / PA, ab % PA, c) * NCOL + (col >> 1)];
       v = (col & 1) ? z.y : z.x;
     }
     dst[idx] = v;
@@ -200,8 +212,8 @@ __global__ void __launch_bounds__(128) leaf_kernel(LeafArgs a) {
     for (int m = 0; m < NCOL; ++m) V[tid * NCOL + m] = acc[m];
   }
   __syncthreads();
-  to_coeffs_smem(V, tid, blockDim.x);
-  store_segment(a.coef + (size_t)row * SEG_DOUBLES, V, tid, blockDim.x);
+  to_coeffs_smem<false>(V, tid, blockDim.x);
+  store_segment<false>(a.coef + (size_t)row * SEG_DOUBLES, V, tid, blockDim.x);
 }
 
 // ------------------------------------------------------- DMMA helpers ----
@@ -304,9 +316,8 @@ struct AccArgs {
 // 4 column tiles of FP64 DMMA, times the re-centering ratio.  The summed
 // values are transformed to coefficients (K3) and written once.
 template <int NK>
-__global__ void __launch_bounds__(160, 3) accum_kernel(AccArgs a) {
+__global__ void __launch_bounds__(160, 6) accum_kernel(AccArgs a) {
   __shared__ double2 acc[WARP_PARTS * PART_NODES * NCOL];   // 19.2 KB
-  __shared__ double2 V[NN * NCOL];                          // 19.2 KB
   const int p = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, tig = lane & 3;
@@ -351,16 +362,9 @@ __global__ void __launch_bounds__(160, 3) accum_kernel(AccArgs a) {
     }
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < NN * NCOL; idx += blockDim.x) {
-    const int node = idx / NCOL, m = idx - node * NCOL;
-    const int b = (node / PA) % PA;
-    const int slot = (node / (PA * PA)) * PA + node % PA;
-    V[idx] = acc[(b * PART_NODES + slot) * NCOL + m];
-  }
-  __syncthreads();
-  to_coeffs_smem(V, threadIdx.x, blockDim.x);
-  store_segment(a.coef_parent + (size_t)p * SEG_DOUBLES, V, threadIdx.x,
-                blockDim.x);
+  to_coeffs_smem<true>(acc, threadIdx.x, 32 * WARP_PARTS);
+  store_segment<true>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, threadIdx.x,
+                      32 * WARP_PARTS);
 }
 
 // ---------------------------------------------------------------- K5 ----
