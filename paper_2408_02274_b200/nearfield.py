@@ -21,6 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import cheb
+from .octree import _pool
 from .surface import SurfaceDiscretization, closest_point_batch
 
 __all__ = ["SingularQuadratureConfig", "SingularityMap", "MomentGroup",
@@ -78,32 +79,16 @@ def classify_targets(disc: SurfaceDiscretization,
     n_t = pts.shape[0]
     delta = config.delta_factor * disc.max_spacing
     grid = cheb.nodes(disc.n_c)
+    global _CLASSIFY_CTX
+    _CLASSIFY_CTX = (disc, pts, delta, grid, on_surface)
     found = [[] for _ in range(n_t)]
-    for p, patch in enumerate(disc.patches):
-        lower = np.linalg.norm(pts - patch.center, axis=1) - patch.bound_radius
-        cand = np.nonzero(lower <= delta[p])[0]
-        if cand.size == 0:
-            continue
-        own = np.zeros(cand.size, dtype=bool)
-        if on_surface:
-            own = disc.patch_of[cand] == p
-            for ell in cand[own]:
-                _, i, j = disc.decode_index(int(ell))
-                found[ell].append((p, grid[i], grid[j], 0.0))
-        rest = cand[~own]
-        if rest.size == 0:
-            continue
-        seed = disc.patch_points(p).reshape(disc.n_c, disc.n_c, 3)
-        dmin = np.min(np.linalg.norm(
-            pts[rest][:, None, :] - seed.reshape(-1, 3)[None, :, :], axis=-1),
-            axis=1)
-        rest = rest[dmin - disc.max_spacing[p] <= delta[p]]
-        if rest.size == 0:
-            continue
-        u, v, dist = closest_point_batch(disc.patches[p], pts[rest], seed)
-        for ell, uu, vv, dd in zip(rest, u, v, dist):
-            if dd <= delta[p]:
-                found[ell].append((p, uu, vv, dd))
+    # per-patch work is independent; entries are sorted per target below, so
+    # the merge order does not matter (the golden-section loops are
+    # Python-bound: processes when fork is available, else in-process)
+    for hits in _map_patches(_classify_patch, disc.n_patches):
+        for ell, ent in hits:
+            found[ell].append(ent)
+    _CLASSIFY_CTX = None
     offsets = np.zeros(n_t + 1, dtype=np.int64)
     ids, uvs, ds = [], [], []
     for ell in range(n_t):
@@ -117,6 +102,64 @@ def classify_targets(disc: SurfaceDiscretization,
                           np.asarray(ids, dtype=np.int32),
                           np.asarray(uvs, dtype=float).reshape(-1, 2),
                           np.asarray(ds, dtype=float))
+
+
+_CLASSIFY_CTX = None
+
+
+def _map_patches(fn, n_patches):
+    """Map fn over patch ids in forked worker processes (results in order)."""
+    import multiprocessing as mp
+    import os
+    workers = min(os.cpu_count() or 1, 32, n_patches)
+    if workers > 1 and n_patches >= 16:
+        import warnings
+        try:
+            with warnings.catch_warnings():
+                # children only run numpy on the inherited (read-only) plan
+                # inputs; a stuck worker falls back to in-process below
+                warnings.simplefilter("ignore", DeprecationWarning)
+                ctx = mp.get_context("fork")
+                with ctx.Pool(workers) as pool:
+                    res = pool.map_async(
+                        fn, range(n_patches),
+                        chunksize=max(1, n_patches // (4 * workers)))
+                    return res.get(timeout=600 + n_patches)
+        except (OSError, ValueError, mp.TimeoutError):
+            pass
+    return [fn(p) for p in range(n_patches)]
+
+
+def _classify_patch(p):
+    """Singular/near pairs of patch p (runs in a worker process)."""
+    disc, pts, delta, grid, on_surface = _CLASSIFY_CTX
+    patch = disc.patches[p]
+    hits = []
+    lower = np.linalg.norm(pts - patch.center, axis=1) - patch.bound_radius
+    cand = np.nonzero(lower <= delta[p])[0]
+    if cand.size == 0:
+        return hits
+    own = np.zeros(cand.size, dtype=bool)
+    if on_surface:
+        own = disc.patch_of[cand] == p
+        for ell in cand[own]:
+            _, i, j = disc.decode_index(int(ell))
+            hits.append((int(ell), (p, grid[i], grid[j], 0.0)))
+    rest = cand[~own]
+    if rest.size == 0:
+        return hits
+    seed = disc.patch_points(p).reshape(disc.n_c, disc.n_c, 3)
+    dmin = np.min(np.linalg.norm(
+        pts[rest][:, None, :] - seed.reshape(-1, 3)[None, :, :], axis=-1),
+        axis=1)
+    rest = rest[dmin - disc.max_spacing[p] <= delta[p]]
+    if rest.size == 0:
+        return hits
+    u, v, dist = closest_point_batch(patch, pts[rest], seed)
+    for ell, uu, vv, dd in zip(rest, u, v, dist):
+        if dd <= delta[p]:
+            hits.append((int(ell), (p, uu, vv, dd)))
+    return hits
 
 
 # ---------------------------------------------------------------------------
@@ -211,7 +254,8 @@ def compute_moments(disc: SurfaceDiscretization, smap: SingularityMap,
     pts = disc.points if target_points is None else target_points
     nrms = disc.normals if target_normals is None else target_normals
     table = SingularMomentTable(n_c, kappas)
-    for p in np.unique(smap.patch_ids):
+
+    def one_patch(p):
         patch = disc.patches[p]
         tg, u0, v0 = smap.pairs_for_patch(int(p))
         b = tg.size
@@ -244,7 +288,10 @@ def compute_moments(disc: SurfaceDiscretization, smap: SingularityMap,
             kd = ks * (ndx * (1j * kappa * r - 1.0) / r**2)
             bs[k] = (put.astype(complex) @ ks) @ pvw
             bd[k] = (put.astype(complex) @ kd) @ pvw
-        table.groups[int(p)] = MomentGroup(tg, bs, bd)
+        return int(p), MomentGroup(tg, bs, bd)
+
+    for p, grp in _pool().map(one_patch, np.unique(smap.patch_ids)):
+        table.groups[p] = grp
     return table
 
 

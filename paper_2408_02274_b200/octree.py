@@ -305,65 +305,85 @@ class ConeLevel:
 
     @property
     def id_stride(self) -> int:
-        return self.n_s * self.n_a * 2 * self.n_a + 1
+        return id_stride(self)
 
     def segs_of(self, b: int) -> np.ndarray:
         return self.seg_ids[self.seg_off[b]:self.seg_off[b + 1]]
 
     def seg_index(self, s, theta, phi) -> np.ndarray:
-        i_s = np.minimum((s / self.delta_s).astype(np.int64), self.n_s - 1)
-        i_t = np.minimum((theta / self.delta_a).astype(np.int64),
-                         self.n_a - 1)
-        i_p = np.minimum((phi / self.delta_a).astype(np.int64),
-                         2 * self.n_a - 1)
-        return (i_s * self.n_a + i_t) * (2 * self.n_a) + i_p
+        return seg_index(self, s, theta, phi)
 
     def seg_unpack(self, flat):
-        i_p = flat % (2 * self.n_a)
-        rest = flat // (2 * self.n_a)
-        return rest // self.n_a, rest % self.n_a, i_p
+        return seg_unpack(self, flat)
 
     def local_coords(self, flat, s, theta, phi):
-        i_s, i_t, i_p = self.seg_unpack(flat)
-        return (2.0 * (s / self.delta_s - i_s) - 1.0,
-                2.0 * (theta / self.delta_a - i_t) - 1.0,
-                2.0 * (phi / self.delta_a - i_p) - 1.0)
-
-    def node_directions(self, flat):
-        """Per segment: radii (nseg, p_s) and unit directions
-        (nseg, p_a, p_a, 3) of its interpolation nodes."""
-        i_s, i_t, i_p = self.seg_unpack(flat)
-        r = self.h / self.s_nodes[i_s]
-        th = self.ang_nodes_t[i_t]
-        ph = self.ang_nodes_p[i_p]
-        st, ct = np.sin(th), np.cos(th)
-        cp, sp = np.cos(ph), np.sin(ph)
-        dirs = np.stack([st[:, :, None] * cp[:, None, :],
-                         st[:, :, None] * sp[:, None, :],
-                         np.broadcast_to(ct[:, :, None],
-                                         (flat.size, th.shape[1],
-                                          ph.shape[1]))], axis=-1)
-        return r, dirs
+        return local_coords(self, flat, s, theta, phi)
 
     def segment_nodes_xyz(self, flat, center):
-        """Cartesian nodes (nseg, p_s*p_a*p_a, 3) = center + r * dir, and
-        node radii; ``center`` may be (3,) or per segment (nseg, 3)."""
-        flat = np.asarray(flat, dtype=np.int64)
-        r, dirs = self.node_directions(flat)
-        c = np.asarray(center, dtype=float)
-        if c.ndim == 2:
-            c = c[:, None, None, None, :]
-        xyz = c + r[:, :, None, None, None] * dirs[:, None]
-        rr = np.broadcast_to(r[:, :, None, None],
-                             xyz.shape[:-1]).reshape(flat.size, -1)
-        return xyz.reshape(flat.size, -1, 3), rr
+        return segment_nodes_xyz(self, flat, center)
 
     def box_keys(self) -> np.ndarray:
-        """Globally sorted (box, segment id) keys, one per segment row."""
-        nb = self.seg_off.size - 1
-        return (np.repeat(np.arange(nb, dtype=np.int64),
-                          np.diff(self.seg_off)) * np.int64(self.id_stride)
-                + self.seg_ids)
+        return box_keys(self)
+
+
+# Cone-level helpers as free functions over the level's attributes, so they
+# apply unchanged to the reference's own ConeLevel objects (drop-in path).
+
+def id_stride(cl) -> int:
+    return cl.n_s * cl.n_a * 2 * cl.n_a + 1
+
+
+def seg_index(cl, s, theta, phi) -> np.ndarray:
+    """Flat segment id, upper edges clamped (reference ifgf.py:349-354)."""
+    i_s = np.minimum((s / cl.delta_s).astype(np.int64), cl.n_s - 1)
+    i_t = np.minimum((theta / cl.delta_a).astype(np.int64), cl.n_a - 1)
+    i_p = np.minimum((phi / cl.delta_a).astype(np.int64), 2 * cl.n_a - 1)
+    return (i_s * cl.n_a + i_t) * (2 * cl.n_a) + i_p
+
+
+def seg_unpack(cl, flat):
+    i_p = flat % (2 * cl.n_a)
+    rest = flat // (2 * cl.n_a)
+    return rest // cl.n_a, rest % cl.n_a, i_p
+
+
+def local_coords(cl, flat, s, theta, phi):
+    """[-1,1]^3 coordinates inside segment `flat` (ifgf.py:361-367)."""
+    i_s, i_t, i_p = seg_unpack(cl, flat)
+    return (2.0 * (s / cl.delta_s - i_s) - 1.0,
+            2.0 * (theta / cl.delta_a - i_t) - 1.0,
+            2.0 * (phi / cl.delta_a - i_p) - 1.0)
+
+
+def segment_nodes_xyz(cl, flat, center):
+    """Cartesian nodes (nseg, p_s*p_a*p_a, 3) = center + r * dir and node
+    radii (ifgf.py:369-387); ``center`` is (3,) or per segment (nseg, 3)."""
+    flat = np.asarray(flat, dtype=np.int64)
+    i_s, i_t, i_p = seg_unpack(cl, flat)
+    r = cl.h / cl.s_nodes[i_s]
+    th = cl.ang_nodes_t[i_t]
+    ph = cl.ang_nodes_p[i_p]
+    st, ct = np.sin(th), np.cos(th)
+    cp, sp = np.cos(ph), np.sin(ph)
+    dirs = np.stack([st[:, :, None] * cp[:, None, :],
+                     st[:, :, None] * sp[:, None, :],
+                     np.broadcast_to(ct[:, :, None],
+                                     (flat.size, th.shape[1], ph.shape[1]))],
+                    axis=-1)
+    c = np.asarray(center, dtype=float)
+    if c.ndim == 2:
+        c = c[:, None, None, None, :]
+    xyz = c + r[:, :, None, None, None] * dirs[:, None]
+    rr = np.broadcast_to(r[:, :, None, None],
+                         xyz.shape[:-1]).reshape(flat.size, -1)
+    return xyz.reshape(flat.size, -1, 3), rr
+
+
+def box_keys(cl) -> np.ndarray:
+    """Globally sorted (box, segment id) keys, one per segment row."""
+    nb = cl.seg_off.size - 1
+    return (np.repeat(np.arange(nb, dtype=np.int64), np.diff(cl.seg_off))
+            * np.int64(id_stride(cl)) + cl.seg_ids)
 
 
 @dataclass
@@ -372,7 +392,6 @@ class ConeHierarchy:
     kappa_max: float
     cone_levels: dict
     _accum_cache: dict = field(default_factory=dict)
-    _emit_cache: dict = field(default_factory=dict)
 
     def level(self, d: int) -> ConeLevel:
         return self.cone_levels[d]
@@ -403,6 +422,20 @@ def _cousin_points(tree: BoxTree, d: int):
                                 lvl.pt_start[cz] + lvl.pt_count[cz])
     box = owner[p_own]
     return pts, _offsets_from_owner(box, lvl.n_boxes), box
+
+
+_POOL = None
+
+
+def _pool():
+    """Shared thread pool for plan construction (numpy releases the GIL)."""
+    global _POOL
+    if _POOL is None:
+        import concurrent.futures
+        import os
+        _POOL = concurrent.futures.ThreadPoolExecutor(
+            max_workers=max(1, min(32, os.cpu_count() or 1)))
+    return _POOL
 
 
 def _chunks(off: np.ndarray, budget: int):
@@ -437,14 +470,14 @@ def build_cone_hierarchy(tree: BoxTree,
             seg_off=np.zeros(lvl.n_boxes + 1, dtype=np.int64),
             cpt_idx=np.empty(0, dtype=np.int64),
             cpt_off=np.zeros(lvl.n_boxes + 1, dtype=np.int64))
-        stride = np.int64(cl.id_stride)
+        stride = np.int64(id_stride(cl))
         cpts, cpt_off, cbox = _cousin_points(tree, d)
         cl.cpt_idx, cl.cpt_off = cpts, cpt_off
         keys = []
         if cpts.size:
             s, th, ph, _ = cone_coords(tree.points[cpts], lvl.centers[cbox],
                                        lvl.side)
-            keys.append(cbox * stride + cl.seg_index(s, th, ph))
+            keys.append(cbox * stride + seg_index(cl, s, th, ph))
         pcl = hier.cone_levels.get(d - 1)
         if pcl is not None:
             up = tree.level(d - 1)
@@ -455,19 +488,26 @@ def build_cone_hierarchy(tree: BoxTree,
             np.cumsum(prow_end - prow_off, out=inst_off[1:])
             pbox_of_row = np.repeat(np.arange(up.n_boxes),
                                     np.diff(pcl.seg_off))
-            budget = max(1, 4_000_000 // nn)
-            for b0, b1 in _chunks(inst_off, budget):
+            budget = max(1, 1_000_000 // nn)
+
+            def chunk_keys(b0, b1):
                 rows, own = _expand_ranges(prow_off[b0:b1], prow_end[b0:b1])
                 if rows.size == 0:
-                    continue
-                xyz, _ = pcl.segment_nodes_xyz(
-                    pcl.seg_ids[rows], up.centers[pbox_of_row[rows]])
+                    return None
+                xyz, _ = segment_nodes_xyz(
+                    pcl, pcl.seg_ids[rows], up.centers[pbox_of_row[rows]])
                 box = own + b0
                 dx = xyz - lvl.centers[box][:, None, :]
                 s, th, ph, _ = cone_coords(dx.reshape(-1, 3), np.zeros(3),
                                            lvl.side)
-                keys.append(np.repeat(box, nn) * stride +
-                            cl.seg_index(s, th, ph))
+                k = np.repeat(box, nn) * stride + seg_index(cl, s, th, ph)
+                return np.unique(k)
+
+            # numpy ufuncs release the GIL: chunks run concurrently, each
+            # element computed by the same expression (bit-identical)
+            keys.extend(k for k in _pool().map(
+                lambda r: chunk_keys(*r), list(_chunks(inst_off, budget)))
+                if k is not None)
         if keys:
             uk = np.unique(np.concatenate(keys))
             box = uk // stride
@@ -531,26 +571,26 @@ def _type_geometry(pcl: ConeLevel, cl: ConeLevel, gamma, octant, child_side):
     bits = np.stack([(octant >> 2) & 1, (octant >> 1) & 1, octant & 1],
                     axis=-1)
     offset = 0.5 * child_side * (bits * 2.0 - 1.0)
-    xyz, rp = pcl.segment_nodes_xyz(gamma, -offset)
+    xyz, rp = segment_nodes_xyz(pcl, gamma, -offset)
     nn = xyz.shape[1]
     s, th, ph, rc = cone_coords(xyz.reshape(-1, 3), np.zeros(3), child_side)
-    flat = cl.seg_index(s, th, ph).reshape(n_t, nn)
+    flat = seg_index(cl, s, th, ph).reshape(n_t, nn)
     order = np.argsort(flat, axis=1, kind="stable")
     fs = np.take_along_axis(flat, order, axis=1)
     take = lambda a: np.take_along_axis(a.reshape(n_t, nn), order, axis=1)
-    xs, xt, xp = cl.local_coords(fs, take(s), take(th), take(ph))
+    xs, xt, xp = local_coords(cl, fs, take(s), take(th), take(ph))
     return fs, order, xs, xt, xp, take(rp), take(rc)
 
 
 def accumulation_plan(tree: BoxTree, hier: ConeHierarchy,
                       d: int) -> AccumulationPlan:
     """Plan for folding level-d child interpolants into level d-1."""
-    cache = hier._accum_cache
+    cache = hier.__dict__.setdefault("_b200_accum", {})
     if d in cache:
         return cache[d]
     cl, pcl = hier.level(d), hier.level(d - 1)
     lvl = tree.level(d)
-    nn = hier.config.n_nodes
+    nn = hier.config.p_s * hier.config.p_a ** 2
     octant = (lvl.codes & np.uint64(7)).astype(np.int64)
     prow, child = _expand_ranges(pcl.seg_off[lvl.parent],
                                  pcl.seg_off[lvl.parent + 1])
@@ -562,14 +602,17 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy,
     fs_all = np.empty((n_t, nn), dtype=np.int64)
     order_all = np.empty((n_t, nn), dtype=np.int64)
     geo = {k: np.empty((n_t, nn)) for k in ("xs", "xt", "xp", "rp", "rc")}
-    step = max(1, 2_000_000 // nn)
-    for t0 in range(0, n_t, step):
+    step = max(1, 250_000 // nn)
+
+    def chunk(t0):
         t1 = min(n_t, t0 + step)
         fs, order, xs, xt, xp, rp, rc = _type_geometry(
             pcl, cl, gamma[t0:t1], toct[t0:t1], lvl.side)
         fs_all[t0:t1], order_all[t0:t1] = fs, order
         for k, v in zip(("xs", "xt", "xp", "rp", "rc"), (xs, xt, xp, rp, rc)):
             geo[k][t0:t1] = v
+
+    list(_pool().map(chunk, range(0, n_t, step)))   # disjoint row blocks
     # sigma groups per type
     newgrp = np.ones((n_t, nn), dtype=bool)
     newgrp[:, 1:] = fs_all[:, 1:] != fs_all[:, :-1]
@@ -589,11 +632,11 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy,
     crow_off = np.zeros(prow.size + 1, dtype=np.int64)
     np.cumsum(nsig, out=crow_off[1:])
     gidx, g_own = _expand_ranges(sig_off[inst_type], sig_off[inst_type + 1])
-    box_keys = cl.box_keys()
-    want = child[g_own] * np.int64(cl.id_stride) + g_sigma[gidx]
-    crow = np.searchsorted(box_keys, want).astype(np.int64)
+    bkeys = box_keys(cl)
+    want = child[g_own] * np.int64(id_stride(cl)) + g_sigma[gidx]
+    crow = np.searchsorted(bkeys, want).astype(np.int64)
     misses = int(np.count_nonzero(
-        box_keys[np.minimum(crow, box_keys.size - 1)] != want))
+        bkeys[np.minimum(crow, bkeys.size - 1)] != want))
     plan = AccumulationPlan(
         level=d, n_types=n_t, type_gamma=gamma, type_octant=toct,
         sig_off=sig_off, group_bounds=g_start, group_end=g_end,
@@ -720,18 +763,18 @@ def emission_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
         return EmissionPlan(d, np.empty(0, np.int64), tg, z,
                             None if disp_points_t is None else z)
     s, th, ph, r = cone_coords(tree.points[tg] - ctr, np.zeros(3), lvl.side)
-    flat = cl.seg_index(s, th, ph)
-    want = box * np.int64(cl.id_stride) + flat
-    keys = cl.box_keys()
+    flat = seg_index(cl, s, th, ph)
+    want = box * np.int64(id_stride(cl)) + flat
+    keys = box_keys(cl)
     row = np.searchsorted(keys, want).astype(np.int64)
     misses = int(np.count_nonzero(keys[np.minimum(row, keys.size - 1)]
                                   != want))
-    geom = np.stack(cl.local_coords(flat, s, th, ph) + (r,), axis=1)
+    geom = np.stack(local_coords(cl, flat, s, th, ph) + (r,), axis=1)
     gd = None
     if disp_points_t is not None:
         sd, td, pd, rd = cone_coords(disp_points_t[tg] - ctr, np.zeros(3),
                                      lvl.side)
-        gd = np.stack(cl.local_coords(flat, sd, td, pd) + (rd,), axis=1)
+        gd = np.stack(local_coords(cl, flat, sd, td, pd) + (rd,), axis=1)
     return EmissionPlan(d, row, tg, geom, gd, misses)
 
 
