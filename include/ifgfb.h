@@ -231,6 +231,39 @@ int ifgfb_plan_kernel_times(ifgfb_plan* plan, double* ms, int64_t* counts);
 /* Number of kernels launched by the last apply on this plan. */
 int64_t ifgfb_plan_last_launches(const ifgfb_plan* plan);
 
+/* ---- multi-GPU partition.  One plan per rank/GPU.  The
+ * upward pass (leaf spectra, propagation, emission) is restricted to the
+ * rank's Morton range of level-3 subtrees: per level, its segment rows and
+ * its box-major emission pair range.  Near field and assembly are
+ * restricted to a patch-aligned original-order target range.  With a
+ * partition set, ifgfb_muller_far_phase leaves PARTIAL far-field sums in the
+ * plan's far buffers (sum them over ranks, e.g. NCCL all-reduce, before the
+ * near phase); ifgfb_muller_near_phase writes only the owned rows of the 4N
+ * output.  Without a partition both phases cover everything and
+ * far_phase + near_phase == ifgfb_muller_apply. */
+typedef struct {
+  int32_t level;
+  int64_t seg_lo, seg_hi;     /* owned segment rows of this level */
+  int64_t pair_lo, pair_hi;   /* owned (box, cousin point) pairs of this level */
+} ifgfb_level_part;
+
+typedef struct {
+  int32_t n_levels;                 /* entries for levels 3..depth */
+  const ifgfb_level_part* levels;
+  int64_t target_lo, target_hi;     /* original order, multiples of n_c^2 */
+} ifgfb_partition_desc;
+
+int ifgfb_plan_set_partition(ifgfb_plan* plan, const ifgfb_partition_desc* part);
+/* density packing (all points) + far field of the owned subtrees */
+int ifgfb_muller_far_phase(ifgfb_plan* plan, const double* y, void* stream);
+/* near field + assembly of the owned targets; rows outside are untouched */
+int ifgfb_muller_near_phase(ifgfb_plan* plan, const double* y, double* out,
+                            void* stream);
+/* device pointers of the far-field buffers (each 16*N complex, layout
+ * (8 ch, 2 kernels, N) original order) for the cross-rank reduction */
+int ifgfb_plan_far_buffers(ifgfb_plan* plan, double** far, double** far_disp,
+                           int64_t* n_complex);
+
 #ifdef __cplusplus
 }
 #endif

@@ -132,13 +132,18 @@ def _coeffs(vals, ps, pa):
 
 
 def far_field(tree, hier, weights, kappas, normals=None, step=1e-6,
-              box_stride: int = 1):
+              box_stride: int = 1, box_ranges: dict | None = None):
     """out[c, k, ell] = sum over sources outside ell's finest neighbour boxes
     of G_k(x_ell, y) w[c, y] (and the same at x_ell + step * n_ell).
 
     box_stride > 1 processes only boxes b % box_stride == 0 (leaf spectra,
     emission, propagation): a bounded, scalable CPU-baseline sample whose
     output is NOT the full result.
+
+    box_ranges {level d: (lo, hi)} restricts the upward pass to those boxes
+    per level (one rank of the multi-GPU partition): the result is that
+    rank's partial sum; summing the partials of a partition gives the full
+    far field.
     """
     cfg = hier.config
     ps, pa = cfg.p_s, cfg.p_a
@@ -160,7 +165,7 @@ def far_field(tree, hier, weights, kappas, normals=None, step=1e-6,
     # --- leaf values (ifgf.py:535-554)
     cl, lvl = hier.level(D), tree.level(D)
     vals = np.zeros((cl.n_segments, nn, nch, nk), dtype=complex)
-    for b in range(0, lvl.n_boxes, box_stride):
+    for b in _boxes(box_ranges, D, lvl.n_boxes, box_stride):
         r0, r1 = cl.seg_off[b], cl.seg_off[b + 1]
         if r1 == r0:
             continue
@@ -175,22 +180,31 @@ def far_field(tree, hier, weights, kappas, normals=None, step=1e-6,
     for d in range(D, 2, -1):
         cl, lvl = hier.level(d), tree.level(d)
         coef = _coeffs(vals.reshape(cl.n_segments, nn, -1), ps, pa)
-        _emit(tree, hier, d, coef, kap, nch, out, outd, disp, box_stride)
+        _emit(tree, hier, d, coef, kap, nch, out, outd, disp, box_stride,
+              box_ranges)
         if d > 3:
-            vals = _propagate(tree, hier, d, coef, kap, nch, box_stride)
+            vals = _propagate(tree, hier, d, coef, kap, nch, box_stride,
+                              box_ranges)
     out = out.transpose(1, 2, 0)[:, :, tree.iperm]
     if outd is not None:
         outd = outd.transpose(1, 2, 0)[:, :, tree.iperm]
     return out, outd
 
 
-def _emit(tree, hier, d, coef, kap, nch, out, outd, disp, box_stride):
+def _boxes(box_ranges, d, n_boxes, stride):
+    lo, hi = (0, n_boxes) if box_ranges is None else box_ranges[d]
+    return range(lo, hi, stride) if stride > 1 else range(lo, hi)
+
+
+def _emit(tree, hier, d, coef, kap, nch, out, outd, disp, box_stride,
+          box_ranges=None):
     """Cousin-point evaluation of level-d interpolants (ifgf.py:630-673)."""
     cfg = hier.config
     cl, lvl = hier.level(d), tree.level(d)
     nk = kap.size
     stride, keys = _row_keys(cl)
-    boxes = np.arange(0, lvl.n_boxes, box_stride)
+    boxes = np.array(list(_boxes(box_ranges, d, lvl.n_boxes, box_stride)),
+                     dtype=np.int64)
     cnt = cl.cpt_off[boxes + 1] - cl.cpt_off[boxes]
     box = np.repeat(boxes, cnt)
     if box.size == 0:
@@ -216,7 +230,7 @@ def _emit(tree, hier, d, coef, kap, nch, out, outd, disp, box_stride):
             np.add.at(dst, tg[z], v)
 
 
-def _propagate(tree, hier, d, coef, kap, nch, box_stride):
+def _propagate(tree, hier, d, coef, kap, nch, box_stride, box_ranges=None):
     """Fold level-d interpolants into the level-(d-1) node values
     (ifgf.py:676-785): per (parent segment id, child octant) type, the
     parent nodes in child coordinates, their child segments and the
@@ -232,7 +246,7 @@ def _propagate(tree, hier, d, coef, kap, nch, box_stride):
     flat_c = coef.reshape(coef.shape[0], nn, -1)
     octant = (lvl.codes & np.uint64(7)).astype(np.int64)
     inst = {}
-    for b in range(0, lvl.n_boxes, box_stride):
+    for b in _boxes(box_ranges, d, lvl.n_boxes, box_stride):
         pb = lvl.parent[b]
         for p in range(pcl.seg_off[pb], pcl.seg_off[pb + 1]):
             inst.setdefault((int(pcl.seg_ids[p]), int(octant[b])), []).append((p, b))
@@ -313,7 +327,7 @@ def _grads(disc, fields):
     return a[..., None] * disc.e_u + b[..., None] * disc.e_v
 
 
-def _neighbor_sums(op, phi, kap):
+def _neighbor_sums(op, phi, kap, stride=1):
     disc, tree, smap = op.disc, op.tree, op.smap
     lvl = tree.level(tree.depth)
     n = disc.n_points
@@ -323,7 +337,7 @@ def _neighbor_sums(op, phi, kap):
     pt = disc.points[tree.perm]
     nt = disc.normals[tree.perm]
     ptch = disc.patch_of
-    for b in range(lvl.n_boxes):
+    for b in range(0, lvl.n_boxes, stride):
         tt = np.arange(lvl.pt_start[b], lvl.pt_start[b] + lvl.pt_count[b])
         st = np.concatenate([np.arange(lvl.pt_start[q], lvl.pt_start[q] + lvl.pt_count[q])
                              for q in lvl.neighbors(b)])
@@ -344,9 +358,9 @@ def _neighbor_sums(op, phi, kap):
     return s_out, d_out
 
 
-def _corrections(op, phi, kap):
+def _corrections(op, phi, kap, stride=1):
     disc = op.disc
-    ell, src = op.corr_ell, op.corr_src
+    ell, src = op.corr_ell[::stride], op.corr_src[::stride]
     dx = disc.points[ell] - disc.points[src]
     r = np.linalg.norm(dx, axis=1)
     ndx = np.einsum("ec,ec->e", dx, disc.normals[ell])
@@ -363,7 +377,7 @@ def _corrections(op, phi, kap):
     return cs, cd
 
 
-def potentials(op: OperatorData, phi):
+def potentials(op: OperatorData, phi, stride: int = 1):
     """(S (8,2,N), D (6,2,N)) (operators.py:321-350)."""
     disc = op.disc
     kap = op.materials.kappas
@@ -374,23 +388,26 @@ def potentials(op: OperatorData, phi):
     n = disc.n_points
     s_near = np.zeros((8, 2, n), dtype=complex)
     d_near = np.zeros((8, 2, n), dtype=complex)
-    for p, grp in op.moments.groups.items():
+    for p, grp in list(op.moments.groups.items())[::stride]:
         s_near[:, :, grp.targets] += np.einsum("kbmn,cmn->ckb", grp.beta_s, coeffs[:, p])
         d_near[:, :, grp.targets] += np.einsum("kbmn,cmn->ckb", grp.beta_d, coeffs[:, p])
     s_if, s_disp = far_field(op.tree, op.hier, phi * disc.weights, kap,
-                             disc.normals, op.fd_step)
-    s_nb, d_nb = _neighbor_sums(op, phi, kap)
+                             disc.normals, op.fd_step, box_stride=stride)
+    s_nb, d_nb = _neighbor_sums(op, phi, kap, stride)
     s_far = s_if + s_nb
     d_far = (s_disp[:6] - s_if[:6]) / op.fd_step + d_nb
-    cs, cd = _corrections(op, phi, kap)
+    cs, cd = _corrections(op, phi, kap, stride)
     for k in range(2):
         s_far[:, k] -= cs[k]
         d_far[:, k] -= cd[k]
     return s_near + s_far, d_near[:6] + d_far
 
 
-def muller_apply(op: OperatorData, y):
-    """y (4N) -> A y (operators.py:399-403 with apply_block :354-397)."""
+def muller_apply(op: OperatorData, y, stride: int = 1):
+    """y (4N) -> A y (operators.py:399-403 with apply_block :354-397).
+
+    stride > 1 runs a bounded CPU-baseline sample (every stride-th box /
+    patch group / correction entry); its output is NOT the full result."""
     disc, mats = op.disc, op.materials
     n = disc.n_points
     y = np.asarray(y, dtype=complex)
@@ -400,7 +417,7 @@ def muller_apply(op: OperatorData, y):
     phi = np.empty((8, n), dtype=complex)
     phi[0:3], phi[3:6] = j.T, m.T
     phi[6], phi[7] = _divergence(disc, j), _divergence(disc, m)
-    S, D = potentials(op, phi)
+    S, D = potentials(op, phi, stride)
     G = _grads(disc, S)
     nrm = disc.normals
     kap = mats.kappas

@@ -73,6 +73,17 @@ class NearDesc(C.Structure):
                 ("dir_src", _ip)]
 
 
+class LevelPart(C.Structure):
+    _fields_ = [("level", C.c_int32), ("seg_lo", C.c_int64),
+                ("seg_hi", C.c_int64), ("pair_lo", C.c_int64),
+                ("pair_hi", C.c_int64)]
+
+
+class PartitionDesc(C.Structure):
+    _fields_ = [("n_levels", C.c_int32), ("levels", C.POINTER(LevelPart)),
+                ("target_lo", C.c_int64), ("target_hi", C.c_int64)]
+
+
 EXPORTS = {
     "ifgfb_abi_version": ([], C.c_int),
     "ifgfb_last_error": ([], C.c_char_p),
@@ -106,6 +117,14 @@ EXPORTS = {
                            C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_basis_combine": ([C.c_void_p, C.c_int64, C.c_int, C.c_int64,
                              C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "ifgfb_plan_set_partition": ([C.c_void_p, C.POINTER(PartitionDesc)],
+                                 C.c_int),
+    "ifgfb_muller_far_phase": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "ifgfb_muller_near_phase": ([C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p], C.c_int),
+    "ifgfb_plan_far_buffers": ([C.c_void_p, C.POINTER(C.c_void_p),
+                                C.POINTER(C.c_void_p), C.POINTER(C.c_int64)],
+                               C.c_int),
     "ifgfb_zscal_div": ([C.c_void_p, C.c_void_p, C.c_double, C.c_int64,
                          C.c_void_p], C.c_int),
 }

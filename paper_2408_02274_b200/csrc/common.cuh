@@ -177,6 +177,17 @@ struct Level {
   int* inst_crow_off = nullptr;
   int* crow = nullptr;
   int64_t n_instances = 0;
+  // multi-GPU partition (defaults: everything)
+  int part_seg_lo = 0, part_seg_hi = -1;     // -1: n_seg
+  int part_pair_lo = 0, part_pair_hi = -1;   // -1: n_pairs
+  int part_tile_lo = 0, part_tile_hi = -1;   // -1: n_etiles
+  std::vector<int> etile_rows;               // host copy (sorted by row)
+  int seg_lo() const { return part_seg_lo; }
+  int seg_hi() const { return part_seg_hi < 0 ? n_seg : part_seg_hi; }
+  int tile_lo() const { return part_tile_lo; }
+  int tile_hi() const { return part_tile_hi < 0 ? n_etiles : part_tile_hi; }
+  int pair_lo() const { return part_pair_lo; }
+  int pair_hi() const { return part_pair_hi < 0 ? (int)n_pairs : part_pair_hi; }
 };
 
 struct Plan {
@@ -222,6 +233,10 @@ struct Plan {
   double* dev_out = nullptr;    // 4N complex
   int64_t launches = 0;
   KTimer timer;
+  bool partitioned = false;
+  int part_t_lo = 0, part_t_hi = -1;         // owned targets (original order)
+  int t_lo() const { return part_t_lo; }
+  int t_hi() const { return part_t_hi < 0 ? n : part_t_hi; }
   size_t bytes = 0;
   std::vector<void*> allocations;
 };
@@ -263,6 +278,8 @@ int far_apply(Plan& p, const double* w, int nch, const double* kappas, int nk,
 int potentials(Plan& p, const double* phi, double* s_val, double* d_val,
                cudaStream_t st);
 int muller_apply(Plan& p, const double* y, double* out, cudaStream_t st);
+int muller_far_phase(Plan& p, const double* y, cudaStream_t st);
+int muller_near_phase(Plan& p, const double* y, double* out, cudaStream_t st);
 
 }  // namespace ifgfb
 

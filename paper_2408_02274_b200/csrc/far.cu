@@ -154,6 +154,7 @@ struct LeafArgs {
   const double2* wt;     // [N][CH]
   double kr[2], ki[2];
   double* coef;
+  int row0;              // first segment row handled (partition)
 };
 
 // One CTA per finest-level segment: node values
@@ -163,7 +164,7 @@ template <int NK>
 __global__ void __launch_bounds__(128) leaf_kernel(LeafArgs a) {
   constexpr int CH = NCOL / NK;
   __shared__ double2 V[NN * NCOL];
-  const int row = blockIdx.x, tid = threadIdx.x;
+  const int row = blockIdx.x + a.row0, tid = threadIdx.x;
   const int box = a.seg_box[row], id = a.seg_id[row];
   if (tid < NN) {
     const int two_na = 2 * a.n_a;
@@ -305,6 +306,7 @@ struct AccArgs {
   const int* crow; const int* tile_off; const uint4* tiles;
   const double* node_geom; const double2* ratio;
   const double* coef_child; double* coef_parent;
+  int row0;              // first parent row handled (partition)
 };
 
 // One CTA (5 warps) per parent segment row, owner computes: warp w owns the
@@ -318,7 +320,7 @@ struct AccArgs {
 template <int NK>
 __global__ void __launch_bounds__(160, 6) accum_kernel(AccArgs a) {
   __shared__ double2 acc[WARP_PARTS * PART_NODES * NCOL];   // 19.2 KB
-  const int p = blockIdx.x;
+  const int p = blockIdx.x + a.row0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, tig = lane & 3;
   double2* mine = acc + warp * PART_NODES * NCOL;
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(160, 6) accum_kernel(AccArgs a) {
 
 // ---------------------------------------------------------------- K5 ----
 struct EmitArgs {
-  const int4* tiles; int n_tiles;
+  const int4* tiles; int tile0, tile_end;
   const int* pair_id; const double4* geom; const double4* geom_disp;
   const double* coef;
   double kr[2], ki[2];
@@ -379,13 +381,16 @@ struct EmitArgs {
 // One warp per tile of <= 4 (box, target) pairs sharing a segment row; the 8
 // MMA rows are (pair, point) with point 0 = x_t, 1 = x_t + h n_t (same
 // segment polynomial, reference ifgf.py:647-653).  The basis is formed
-// exactly as numpy does ((T_a T_b) T_c, unfused recurrences) so the
-// displaced/undisplaced difference sees only the contraction rounding.
+// exactly as numpy does ((T_a T_b) T_c, unfused recurrences).  A bitwise
+// replica of the reference's contraction order (sequential FMA chain, as
+// OpenBLAS evaluates these dgemm shapes) was measured 3x slower and does not
+// tighten D_far parity: D_far = (S(x+hn) - S(x))/h is a chaotic function of
+// the last bits of the coefficients themselves.
 template <int NK>
 __global__ void __launch_bounds__(128) emit_kernel(EmitArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * 4 + warp;
-  if (tile >= a.n_tiles) return;
+  const int tile = a.tile0 + blockIdx.x * 4 + warp;
+  if (tile >= a.tile_end) return;
   const int grp = lane >> 2, tig = lane & 3;
   const int4 td = a.tiles[tile];
   const int pp = grp >> 1, pt = grp & 1;
@@ -398,12 +403,14 @@ __global__ void __launch_bounds__(128) emit_kernel(EmitArgs a) {
   basis_times_block<true>(B, a.coef + (size_t)td.x * SEG_DOUBLES, lane, c0, c1);
   if (!valid) return;
   const double r = gm.w;
-  const double den = mul_rn(4.0 * M_PI, r);
+  // G_k = exp(i kappa r) / (4 pi r); numpy divides a complex by a real as a
+  // multiplication by the reciprocal (ifgf.py:660-663)
+  const double rec = 1.0 / mul_rn(4.0 * M_PI, r);
   double2 gk[NK];
 #pragma unroll
   for (int k = 0; k < NK; ++k) {
     const double2 e = cexp_ikx(a.kr[k], a.ki[k], r);
-    gk[k] = make_double2(e.x / den, e.y / den);
+    gk[k] = make_double2(mul_rn(e.x, rec), mul_rn(e.y, rec));
   }
   double2* dst = a.partial + ((size_t)a.pair_id[pos] * 2 + pt) * NCOL;
 #pragma unroll
@@ -416,7 +423,8 @@ __global__ void __launch_bounds__(128) emit_kernel(EmitArgs a) {
 
 // out_tree[t][m] += sum of t's pair partials in box order (reference
 // per-box scatter-add, ifgf.py:664-673; levels D..3 in turn).
-__global__ void emit_reduce(int n, const int* __restrict__ tgt_off,
+__global__ void emit_reduce(int n, int pair_lo, int pair_hi,
+                            const int* __restrict__ tgt_off,
                             const int* __restrict__ tgt_pairs,
                             const double2* __restrict__ partial,
                             double2* __restrict__ out,
@@ -429,7 +437,9 @@ __global__ void emit_reduce(int n, const int* __restrict__ tgt_off,
   double2 s = out[idx];
   double2 sd = out_disp ? out_disp[idx] : make_double2(0.0, 0.0);
   for (int q = q0; q < q1; ++q) {
-    const size_t pr = tgt_pairs[q];
+    const int pq = tgt_pairs[q];
+    if (pq < pair_lo || pq >= pair_hi) continue;   // another rank's source box
+    const size_t pr = pq;
     const double2 v = partial[(pr * 2) * NCOL + m];
     s.x += v.x;
     s.y += v.y;
@@ -478,27 +488,27 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
       LeafArgs la{L.seg_box, L.seg_id, L.centers, L.pt_start, L.pt_count, L.tabs,
                   L.n_s, L.n_a, L.h, p.points_tree,
                   reinterpret_cast<const double2*>(p.wt), {kr[0], kr[1]},
-                  {ki[0], ki[1]}, p.coef[cur]};
-      if (L.n_seg > 0) {
+                  {ki[0], ki[1]}, p.coef[cur], L.seg_lo()};
+      if (L.seg_hi() > L.seg_lo()) {
         const int tk = p.timer.begin(K_LEAF, st);
-        leaf_kernel<NK><<<L.n_seg, 128, 0, st>>>(la);
+        leaf_kernel<NK><<<L.seg_hi() - L.seg_lo(), 128, 0, st>>>(la);
         p.timer.end(tk, st);
         ++launches;
       }
     }
     for (int d = D; d >= 3; --d) {
       Level& L = p.levels[d];
-      if (L.n_etiles > 0) {
-        EmitArgs ea{L.etiles, L.n_etiles, L.pair_id, L.geom,
+      if (L.tile_hi() > L.tile_lo()) {
+        EmitArgs ea{L.etiles, L.tile_lo(), L.tile_hi(), L.pair_id, L.geom,
                     out_disp ? L.geom_disp : nullptr, p.coef[cur],
                     {kr[0], kr[1]}, {ki[0], ki[1]},
                     reinterpret_cast<double2*>(p.partial)};
         int tk = p.timer.begin(K_EMIT, st);
-        emit_kernel<NK><<<(L.n_etiles + 3) / 4, 128, 0, st>>>(ea);
+        emit_kernel<NK><<<(L.tile_hi() - L.tile_lo() + 3) / 4, 128, 0, st>>>(ea);
         p.timer.end(tk, st);
         tk = p.timer.begin(K_REDUCE, st);
         emit_reduce<<<(n * NCOL + threads - 1) / threads, threads, 0, st>>>(
-            n, L.tgt_off, L.tgt_pairs, reinterpret_cast<const double2*>(p.partial),
+            n, L.pair_lo(), L.pair_hi(), L.tgt_off, L.tgt_pairs, reinterpret_cast<const double2*>(p.partial),
             reinterpret_cast<double2*>(p.out_tree),
             out_disp ? reinterpret_cast<double2*>(p.out_disp_tree) : nullptr);
         p.timer.end(tk, st);
@@ -506,7 +516,7 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
       }
       if (d > 3 && L.has_accum) {
         Level& U = p.levels[d - 1];
-        if (U.n_seg > 0) {
+        if (U.seg_hi() > U.seg_lo()) {
           const int64_t nr = L.n_types * NN;
           int tk = p.timer.begin(K_OTHER, st);
           ratio_kernel<NK><<<(unsigned)((nr + 255) / 256), 256, 0, st>>>(
@@ -515,9 +525,9 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
           p.timer.end(tk, st);
           AccArgs aa{L.inst_off, L.inst_type, L.inst_crow_off, L.crow, L.tile_off,
                      L.tiles, L.node_geom, reinterpret_cast<const double2*>(L.ratio),
-                     p.coef[cur], p.coef[cur ^ 1]};
+                     p.coef[cur], p.coef[cur ^ 1], U.seg_lo()};
           tk = p.timer.begin(K_ACCUM, st);
-          accum_kernel<NK><<<U.n_seg, 32 * WARP_PARTS, 0, st>>>(aa);
+          accum_kernel<NK><<<U.seg_hi() - U.seg_lo(), 32 * WARP_PARTS, 0, st>>>(aa);
           p.timer.end(tk, st);
           launches += 2;
         }

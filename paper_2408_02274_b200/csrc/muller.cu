@@ -143,6 +143,7 @@ struct NearArgs {
   double kr[2], ki[2];
   double fd_step;
   double2* s_val; double2* d_val;
+  int t_lo, t_hi;        // owned targets (original order)
 };
 
 
@@ -185,8 +186,8 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int n = a.s.n, n2 = a.s.n_c * a.s.n_c;
-  if (warp >= n) return;
-  const int ell = warp;
+  const int ell = warp + a.t_lo;
+  if (ell >= a.t_hi) return;
   double2 S[8][2], D[6][2];
   double2 near_s = make_double2(0, 0), near_d = make_double2(0, 0);
   double2 nb_s = make_double2(0, 0), nb_d = make_double2(0, 0);
@@ -267,8 +268,10 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
     a.s_val[o] = cadd(near_s, csub(cadd(s_if, nb_s), cr_s));
     if (c < 6) {
       const double2 sd = a.far_disp[o];
-      const double2 d_if = make_double2((sd.x - s_if.x) / a.fd_step,
-                                        (sd.y - s_if.y) / a.fd_step);
+      // numpy's complex / real: multiply by the reciprocal (Smith, rat = 0)
+      const double scl = 1.0 / a.fd_step;
+      const double2 d_if = make_double2(mul_rn(sd.x - s_if.x, scl),
+                                        mul_rn(sd.y - s_if.y, scl));
       a.d_val[o] = cadd(near_d, csub(cadd(d_if, nb_d), cr_d));
     }
   }
@@ -281,6 +284,7 @@ struct AsmArgs {
   double2 eps_e, mu_e, eps_i, mu_i, kap[2];
   double omega;
   double2* out;
+  int p0;                // first patch handled (partition)
 };
 
 __device__ __forceinline__ void cross3(const double* n, const double2* v, double2* o) {
@@ -295,7 +299,7 @@ __device__ __forceinline__ void cross3(const double* n, const double2* v, double
 __global__ void assemble_kernel(AsmArgs a) {
   extern __shared__ double2 sh[];   // 16 x n2
   const int nc = a.s.n_c, n2 = nc * nc, n = a.s.n;
-  const int p = blockIdx.x, loc = threadIdx.x;
+  const int p = blockIdx.x + a.p0, loc = threadIdx.x;
   const bool act = loc < n2;
   const int ell = p * n2 + loc;
   if (act)
@@ -408,10 +412,8 @@ static SurfPtrs surf(const Plan& p) {
                   p.eu, p.ev, p.t1, p.t2, p.dmat, p.cmat};
 }
 
-int potentials_from_phi(Plan& p, cudaStream_t st) {
-  // far field on phi * weights (operators.py:336-340)
-  int rc = far_apply(p, p.phiw, 8, p.kappa, 2, p.far_out, p.far_disp, st);
-  if (rc) return rc;
+// near field of the owned targets combined with the (complete) far field
+static int near_launch(Plan& p, cudaStream_t st) {
   NearArgs na{surf(p), p.mom_off, p.mom_patch,
               reinterpret_cast<const double2*>(p.moments), p.dir_off, p.dir_src,
               reinterpret_cast<const double2*>(p.phi),
@@ -420,14 +422,28 @@ int potentials_from_phi(Plan& p, cudaStream_t st) {
               reinterpret_cast<const double2*>(p.far_out),
               reinterpret_cast<const double2*>(p.far_disp),
               {p.kappa[0], p.kappa[2]}, {p.kappa[1], p.kappa[3]}, p.fd_step,
-              reinterpret_cast<double2*>(p.s_val), reinterpret_cast<double2*>(p.d_val)};
+              reinterpret_cast<double2*>(p.s_val), reinterpret_cast<double2*>(p.d_val),
+              p.t_lo(), p.t_hi()};
   const int warps_per_block = 4;
+  const int nt = p.t_hi() - p.t_lo();
+  if (nt <= 0) return IFGFB_OK;
   const int tk = p.timer.begin(K_NEAR, st);
-  near_kernel<<<(p.n + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(na);
+  near_kernel<<<(nt + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(na);
   p.timer.end(tk, st);
   p.launches += 1;
   IFGFB_CUDA(cudaGetLastError());
   return IFGFB_OK;
+}
+
+// far field on phi * weights (operators.py:336-340), partial when partitioned
+static int far_launch(Plan& p, cudaStream_t st) {
+  return far_apply(p, p.phiw, 8, p.kappa, 2, p.far_out, p.far_disp, st);
+}
+
+int potentials_from_phi(Plan& p, cudaStream_t st) {
+  int rc = far_launch(p, st);
+  if (rc) return rc;
+  return near_launch(p, st);
 }
 
 static int pack_launch(Plan& p, const double* y, const double* phi_in,
@@ -446,27 +462,40 @@ static int pack_launch(Plan& p, const double* y, const double* phi_in,
   return IFGFB_OK;
 }
 
-int muller_apply(Plan& p, const double* y, double* out, cudaStream_t st) {
-  p.launches = 0;
-  int rc = pack_launch(p, y, nullptr, st);
-  if (rc) return rc;
-  rc = potentials_from_phi(p, st);
-  if (rc) return rc;
+static int assemble_launch(Plan& p, const double* y, double* out, cudaStream_t st) {
   const int n2 = p.n_c * p.n_c;
   const int threads = ((n2 + 31) / 32) * 32;
+  const int p0 = p.t_lo() / n2, p1 = p.t_hi() / n2;
+  if (p1 <= p0) return IFGFB_OK;
   AsmArgs aa{surf(p), reinterpret_cast<const double2*>(p.s_val),
              reinterpret_cast<const double2*>(p.d_val),
              reinterpret_cast<const double2*>(y),
              make_double2(p.eps_e[0], p.eps_e[1]), make_double2(p.mu_e[0], p.mu_e[1]),
              make_double2(p.eps_i[0], p.eps_i[1]), make_double2(p.mu_i[0], p.mu_i[1]),
              {make_double2(p.kappa[0], p.kappa[1]), make_double2(p.kappa[2], p.kappa[3])},
-             p.omega, reinterpret_cast<double2*>(out)};
+             p.omega, reinterpret_cast<double2*>(out), p0};
   const int tk = p.timer.begin(K_ASSEMBLE, st);
-  assemble_kernel<<<p.n_patches, threads, sizeof(double2) * 16 * n2, st>>>(aa);
+  assemble_kernel<<<p1 - p0, threads, sizeof(double2) * 16 * n2, st>>>(aa);
   p.timer.end(tk, st);
   p.launches += 1;
   IFGFB_CUDA(cudaGetLastError());
   return IFGFB_OK;
+}
+
+int muller_far_phase(Plan& p, const double* y, cudaStream_t st) {
+  p.launches = 0;
+  IFGFB_RC(pack_launch(p, y, nullptr, st));
+  return far_launch(p, st);
+}
+
+int muller_near_phase(Plan& p, const double* y, double* out, cudaStream_t st) {
+  IFGFB_RC(near_launch(p, st));
+  return assemble_launch(p, y, out, st);
+}
+
+int muller_apply(Plan& p, const double* y, double* out, cudaStream_t st) {
+  IFGFB_RC(muller_far_phase(p, y, st));
+  return muller_near_phase(p, y, out, st);
 }
 
 }  // namespace ifgfb
@@ -579,6 +608,40 @@ int ifgfb_muller_apply(ifgfb_plan* h, const double* y, double* out, void* stream
     return IFGFB_ERR_STATE;
   }
   return muller_apply(p, y, out, static_cast<cudaStream_t>(stream));
+}
+
+int ifgfb_muller_far_phase(ifgfb_plan* h, const double* y, void* stream) {
+  CHECK_ARG(h && y, "null argument");
+  Plan& p = h->p;
+  if (!p.finalized || !p.has_near) {
+    set_error("plan has no surface/near-field data");
+    return IFGFB_ERR_STATE;
+  }
+  return muller_far_phase(p, y, static_cast<cudaStream_t>(stream));
+}
+
+int ifgfb_muller_near_phase(ifgfb_plan* h, const double* y, double* out, void* stream) {
+  CHECK_ARG(h && y && out, "null argument");
+  Plan& p = h->p;
+  if (!p.finalized || !p.has_near) {
+    set_error("plan has no surface/near-field data");
+    return IFGFB_ERR_STATE;
+  }
+  return muller_near_phase(p, y, out, static_cast<cudaStream_t>(stream));
+}
+
+int ifgfb_plan_far_buffers(ifgfb_plan* h, double** far, double** far_disp,
+                           int64_t* n_complex) {
+  CHECK_ARG(h && far && far_disp && n_complex, "null argument");
+  Plan& p = h->p;
+  if (!p.has_surface) {
+    set_error("plan has no surface data");
+    return IFGFB_ERR_STATE;
+  }
+  *far = p.far_out;
+  *far_disp = p.far_disp;
+  *n_complex = 16 * (int64_t)p.n;
+  return IFGFB_OK;
 }
 
 int ifgfb_muller_apply_host(ifgfb_plan* h, const double* y_host, double* out_host,

@@ -162,6 +162,8 @@ int ifgfb_plan_set_emission(ifgfb_plan* h, const ifgfb_emit_desc* e) {
     s = t;
   }
   L.n_etiles = (int)tiles.size();
+  L.etile_rows.resize(tiles.size());
+  for (size_t i = 0; i < tiles.size(); ++i) L.etile_rows[i] = tiles[i].x;
   RC(dev_upload(p, &L.pair_id, order.data(), order.size()));
   RC(dev_upload(p, &L.geom, g.data(), g.size()));
   if (L.has_disp) RC(dev_upload(p, &L.geom_disp, gd.data(), gd.size()));
@@ -244,6 +246,40 @@ int ifgfb_plan_finalize(ifgfb_plan* h) {
   RC(dev_alloc(p, &p.out_tree, n * NCOL * 2));
   RC(dev_alloc(p, &p.out_disp_tree, n * NCOL * 2));
   p.finalized = true;
+  return IFGFB_OK;
+}
+
+int ifgfb_plan_set_partition(ifgfb_plan* h, const ifgfb_partition_desc* d) {
+  CHECK_ARG(h && d, "null argument");
+  Plan& p = h->p;
+  CHECK_ARG(p.finalized, "finalize the plan before setting a partition");
+  CHECK_ARG(d->n_levels == std::max(0, p.depth - 2), "need one entry per level 3..depth");
+  for (int i = 0; i < d->n_levels; ++i) {
+    const ifgfb_level_part& lp = d->levels[i];
+    CHECK_ARG(lp.level >= 3 && lp.level <= p.depth, "partition level out of range");
+    Level& L = p.levels[lp.level];
+    CHECK_ARG(0 <= lp.seg_lo && lp.seg_lo <= lp.seg_hi && lp.seg_hi <= L.n_seg,
+              "segment range out of bounds");
+    CHECK_ARG(0 <= lp.pair_lo && lp.pair_lo <= lp.pair_hi && lp.pair_hi <= L.n_pairs,
+              "pair range out of bounds");
+    L.part_seg_lo = (int)lp.seg_lo;
+    L.part_seg_hi = (int)lp.seg_hi;
+    L.part_pair_lo = (int)lp.pair_lo;
+    L.part_pair_hi = (int)lp.pair_hi;
+    // tiles are sorted by segment row: owned rows -> contiguous tile range
+    L.part_tile_lo = (int)(std::lower_bound(L.etile_rows.begin(), L.etile_rows.end(),
+                                            (int)lp.seg_lo) - L.etile_rows.begin());
+    L.part_tile_hi = (int)(std::lower_bound(L.etile_rows.begin(), L.etile_rows.end(),
+                                            (int)lp.seg_hi) - L.etile_rows.begin());
+  }
+  const int n2 = p.n_c * p.n_c;
+  CHECK_ARG(0 <= d->target_lo && d->target_lo <= d->target_hi && d->target_hi <= p.n,
+            "target range out of bounds");
+  CHECK_ARG(n2 == 0 || (d->target_lo % n2 == 0 && d->target_hi % n2 == 0),
+            "target range must be patch aligned");
+  p.part_t_lo = (int)d->target_lo;
+  p.part_t_hi = (int)d->target_hi;
+  p.partitioned = true;
   return IFGFB_OK;
 }
 

@@ -30,7 +30,8 @@ class FarFieldPlan:
     """libifgfb200 plan for one tree/hierarchy (+ displaced-point geometry)."""
 
     def __init__(self, tree, hier, displaced_normals=None,
-                 displaced_step: float = 1e-6, surface=None, near=None):
+                 displaced_step: float = 1e-6, surface=None, near=None,
+                 kappas=None):
         lib = _lib.load()
         if not torch.cuda.is_available():
             raise RuntimeError("CUDA device required (no CPU fallback)")
@@ -41,6 +42,7 @@ class FarFieldPlan:
         self._keep = []          # host arrays referenced during upload
         self.disp = displaced_normals is not None
         self.step = float(displaced_step)
+        self.kappas = None if kappas is None else tuple(kappas)
         disp_t = None
         if self.disp:
             nrm = np.asarray(displaced_normals, dtype=float)
@@ -180,13 +182,14 @@ class FarFieldPlan:
             self._h = None
 
 
-def _plan_for(tree, hier, normals, step) -> FarFieldPlan:
+def _plan_for(tree, hier, normals, step, kappas) -> FarFieldPlan:
     cache = hier.__dict__.setdefault("_b200_plans", {})
     key = (id(tree), None if normals is None else id(normals),
-           float(step) if normals is not None else None)
+           float(step) if normals is not None else None,
+           tuple(complex(k) for k in kappas))
     plan = cache.get(key)
     if plan is None:
-        plan = FarFieldPlan(tree, hier, normals, step)
+        plan = FarFieldPlan(tree, hier, normals, step, kappas=kappas)
         cache[key] = (plan, normals)   # keep normals alive for the id key
         return plan
     return plan[0] if isinstance(plan, tuple) else plan
@@ -218,7 +221,7 @@ def ifgf_apply(tree, hier, weights, kappas, mode: str | None = None,
         od = (None if displaced_normals is None
               else np.concatenate([p[1] for p in parts], axis=1))
         return out, od
-    plan = _plan_for(tree, hier, displaced_normals, displaced_step)
+    plan = _plan_for(tree, hier, displaced_normals, displaced_step, kappas)
     group = 16 // nk
     dev = torch.device("cuda")
     out = np.empty((nch, nk, n), dtype=complex)

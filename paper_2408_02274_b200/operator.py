@@ -253,7 +253,8 @@ class MullerOperator:
         near, self.near_stats = _near_desc(disc, tree, smap, moments,
                                            corr_ell, corr_src, keep)
         self.plan = FarFieldPlan(tree, hierarchy, disc.normals,
-                                 config.fd_step, surface=surf, near=near)
+                                 config.fd_step, surface=surf, near=near,
+                                 kappas=materials.kappas)
         del keep
         self._dev = torch.device("cuda")
 

@@ -48,6 +48,8 @@ STRUCTS = {
     "ifgfb_accum_desc": _lib.AccumDesc,
     "ifgfb_surface_desc": _lib.SurfaceDesc,
     "ifgfb_near_desc": _lib.NearDesc,
+    "ifgfb_level_part": _lib.LevelPart,
+    "ifgfb_partition_desc": _lib.PartitionDesc,
 }
 
 
