@@ -6,10 +6,11 @@
 // Reference: ifgf.py:788-882 (propagate_and_emit), ifgf.py:535-554 (K2),
 // ifgf.py:502-522 (K3), ifgf.py:752-785 (K4), ifgf.py:630-673 (K5).
 //
-// Data layout in HBM: per level one coefficient array [n_seg][75][16]
-// complex (node-major, column m = channel*nk + kernel, the reference's
-// c*nk + k flattening), 19.2 KB per segment; two such arrays are live
-// (child level / parent level ping-pong).
+// Data layout in HBM: per level one coefficient array of 20 KB segments in
+// DMMA fragment order (see SEG_DOUBLES), holding the rows this rank owns
+// (all rows without a partition; buffers are addressed through a base
+// pointer shifted by the first owned row); two arrays are live (child level
+// / parent level ping-pong).
 #include "common.cuh"
 
 namespace ifgfb {
@@ -488,7 +489,8 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
       LeafArgs la{L.seg_box, L.seg_id, L.centers, L.pt_start, L.pt_count, L.tabs,
                   L.n_s, L.n_a, L.h, p.points_tree,
                   reinterpret_cast<const double2*>(p.wt), {kr[0], kr[1]},
-                  {ki[0], ki[1]}, p.coef[cur], L.seg_lo()};
+                  {ki[0], ki[1]}, p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
+                  L.seg_lo()};
       if (L.seg_hi() > L.seg_lo()) {
         const int tk = p.timer.begin(K_LEAF, st);
         leaf_kernel<NK><<<L.seg_hi() - L.seg_lo(), 128, 0, st>>>(la);
@@ -500,7 +502,8 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
       Level& L = p.levels[d];
       if (L.tile_hi() > L.tile_lo()) {
         EmitArgs ea{L.etiles, L.tile_lo(), L.tile_hi(), L.pair_id, L.geom,
-                    out_disp ? L.geom_disp : nullptr, p.coef[cur],
+                    out_disp ? L.geom_disp : nullptr,
+                    p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
                     {kr[0], kr[1]}, {ki[0], ki[1]},
                     reinterpret_cast<double2*>(p.partial)};
         int tk = p.timer.begin(K_EMIT, st);
@@ -525,7 +528,8 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
           p.timer.end(tk, st);
           AccArgs aa{L.inst_off, L.inst_type, L.inst_crow_off, L.crow, L.tile_off,
                      L.tiles, L.node_geom, reinterpret_cast<const double2*>(L.ratio),
-                     p.coef[cur], p.coef[cur ^ 1], U.seg_lo()};
+                     p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
+                     p.coef[cur ^ 1] - (size_t)U.seg_lo() * SEG_DOUBLES, U.seg_lo()};
           tk = p.timer.begin(K_ACCUM, st);
           accum_kernel<NK><<<U.seg_hi() - U.seg_lo(), 32 * WARP_PARTS, 0, st>>>(aa);
           p.timer.end(tk, st);

@@ -280,6 +280,20 @@ int ifgfb_plan_set_partition(ifgfb_plan* h, const ifgfb_partition_desc* d) {
   p.part_t_lo = (int)d->target_lo;
   p.part_t_hi = (int)d->target_hi;
   p.partitioned = true;
+  // coefficient buffers only need the owned rows of any level
+  size_t need = 1;
+  for (int dd = 3; dd <= p.depth; ++dd)
+    need = std::max(need, (size_t)(p.levels[dd].seg_hi() - p.levels[dd].seg_lo()));
+  if (need < p.coef_cap) {
+    for (int i = 0; i < 2; ++i) {
+      auto it = std::find(p.allocations.begin(), p.allocations.end(), (void*)p.coef[i]);
+      if (it != p.allocations.end()) p.allocations.erase(it);
+      IFGFB_CUDA(cudaFree(p.coef[i]));
+      p.bytes -= p.coef_cap * SEG_DOUBLES * sizeof(double);
+      RC(dev_alloc(p, &p.coef[i], need * SEG_DOUBLES));
+    }
+    p.coef_cap = need;
+  }
   return IFGFB_OK;
 }
 

@@ -65,6 +65,8 @@ def test_partitioned_apply_equals_single_gpu(name, n_ranks):
                                  tree=ops[0].op.tree, hierarchy=ops[0].op.hierarchy)
     ref1 = single.apply(z["y"])
     assert rel(got, ref1) < 1e-10
+    # each rank only holds coefficient rows of its own subtrees
+    assert all(o.op.plan.device_bytes() < single.plan.device_bytes() for o in ops)
     if plan_matches_golden(name):
         assert rel(got, z["apply_y"]) < 1e-10
 
