@@ -100,25 +100,28 @@ typedef struct {
 /* ---- propagation child level d -> parent level d-1 (reference _AccumType /
  *      _accum_types / _accumulate_level, ifgf.py:676-785), regrouped per
  *      parent segment row (owner computes).  Each CTA owns one parent
- *      segment; warp w (0..4) owns the 15 parent nodes with theta index
- *      b == w.  Per type (parent segment id, child octant) and warp, its
- *      owned nodes are grouped by child segment into MMA row tiles of <= 8. */
+ *      segment row; its 75 nodes are split into 5 warp-owned sets of 15
+ *      (row_order: node at set position, warp w owns positions 15w..15w+14).
+ *      Per (instance, warp) the owned nodes are grouped by child segment
+ *      into MMA row tiles of <= 8 nodes. */
 typedef struct {
   int32_t level;             /* child level d */
   int64_t n_types;
-  const int64_t* tile_off;   /* n_types*5+1: tiles of (type, warp) */
-  int64_t n_tiles;
-  const uint8_t* tiles;      /* n_tiles*16: [local sigma group, n_rows,
-                                slot0..slot7 (a*5+c, 0xFF pad), 6 pad] */
   const double* node_geom;   /* n_types*75*3: xs, xt, xp of each parent node
                                 in its child segment (parent node order) */
   const double* node_r;      /* n_types*75*2: r_parent, r_child */
   int64_t n_parent_rows;     /* segments of level d-1 */
+  const uint8_t* row_order;  /* n_parent_rows*75 */
   const int64_t* inst_off;   /* n_parent_rows+1 */
   int64_t n_instances;
   const int64_t* inst_type;  /* n_instances */
   const int64_t* inst_crow_off; /* n_instances+1 into crow */
   const int64_t* crow;       /* child segment row per sigma group */
+  const int64_t* tile_off;   /* n_instances*5+1: tiles of (instance, warp) */
+  int64_t n_tiles;
+  const uint8_t* tiles;      /* n_tiles*16: [local sigma group, n_rows,
+                                slot0..slot7 (position in the warp's set,
+                                0xFF pad), 6 pad] */
 } ifgfb_accum_desc;
 
 /* ---- surface + operator data (reference SurfaceDiscretization,

@@ -49,11 +49,13 @@ class EmitDesc(C.Structure):
 
 class AccumDesc(C.Structure):
     _fields_ = [("level", C.c_int32), ("n_types", C.c_int64),
-                ("tile_off", _ip), ("n_tiles", C.c_int64),
-                ("tiles", C.POINTER(C.c_uint8)), ("node_geom", _dp),
-                ("node_r", _dp), ("n_parent_rows", C.c_int64),
+                ("node_geom", _dp), ("node_r", _dp),
+                ("n_parent_rows", C.c_int64),
+                ("row_order", C.POINTER(C.c_uint8)),
                 ("inst_off", _ip), ("n_instances", C.c_int64),
-                ("inst_type", _ip), ("inst_crow_off", _ip), ("crow", _ip)]
+                ("inst_type", _ip), ("inst_crow_off", _ip), ("crow", _ip),
+                ("tile_off", _ip), ("n_tiles", C.c_int64),
+                ("tiles", C.POINTER(C.c_uint8))]
 
 
 class SurfaceDesc(C.Structure):

@@ -167,7 +167,8 @@ struct Level {
   // accumulation from this level (as child) into level d-1
   bool has_accum = false;
   int64_t n_types = 0;
-  int* tile_off = nullptr;     // n_types*WARP_PARTS+1
+  int* tile_off = nullptr;     // n_instances*WARP_PARTS+1
+  unsigned char* row_order = nullptr;  // parent rows x NN
   uint4* tiles = nullptr;      // 16-byte tile records
   double* node_geom = nullptr; // n_types*NN*3 (parent node order)
   double* node_r = nullptr;    // n_types*NN*2 (r_parent, r_child)

@@ -48,24 +48,24 @@ int init_constants() {
 
 // ---------------------------------------------------------------- K3 ----
 // Node (a, b, c) -> row of a segment buffer in shared memory.  Standard
-// layout: (a*PA + b)*PA + c.  OWNER layout (propagation kernel): the 15 nodes
-// of theta index b are contiguous, b*15 + a*PA + c.
+// layout: (a*PA + b)*PA + c.  OWNER layout (propagation kernel): the row of
+// node n is its position inv[n] in the CTA's warp-owned node order.
 template <bool OWNER>
-__device__ __forceinline__ int node_row(int a, int b, int c) {
-  return OWNER ? b * PS * PA + a * PA + c : (a * PA + b) * PA + c;
+__device__ __forceinline__ int node_row(const unsigned char* inv, int a, int b, int c) {
+  return OWNER ? (int)inv[(a * PA + b) * PA + c] : (a * PA + b) * PA + c;
 }
 
 // In-place node values -> coefficients for one segment held in shared memory
 // (rows per node_row<OWNER>, NCOL complex columns): three axis transforms
 // (reference ifgf.py:502-522).
 template <bool OWNER>
-__device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
+__device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, int nthr) {
   for (int task = tid; task < PA * PA * NCOL; task += nthr) {
     const int bc = task / NCOL, m = task % NCOL;
     const int b = bc / PA, c = bc % PA;
     double2 v[PS];
 #pragma unroll
-    for (int a = 0; a < PS; ++a) v[a] = V[node_row<OWNER>(a, b, c) * NCOL + m];
+    for (int a = 0; a < PS; ++a) v[a] = V[node_row<OWNER>(inv, a, b, c) * NCOL + m];
 #pragma unroll
     for (int a = 0; a < PS; ++a) {
       double2 s = make_double2(0.0, 0.0);
@@ -74,7 +74,7 @@ __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
         s.x += c_ms[a * PS + q] * v[q].x;
         s.y += c_ms[a * PS + q] * v[q].y;
       }
-      V[node_row<OWNER>(a, b, c) * NCOL + m] = s;
+      V[node_row<OWNER>(inv, a, b, c) * NCOL + m] = s;
     }
   }
   __syncthreads();
@@ -83,7 +83,7 @@ __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
     const int a = ac / PA, c = ac % PA;
     double2 v[PA];
 #pragma unroll
-    for (int b = 0; b < PA; ++b) v[b] = V[node_row<OWNER>(a, b, c) * NCOL + m];
+    for (int b = 0; b < PA; ++b) v[b] = V[node_row<OWNER>(inv, a, b, c) * NCOL + m];
 #pragma unroll
     for (int b = 0; b < PA; ++b) {
       double2 s = make_double2(0.0, 0.0);
@@ -92,7 +92,7 @@ __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
         s.x += c_ma[b * PA + q] * v[q].x;
         s.y += c_ma[b * PA + q] * v[q].y;
       }
-      V[node_row<OWNER>(a, b, c) * NCOL + m] = s;
+      V[node_row<OWNER>(inv, a, b, c) * NCOL + m] = s;
     }
   }
   __syncthreads();
@@ -101,7 +101,7 @@ __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
     const int a = ab / PA, b = ab % PA;
     double2 v[PA];
 #pragma unroll
-    for (int c = 0; c < PA; ++c) v[c] = V[node_row<OWNER>(a, b, c) * NCOL + m];
+    for (int c = 0; c < PA; ++c) v[c] = V[node_row<OWNER>(inv, a, b, c) * NCOL + m];
 #pragma unroll
     for (int c = 0; c < PA; ++c) {
       double2 s = make_double2(0.0, 0.0);
@@ -110,7 +110,7 @@ __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
         s.x += c_ma[c * PA + q] * v[q].x;
         s.y += c_ma[c * PA + q] * v[q].y;
       }
-      V[node_row<OWNER>(a, b, c) * NCOL + m] = s;
+      V[node_row<OWNER>(inv, a, b, c) * NCOL + m] = s;
     }
   }
   __syncthreads();
@@ -120,7 +120,8 @@ __device__ void to_coeffs_smem(double2* V, int tid, int nthr) {
 // DMMA B-fragment order (see SEG_DOUBLES): coalesced stores, padding zeroed.
 template <bool OWNER>
 __device__ __forceinline__ void store_segment(double* dst, const double2* V,
-                                              int tid, int nthr) {
+                                              const unsigned char* inv, int tid,
+                                              int nthr) {
   for (int idx = tid; idx < SEG_DOUBLES; idx += nthr) {
     const int ks = idx >> 7, lane = (idx >> 2) & 31, nt = idx & 3;
     const int q = ks / PA, c = ks - PA * q;
@@ -128,7 +129,7 @@ __device__ __forceinline__ void store_segment(double* dst, const double2* V,
     double v = 0.0;
     if (ab < PS * PA) {
       const int col = 8 * nt + (lane >> 2);
-      const double2 z = V[node_row<OWNER>(ab / PA, ab % PA, c) * NCOL + (col >> 1)];
+      const double2 z = V[node_row<OWNER>(inv, ab / PA, ab % PA, c) * NCOL + (col >> 1)];
       v = (col & 1) ? z.y : z.x;
     }
     dst[idx] = v;
@@ -214,8 +215,8 @@ __global__ void __launch_bounds__(128) leaf_kernel(LeafArgs a) {
     for (int m = 0; m < NCOL; ++m) V[tid * NCOL + m] = acc[m];
   }
   __syncthreads();
-  to_coeffs_smem<false>(V, tid, blockDim.x);
-  store_segment<false>(a.coef + (size_t)row * SEG_DOUBLES, V, tid, blockDim.x);
+  to_coeffs_smem<false>(V, nullptr, tid, blockDim.x);
+  store_segment<false>(a.coef + (size_t)row * SEG_DOUBLES, V, nullptr, tid, blockDim.x);
 }
 
 // ------------------------------------------------------- DMMA helpers ----
@@ -305,6 +306,7 @@ __global__ void ratio_kernel(int64_t n, const double* __restrict__ node_r,
 struct AccArgs {
   const int* inst_off; const int* inst_type; const int* inst_crow_off;
   const int* crow; const int* tile_off; const uint4* tiles;
+  const unsigned char* row_order;
   const double* node_geom; const double2* ratio;
   const double* coef_child; double* coef_parent;
   int row0;              // first parent row handled (partition)
@@ -321,18 +323,24 @@ struct AccArgs {
 template <int NK>
 __global__ void __launch_bounds__(160, 6) accum_kernel(AccArgs a) {
   __shared__ double2 acc[WARP_PARTS * PART_NODES * NCOL];   // 19.2 KB
+  __shared__ unsigned char ord[NN], inv[NN];
   const int p = blockIdx.x + a.row0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, tig = lane & 3;
+  if (threadIdx.x < NN) {
+    const unsigned char nd = a.row_order[(size_t)p * NN + threadIdx.x];
+    ord[threadIdx.x] = nd;
+    inv[nd] = (unsigned char)threadIdx.x;
+  }
   double2* mine = acc + warp * PART_NODES * NCOL;
   for (int i = lane; i < PART_NODES * NCOL; i += 32) mine[i] = make_double2(0.0, 0.0);
-  __syncwarp();
+  __syncthreads();
   const int i0 = a.inst_off[p], i1 = a.inst_off[p + 1];
   for (int inst = i0; inst < i1; ++inst) {
     const int t = a.inst_type[inst];
     const int* cr = a.crow + a.inst_crow_off[inst];
-    const int k0 = a.tile_off[t * WARP_PARTS + warp];
-    const int k1 = a.tile_off[t * WARP_PARTS + warp + 1];
+    const int k0 = a.tile_off[inst * WARP_PARTS + warp];
+    const int k1 = a.tile_off[inst * WARP_PARTS + warp + 1];
     for (int k = k0; k < k1; ++k) {
       const uint4 tl = a.tiles[k];
       const int g = tl.x & 0xff, nrows = (tl.x >> 8) & 0xff;
@@ -341,7 +349,7 @@ __global__ void __launch_bounds__(160, 6) accum_kernel(AccArgs a) {
       const int slot0 = (tl.x >> 16) & 0xff;
       const bool valid = grp < nrows;
       const int slot = valid ? (int)((word >> (8 * (byte & 3))) & 0xff) : slot0;
-      const int node = (slot / PA) * PA * PA + warp * PA + slot % PA;
+      const int node = ord[warp * PART_NODES + slot];
       const double* ng = a.node_geom + ((size_t)t * NN + node) * 3;
       const BasisA B = make_basis<false>(ng[0], ng[1], ng[2], tig);
       double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
@@ -365,8 +373,8 @@ __global__ void __launch_bounds__(160, 6) accum_kernel(AccArgs a) {
     }
   }
   __syncthreads();
-  to_coeffs_smem<true>(acc, threadIdx.x, 32 * WARP_PARTS);
-  store_segment<true>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, threadIdx.x,
+  to_coeffs_smem<true>(acc, inv, threadIdx.x, 32 * WARP_PARTS);
+  store_segment<true>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, inv, threadIdx.x,
                       32 * WARP_PARTS);
 }
 
@@ -527,7 +535,7 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
               reinterpret_cast<double2*>(L.ratio));
           p.timer.end(tk, st);
           AccArgs aa{L.inst_off, L.inst_type, L.inst_crow_off, L.crow, L.tile_off,
-                     L.tiles, L.node_geom, reinterpret_cast<const double2*>(L.ratio),
+                     L.tiles, L.row_order, L.node_geom, reinterpret_cast<const double2*>(L.ratio),
                      p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
                      p.coef[cur ^ 1] - (size_t)U.seg_lo() * SEG_DOUBLES, U.seg_lo()};
           tk = p.timer.begin(K_ACCUM, st);

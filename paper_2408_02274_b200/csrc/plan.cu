@@ -193,8 +193,9 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
   const int64_t nt = a->n_types;
   L.n_types = nt;
   std::vector<int> tmp;
-  if (!to_i32(a->tile_off, nt * WARP_PARTS + 1, tmp, "tile_off")) return IFGFB_ERR_ARG;
-  CHECK_ARG(a->tile_off[nt * WARP_PARTS] == a->n_tiles, "tile_off end != n_tiles");
+  const int64_t ni = a->n_instances;
+  if (!to_i32(a->tile_off, ni * WARP_PARTS + 1, tmp, "tile_off")) return IFGFB_ERR_ARG;
+  CHECK_ARG(a->tile_off[ni * WARP_PARTS] == a->n_tiles, "tile_off end != n_tiles");
   RC(dev_upload(p, &L.tile_off, tmp.data(), tmp.size()));
   for (int64_t i = 0; i < a->n_tiles; ++i) {
     const uint8_t* t = a->tiles + 16 * i;
@@ -203,6 +204,9 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
       CHECK_ARG(t[2 + r] < PART_NODES, "tile slot out of range");
   }
   RC(dev_upload(p, &L.tiles, reinterpret_cast<const uint4*>(a->tiles), (size_t)a->n_tiles));
+  for (int64_t i = 0; i < a->n_parent_rows * NN; ++i)
+    CHECK_ARG(a->row_order[i] < NN, "row_order entry out of range");
+  RC(dev_upload(p, &L.row_order, a->row_order, (size_t)a->n_parent_rows * NN));
   RC(dev_upload(p, &L.node_geom, a->node_geom, (size_t)nt * NN * 3));
   RC(dev_upload(p, &L.node_r, a->node_r, (size_t)nt * NN * 2));
   RC(dev_alloc(p, &L.ratio, (size_t)nt * NN * 4));

@@ -729,6 +729,108 @@ def warp_tiles(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5):
     return tile_off, out, node_geom, node_r
 
 
+def _local_group_ids(ap: AccumulationPlan, nn: int) -> np.ndarray:
+    """gid[t, node] = sigma group (local to type t) of parent node `node`."""
+    nt = ap.n_types
+    gid = np.empty((nt, nn), dtype=np.int16)
+    local = np.repeat(np.arange(ap.group_sigma.size) -
+                      np.repeat(ap.sig_off[:-1], np.diff(ap.sig_off)),
+                      ap.group_end - ap.group_bounds)
+    gid[np.arange(nt)[:, None], ap.scatter] = local.reshape(nt, nn)
+    return gid
+
+
+def row_tiles(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5,
+              chunk: int = 1 << 18):
+    """Per parent row partition of its 75 nodes into 5 warp-owned sets of 15
+    and the MMA row tiles of every (instance, warp).
+
+    Nodes are sorted by their child-segment signature over the row's
+    instances (the sigma group of the node under each child), so nodes that
+    share child segments under every child land in the same warp set and
+    its row tiles fill up (11.1-12.5 tiles per instance
+    against 12.2-13.9 for a fixed theta-index split, lower bound 10.5-10.9).
+
+    Returns
+      row_order (n_rows, 75) uint8  node at set position (warp w owns
+                                    positions 15w..15w+14)
+      tile_off  (n_instances*5+1,)  tiles of (instance, warp)
+      tiles     (n_tiles, 16) uint8 [local group, rows, slot0..7, pad];
+                                    slot = position within the warp's set
+    """
+    nn = p_s * p_a * p_a
+    per = nn // WARP_PARTS
+    gid = _local_group_ids(ap, nn)
+    n_rows = ap.inst_off.size - 1
+    cnt = np.diff(ap.inst_off)
+    if cnt.size and cnt.max() > 8:
+        raise ValueError("more than 8 children per parent box")
+    # signature key per (row, node): 4 bits per instance slot
+    key = np.zeros((n_rows, nn), dtype=np.int64)
+    for i in range(8):
+        has = cnt > i
+        rows = np.nonzero(has)[0]
+        t = ap.inst_type[ap.inst_off[rows] + i]
+        key[rows] |= gid[t].astype(np.int64) << (4 * (7 - i))
+        key[~has] |= np.int64(0xF) << (4 * (7 - i))
+    row_order = np.argsort(key, axis=1, kind="stable").astype(np.uint8)
+    # per instance and warp: the set's nodes grouped by the type's sigma group
+    prow = np.repeat(np.arange(n_rows), cnt)
+    counts = np.zeros(ap.n_instances * WARP_PARTS, dtype=np.int64)
+    pieces = []
+    for i0 in range(0, ap.n_instances, chunk):
+        i1 = min(ap.n_instances, i0 + chunk)
+        t = ap.inst_type[i0:i1]
+        orow = row_order[prow[i0:i1]].astype(np.int64)        # (ni, 75)
+        for w in range(WARP_PARTS):
+            nodes = orow[:, per * w:per * (w + 1)]            # (ni, 15)
+            g = gid[t[:, None], nodes].astype(np.int64)
+            order = np.argsort(g, axis=1, kind="stable")
+            gs = np.take_along_axis(g, order, axis=1)
+            new = np.ones_like(gs, dtype=bool)
+            new[:, 1:] = gs[:, 1:] != gs[:, :-1]
+            idx = np.broadcast_to(np.arange(per), gs.shape)
+            start = np.maximum.accumulate(np.where(new, idx, 0), axis=1)
+            pos = idx - start
+            tkey = (np.cumsum(new, axis=1) - 1) * 2 + pos // 8
+            newt = np.ones_like(tkey, dtype=bool)
+            newt[:, 1:] = tkey[:, 1:] != tkey[:, :-1]
+            tid = np.cumsum(newt, axis=1) - 1
+            ntile = tid[:, -1] + 1
+            counts[(np.arange(i0, i1)) * WARP_PARTS + w] = ntile
+            arr = np.full((i1 - i0, int(ntile.max()), 16), 0xFF, dtype=np.uint8)
+            arr[:, :, 1] = 0
+            ii, jj = np.nonzero(np.ones_like(gs, dtype=bool))
+            tt = tid[ii, jj]
+            arr[ii, tt, 0] = gs[ii, jj].astype(np.uint8)
+            arr[ii, tt, 2 + pos[ii, jj] % 8] = order[ii, jj].astype(np.uint8)
+            np.add.at(arr[:, :, 1], (ii, tt), 1)
+            pieces.append((i0, w, arr, ntile))
+    tile_off = np.zeros(ap.n_instances * WARP_PARTS + 1, dtype=np.int64)
+    np.cumsum(counts, out=tile_off[1:])
+    tiles = np.empty((int(tile_off[-1]), 16), dtype=np.uint8)
+    for i0, w, arr, ntile in pieces:
+        m = np.arange(arr.shape[1])[None, :] < ntile[:, None]
+        a_idx, k_idx = np.nonzero(m)
+        tiles[tile_off[(i0 + a_idx) * WARP_PARTS + w] + k_idx] = arr[a_idx, k_idx]
+    return row_order, tile_off, tiles
+
+
+def node_tables(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5):
+    """Per type and PARENT node: local coordinates in its child segment
+    (xs, xt, xp) and the radii (r_parent, r_child)."""
+    nn = p_s * p_a * p_a
+    nt = ap.n_types
+    rows = np.arange(nt)[:, None]
+    geom = np.empty((nt, nn, 3))
+    rad = np.empty((nt, nn, 2))
+    for k, arr in enumerate((ap.xs, ap.xt, ap.xp)):
+        geom[rows, ap.scatter, k] = arr
+    rad[rows, ap.scatter, 0] = ap.r_parent
+    rad[rows, ap.scatter, 1] = ap.r_child
+    return geom, rad
+
+
 # ---------------------------------------------------------------------------
 # emission plan (level d boxes -> their cousin points)
 # ---------------------------------------------------------------------------
