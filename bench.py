@@ -165,25 +165,30 @@ class ClockSampler:
 
 def cpu_baseline(disc, mats, y, inputs, budget_s, counts):
     """The oracle (numpy restatement of the reference) on a bounded sample of
-    the same matvec: every k-th box per level (leaf, emission, propagation,
-    neighbour sums), every k-th singular-moment patch group and correction
-    entry; the sample time is scaled by k (density packing and assembly run
-    in full and are negligible)."""
+    the same matvec: the far field of one Morton-contiguous block of level-3
+    subtrees holding 1/k of the modelled far-field work (the multi-GPU
+    partition of k parts, part 0), and every k-th near-field target group /
+    correction entry; the sample time is scaled by k."""
     import oracle
+    from paper_2408_02274_b200.partition import level3_partition
     tree, hier, smap, mom, cp = inputs
     op = oracle.OperatorData(disc, mats, smap, mom, cp.ell_idx, cp.src_idx, tree, hier)
     # the numpy port runs ~1.5 GFLOP/s of the algorithmic count on 16 cores
     k = max(1, int(round(counts["total"] / 1.5e9 / budget_s)))
+    k = min(k, tree.level(3).n_boxes)
+    part = level3_partition(tree, hier, k, disc.n_patches, disc.n_c)[0]
+    ranges = {d: part.levels[d]["box"] for d in part.levels}
     t0 = time.perf_counter()
-    oracle.muller_apply(op, y, stride=k)
+    oracle.muller_apply(op, y, stride=k, box_ranges=ranges)
     wall = time.perf_counter() - t0
     est = wall * k
     cores = os.cpu_count()
     return {"value": 4 * disc.n_points / est, "unit": "unknowns*matvec/s",
             "cores": cores, "kind": "port",
-            "sample": (f"oracle/ (numpy restatement of the reference) on every {k}-th "
-                       f"box of each level, patch group and correction entry; sample "
-                       f"wall {wall:.1f}s x{k} = estimated full matvec {est:.1f}s; "
+            "sample": (f"oracle/ (numpy restatement of the reference): far field of "
+                       f"level-3 subtrees {part.box3} (1/{k} of the modelled work), "
+                       f"every {k}-th near-field box / patch group / correction entry; "
+                       f"sample wall {wall:.1f}s x{k} = estimated full matvec {est:.1f}s; "
                        f"numpy/OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', cores)}")}
 
 

@@ -162,14 +162,23 @@ def far_field(tree, hier, weights, kappas, normals=None, step=1e-6,
     if normals is not None:
         disp = tree.points + step * np.asarray(normals)[tree.perm]
     D = tree.depth
+    # segment-row window per level: only the rows of the processed boxes are
+    # materialised (whole level without box_ranges)
+    win = {}
+    for d in range(3, D + 1):
+        lo, hi = ((0, tree.level(d).n_boxes) if box_ranges is None
+                  else box_ranges[d])
+        win[d] = (int(hier.level(d).seg_off[lo]), int(hier.level(d).seg_off[hi]))
     # --- leaf values (ifgf.py:535-554)
     cl, lvl = hier.level(D), tree.level(D)
-    vals = np.zeros((cl.n_segments, nn, nch, nk), dtype=complex)
+    base = win[D][0]
+    vals = np.zeros((win[D][1] - base, nn, nch, nk), dtype=complex)
     for b in _boxes(box_ranges, D, lvl.n_boxes, box_stride):
-        r0, r1 = cl.seg_off[b], cl.seg_off[b + 1]
+        g0, g1 = cl.seg_off[b], cl.seg_off[b + 1]
+        r0, r1 = g0 - base, g1 - base
         if r1 == r0:
             continue
-        xyz, rt = _nodes(cl, cl.seg_ids[r0:r1], lvl.centers[b])
+        xyz, rt = _nodes(cl, cl.seg_ids[g0:g1], lvl.centers[b])
         x = xyz.reshape(-1, 3)
         src = np.arange(lvl.pt_start[b], lvl.pt_start[b] + lvl.pt_count[b])
         dist = np.linalg.norm(x[:, None, :] - tree.points[src][None], axis=-1)
@@ -179,12 +188,12 @@ def far_field(tree, hier, weights, kappas, normals=None, step=1e-6,
             vals[r0:r1, :, :, k] = (g @ w_t[:, src].T).reshape(r1 - r0, nn, nch)
     for d in range(D, 2, -1):
         cl, lvl = hier.level(d), tree.level(d)
-        coef = _coeffs(vals.reshape(cl.n_segments, nn, -1), ps, pa)
+        coef = _coeffs(vals.reshape(vals.shape[0], nn, -1), ps, pa)
         _emit(tree, hier, d, coef, kap, nch, out, outd, disp, box_stride,
-              box_ranges)
+              box_ranges, win[d][0])
         if d > 3:
             vals = _propagate(tree, hier, d, coef, kap, nch, box_stride,
-                              box_ranges)
+                              box_ranges, win[d][0], win[d - 1])
     out = out.transpose(1, 2, 0)[:, :, tree.iperm]
     if outd is not None:
         outd = outd.transpose(1, 2, 0)[:, :, tree.iperm]
@@ -197,7 +206,7 @@ def _boxes(box_ranges, d, n_boxes, stride):
 
 
 def _emit(tree, hier, d, coef, kap, nch, out, outd, disp, box_stride,
-          box_ranges=None):
+          box_ranges=None, row_base=0):
     """Cousin-point evaluation of level-d interpolants (ifgf.py:630-673)."""
     cfg = hier.config
     cl, lvl = hier.level(d), tree.level(d)
@@ -214,7 +223,7 @@ def _emit(tree, hier, d, coef, kap, nch, out, outd, disp, box_stride,
     ctr = lvl.centers[box]
     s, th, ph, r = _cone(tree.points[tg] - ctr, lvl.side)
     f = _flat(cl, s, th, ph)
-    rows = np.searchsorted(keys, box * stride + f)
+    rows = np.searchsorted(keys, box * stride + f) - row_base
     pts = [(s, th, ph, r, out)]
     if outd is not None:
         pts.append(_cone(disp[tg] - ctr, lvl.side) + (outd,))
@@ -230,7 +239,8 @@ def _emit(tree, hier, d, coef, kap, nch, out, outd, disp, box_stride,
             np.add.at(dst, tg[z], v)
 
 
-def _propagate(tree, hier, d, coef, kap, nch, box_stride, box_ranges=None):
+def _propagate(tree, hier, d, coef, kap, nch, box_stride, box_ranges=None,
+               row_base=0, parent_win=None):
     """Fold level-d interpolants into the level-(d-1) node values
     (ifgf.py:676-785): per (parent segment id, child octant) type, the
     parent nodes in child coordinates, their child segments and the
@@ -242,7 +252,8 @@ def _propagate(tree, hier, d, coef, kap, nch, box_stride, box_ranges=None):
     cl, lvl = hier.level(d), tree.level(d)
     pcl = hier.level(d - 1)
     stride, keys = _row_keys(cl)
-    pvals = np.zeros((pcl.n_segments, nn, nch, nk), dtype=complex)
+    plo, phi = parent_win if parent_win is not None else (0, pcl.n_segments)
+    pvals = np.zeros((phi - plo, nn, nch, nk), dtype=complex)
     flat_c = coef.reshape(coef.shape[0], nn, -1)
     octant = (lvl.codes & np.uint64(7)).astype(np.int64)
     inst = {}
@@ -263,11 +274,11 @@ def _propagate(tree, hier, d, coef, kap, nch, box_stride, box_ranges=None):
         kids = np.array([q[1] for q in lst])
         for sig in np.unique(f):
             nodes = np.nonzero(f == sig)[0]
-            rows = np.searchsorted(keys, kids * stride + sig)
+            rows = np.searchsorted(keys, kids * stride + sig) - row_base
             blk = flat_c[rows]                                   # (inst, nn, C)
             v = np.matmul(bas[nodes].astype(complex), blk).reshape(len(lst), nodes.size, nch, nk)
             v *= ratio[nodes][None, :, None, :]
-            pvals[prow[:, None], nodes[None, :]] += v
+            pvals[prow[:, None] - plo, nodes[None, :]] += v
     return pvals
 
 
@@ -377,7 +388,7 @@ def _corrections(op, phi, kap, stride=1):
     return cs, cd
 
 
-def potentials(op: OperatorData, phi, stride: int = 1):
+def potentials(op: OperatorData, phi, stride: int = 1, box_ranges=None):
     """(S (8,2,N), D (6,2,N)) (operators.py:321-350)."""
     disc = op.disc
     kap = op.materials.kappas
@@ -392,7 +403,9 @@ def potentials(op: OperatorData, phi, stride: int = 1):
         s_near[:, :, grp.targets] += np.einsum("kbmn,cmn->ckb", grp.beta_s, coeffs[:, p])
         d_near[:, :, grp.targets] += np.einsum("kbmn,cmn->ckb", grp.beta_d, coeffs[:, p])
     s_if, s_disp = far_field(op.tree, op.hier, phi * disc.weights, kap,
-                             disc.normals, op.fd_step, box_stride=stride)
+                             disc.normals, op.fd_step,
+                             box_stride=1 if box_ranges is not None else stride,
+                             box_ranges=box_ranges)
     s_nb, d_nb = _neighbor_sums(op, phi, kap, stride)
     s_far = s_if + s_nb
     d_far = (s_disp[:6] - s_if[:6]) / op.fd_step + d_nb
@@ -403,7 +416,7 @@ def potentials(op: OperatorData, phi, stride: int = 1):
     return s_near + s_far, d_near[:6] + d_far
 
 
-def muller_apply(op: OperatorData, y, stride: int = 1):
+def muller_apply(op: OperatorData, y, stride: int = 1, box_ranges=None):
     """y (4N) -> A y (operators.py:399-403 with apply_block :354-397).
 
     stride > 1 runs a bounded CPU-baseline sample (every stride-th box /
@@ -417,7 +430,7 @@ def muller_apply(op: OperatorData, y, stride: int = 1):
     phi = np.empty((8, n), dtype=complex)
     phi[0:3], phi[3:6] = j.T, m.T
     phi[6], phi[7] = _divergence(disc, j), _divergence(disc, m)
-    S, D = potentials(op, phi, stride)
+    S, D = potentials(op, phi, stride, box_ranges)
     G = _grads(disc, S)
     nrm = disc.normals
     kap = mats.kappas
