@@ -12,7 +12,11 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libifgfb200.so"
+import os
+
+# IFGFB_LIB overrides the in-tree library (used to A/B kernel variants)
+LIB_PATH = Path(os.environ.get("IFGFB_LIB") or
+                Path(__file__).resolve().parent / "libifgfb200.so")
 
 KERNEL_KINDS = ("leaf", "propagate", "emit", "emit_reduce", "near",
                 "pack", "assemble", "other")

@@ -264,13 +264,23 @@ __device__ __forceinline__ BasisA make_basis(double xs, double xt, double xp,
 // acc[nt] (+)= sum_i basis_i * C[i][8nt + grp]: 20 k-steps x 4 column tiles
 // of DMMA; the B fragments of a k-step are one coalesced 32-byte load per
 // lane from the fragment-ordered segment.
-template <bool EXACT>
+#ifndef IFGFB_ACC_QUNROLL
+#define IFGFB_ACC_QUNROLL 4
+#endif
+#ifndef IFGFB_ACC_MINB
+#define IFGFB_ACC_MINB 6
+#endif
+#ifndef IFGFB_ACC_ROWS
+#define IFGFB_ACC_ROWS 1
+#endif
+
+template <bool EXACT, int QU = 4>
 __device__ __forceinline__ void basis_times_block(const BasisA& B,
                                                   const double* __restrict__ C,
                                                   int lane, double (&c0)[4],
                                                   double (&c1)[4]) {
   const double4* F = reinterpret_cast<const double4*>(C) + lane;
-#pragma unroll
+#pragma unroll QU
   for (int q = 0; q < 4; ++q) {
 #pragma unroll
     for (int c = 0; c < PA; ++c) {
@@ -310,6 +320,8 @@ struct AccArgs {
   const double* node_geom; const double2* ratio;
   const double* coef_child; double* coef_parent;
   int row0;              // first parent row handled (partition)
+  int row_end;           // one past the last parent row handled
+  int rows_per_cta;      // consecutive parent rows per CTA
 };
 
 // One CTA (5 warps) per parent segment row, owner computes: warp w owns the
@@ -321,20 +333,20 @@ struct AccArgs {
 // 4 column tiles of FP64 DMMA, times the re-centering ratio.  The summed
 // values are transformed to coefficients (K3) and written once.
 template <int NK>
-__global__ void __launch_bounds__(160, 6) accum_kernel(AccArgs a) {
+__global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
   __shared__ double2 acc[WARP_PARTS * PART_NODES * NCOL];   // 19.2 KB
   __shared__ unsigned char ord[NN], inv[NN];
-  const int p = blockIdx.x + a.row0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, tig = lane & 3;
-  if (threadIdx.x < NN) {
-    const unsigned char nd = a.row_order[(size_t)p * NN + threadIdx.x];
-    ord[threadIdx.x] = nd;
-    inv[nd] = (unsigned char)threadIdx.x;
-  }
   double2* mine = acc + warp * PART_NODES * NCOL;
+  const int pbeg = a.row0 + blockIdx.x * a.rows_per_cta;
+  const int pend = min(pbeg + a.rows_per_cta, a.row_end);
+  // consecutive parent rows (mostly of one parent box: shared children)
+  for (int p = pbeg; p < pend; ++p) {
+  if (lane < PART_NODES)         // each warp loads its own part of the order
+    ord[warp * PART_NODES + lane] = a.row_order[(size_t)p * NN + warp * PART_NODES + lane];
   for (int i = lane; i < PART_NODES * NCOL; i += 32) mine[i] = make_double2(0.0, 0.0);
-  __syncthreads();
+  __syncwarp();
   const int i0 = a.inst_off[p], i1 = a.inst_off[p + 1];
   for (int inst = i0; inst < i1; ++inst) {
     const int t = a.inst_type[inst];
@@ -353,7 +365,7 @@ __global__ void __launch_bounds__(160, 6) accum_kernel(AccArgs a) {
       const double* ng = a.node_geom + ((size_t)t * NN + node) * 3;
       const BasisA B = make_basis<false>(ng[0], ng[1], ng[2], tig);
       double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
-      basis_times_block<false>(B, a.coef_child + (size_t)cr[g] * SEG_DOUBLES, lane,
+      basis_times_block<false, IFGFB_ACC_QUNROLL>(B, a.coef_child + (size_t)cr[g] * SEG_DOUBLES, lane,
                                c0, c1);
       if (valid) {
         const double2* rt = a.ratio + ((size_t)t * NN + node) * NK;
@@ -373,9 +385,13 @@ __global__ void __launch_bounds__(160, 6) accum_kernel(AccArgs a) {
     }
   }
   __syncthreads();
+  if (threadIdx.x < NN) inv[ord[threadIdx.x]] = (unsigned char)threadIdx.x;
+  __syncthreads();
   to_coeffs_smem<true>(acc, inv, threadIdx.x, 32 * WARP_PARTS);
   store_segment<true>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, inv, threadIdx.x,
                       32 * WARP_PARTS);
+  __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------- K5 ----
@@ -539,7 +555,11 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
                      p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
                      p.coef[cur ^ 1] - (size_t)U.seg_lo() * SEG_DOUBLES, U.seg_lo()};
           tk = p.timer.begin(K_ACCUM, st);
-          accum_kernel<NK><<<U.seg_hi() - U.seg_lo(), 32 * WARP_PARTS, 0, st>>>(aa);
+          aa.row_end = U.seg_hi();
+          aa.rows_per_cta = IFGFB_ACC_ROWS;
+          const int nrows = U.seg_hi() - U.seg_lo();
+          accum_kernel<NK><<<(nrows + IFGFB_ACC_ROWS - 1) / IFGFB_ACC_ROWS, 32 * WARP_PARTS,
+                             0, st>>>(aa);
           p.timer.end(tk, st);
           launches += 2;
         }

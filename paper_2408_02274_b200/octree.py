@@ -740,16 +740,33 @@ def _local_group_ids(ap: AccumulationPlan, nn: int) -> np.ndarray:
     return gid
 
 
+def _warp_set_tiles(gid, t, orow, w, per):
+    """Tiles of warp w for a block of instances: (tile id per element,
+    tiles per instance, sorted groups, slots, position in run)."""
+    nodes = orow[:, per * w:per * (w + 1)]                   # (ni, per)
+    g = gid[t[:, None], nodes]                              # (ni, per) int16
+    order = np.argsort(g, axis=1, kind="stable")
+    gs = np.take_along_axis(g, order, axis=1)
+    new = np.ones(gs.shape, dtype=bool)
+    new[:, 1:] = gs[:, 1:] != gs[:, :-1]
+    idx = np.broadcast_to(np.arange(per, dtype=np.int16), gs.shape)
+    start = np.maximum.accumulate(np.where(new, idx, 0), axis=1)
+    pos = idx - start                                       # position in run
+    newt = new | (pos % 8 == 0)
+    tid = np.cumsum(newt, axis=1, dtype=np.int32) - 1       # tile per element
+    return tid, tid[:, -1] + 1, gs, order, pos
+
+
 def row_tiles(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5,
-              chunk: int = 1 << 18):
+              chunk: int = 1 << 17):
     """Per parent row partition of its 75 nodes into 5 warp-owned sets of 15
     and the MMA row tiles of every (instance, warp).
 
     Nodes are sorted by their child-segment signature over the row's
     instances (the sigma group of the node under each child), so nodes that
     share child segments under every child land in the same warp set and
-    its row tiles fill up (11.1-12.5 tiles per instance
-    against 12.2-13.9 for a fixed theta-index split, lower bound 10.5-10.9).
+    its row tiles fill up (11.1-12.7 tiles per instance against 12.2-13.9
+    for a fixed theta-index split; lower bound 10.5-10.9).
 
     Returns
       row_order (n_rows, 75) uint8  node at set position (warp w owns
@@ -774,45 +791,40 @@ def row_tiles(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5,
         key[rows] |= gid[t].astype(np.int64) << (4 * (7 - i))
         key[~has] |= np.int64(0xF) << (4 * (7 - i))
     row_order = np.argsort(key, axis=1, kind="stable").astype(np.uint8)
-    # per instance and warp: the set's nodes grouped by the type's sigma group
+    del key
     prow = np.repeat(np.arange(n_rows), cnt)
-    counts = np.zeros(ap.n_instances * WARP_PARTS, dtype=np.int64)
-    pieces = []
-    for i0 in range(0, ap.n_instances, chunk):
-        i1 = min(ap.n_instances, i0 + chunk)
+    ni_all = ap.n_instances
+    blocks = [(i0, min(ni_all, i0 + chunk)) for i0 in range(0, ni_all, chunk)]
+    counts = np.zeros((ni_all, WARP_PARTS), dtype=np.int64)
+
+    def count(blk):                       # pass 1: tiles per (instance, warp)
+        i0, i1 = blk
         t = ap.inst_type[i0:i1]
-        orow = row_order[prow[i0:i1]].astype(np.int64)        # (ni, 75)
+        orow = row_order[prow[i0:i1]]
         for w in range(WARP_PARTS):
-            nodes = orow[:, per * w:per * (w + 1)]            # (ni, 15)
-            g = gid[t[:, None], nodes].astype(np.int64)
-            order = np.argsort(g, axis=1, kind="stable")
-            gs = np.take_along_axis(g, order, axis=1)
-            new = np.ones_like(gs, dtype=bool)
-            new[:, 1:] = gs[:, 1:] != gs[:, :-1]
-            idx = np.broadcast_to(np.arange(per), gs.shape)
-            start = np.maximum.accumulate(np.where(new, idx, 0), axis=1)
-            pos = idx - start
-            tkey = (np.cumsum(new, axis=1) - 1) * 2 + pos // 8
-            newt = np.ones_like(tkey, dtype=bool)
-            newt[:, 1:] = tkey[:, 1:] != tkey[:, :-1]
-            tid = np.cumsum(newt, axis=1) - 1
-            ntile = tid[:, -1] + 1
-            counts[(np.arange(i0, i1)) * WARP_PARTS + w] = ntile
-            arr = np.full((i1 - i0, int(ntile.max()), 16), 0xFF, dtype=np.uint8)
-            arr[:, :, 1] = 0
-            ii, jj = np.nonzero(np.ones_like(gs, dtype=bool))
-            tt = tid[ii, jj]
-            arr[ii, tt, 0] = gs[ii, jj].astype(np.uint8)
-            arr[ii, tt, 2 + pos[ii, jj] % 8] = order[ii, jj].astype(np.uint8)
-            np.add.at(arr[:, :, 1], (ii, tt), 1)
-            pieces.append((i0, w, arr, ntile))
-    tile_off = np.zeros(ap.n_instances * WARP_PARTS + 1, dtype=np.int64)
-    np.cumsum(counts, out=tile_off[1:])
-    tiles = np.empty((int(tile_off[-1]), 16), dtype=np.uint8)
-    for i0, w, arr, ntile in pieces:
-        m = np.arange(arr.shape[1])[None, :] < ntile[:, None]
-        a_idx, k_idx = np.nonzero(m)
-        tiles[tile_off[(i0 + a_idx) * WARP_PARTS + w] + k_idx] = arr[a_idx, k_idx]
+            counts[i0:i1, w] = _warp_set_tiles(gid, t, orow, w, per)[1]
+
+    list(_pool().map(count, blocks))
+    tile_off = np.zeros(ni_all * WARP_PARTS + 1, dtype=np.int64)
+    np.cumsum(counts.ravel(), out=tile_off[1:])
+    tiles = np.full((int(tile_off[-1]), 16), 0xFF, dtype=np.uint8)
+
+    def fill(blk):                        # pass 2: disjoint records per block
+        i0, i1 = blk
+        t = ap.inst_type[i0:i1]
+        orow = row_order[prow[i0:i1]]
+        for w in range(WARP_PARTS):
+            tid, ntile, gs, order, pos = _warp_set_tiles(gid, t, orow, w, per)
+            base = tile_off[np.arange(i0, i1) * WARP_PARTS + w]
+            gidx = (base[:, None] + tid).ravel()
+            tiles[gidx, 0] = gs.ravel().astype(np.uint8)
+            tiles[gidx, 2 + (pos.ravel() % 8)] = order.ravel().astype(np.uint8)
+            lo = int(gidx.min())
+            rows_per = np.bincount(gidx - lo)
+            nz = np.nonzero(rows_per)[0]
+            tiles[lo + nz, 1] = rows_per[nz].astype(np.uint8)
+
+    list(_pool().map(fill, blocks))
     return row_order, tile_off, tiles
 
 

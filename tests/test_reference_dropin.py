@@ -42,7 +42,7 @@ def test_accumulation_and_emission_plans_from_reference_objects(ref_op):
                   "xs", "xt", "xp", "r_parent", "r_child", "inst_off", "inst_type",
                   "inst_child", "inst_crow_off", "crow"):
             assert np.array_equal(getattr(a, f), getattr(b, f)), (d, f)
-        for x, y in zip(octree.warp_tiles(a), octree.warp_tiles(b)):
+        for x, y in zip(octree.row_tiles(a), octree.row_tiles(b)):
             assert np.array_equal(x, y)
     for d in range(3, ref_op.tree.depth + 1):
         a = octree.emission_plan(ref_op.tree, ref_op.hierarchy, d, disp_r)
