@@ -257,6 +257,14 @@ typedef struct {
 } ifgfb_partition_desc;
 
 int ifgfb_plan_set_partition(ifgfb_plan* plan, const ifgfb_partition_desc* part);
+/* Single-GPU streaming: run the upward pass as n_parts sequential passes,
+ * one per group of Morton-contiguous level-3 subtrees (same descriptor as a
+ * rank's partition; target ranges ignored), accumulating the far field.
+ * The coefficient buffers shrink to the largest part, so levels larger than
+ * half the HBM fit (e.g. cfg 2 at n_refine = 24 on one B200).  Exclusive
+ * with ifgfb_plan_set_partition. */
+int ifgfb_plan_set_streaming(ifgfb_plan* plan, const ifgfb_partition_desc* parts,
+                             int n_parts);
 /* density packing (all points) + far field of the owned subtrees */
 int ifgfb_muller_far_phase(ifgfb_plan* plan, const double* y, void* stream);
 /* near field + assembly of the owned targets; rows outside are untouched */

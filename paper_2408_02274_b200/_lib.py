@@ -125,6 +125,8 @@ EXPORTS = {
                              C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_plan_set_partition": ([C.c_void_p, C.POINTER(PartitionDesc)],
                                  C.c_int),
+    "ifgfb_plan_set_streaming": ([C.c_void_p, C.POINTER(PartitionDesc),
+                                  C.c_int], C.c_int),
     "ifgfb_muller_far_phase": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_muller_near_phase": ([C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p], C.c_int),

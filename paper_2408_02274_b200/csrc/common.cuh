@@ -191,6 +191,10 @@ struct Level {
   int pair_hi() const { return part_pair_hi < 0 ? (int)n_pairs : part_pair_hi; }
 };
 
+struct StreamRange {
+  int seg_lo = 0, seg_hi = 0, pair_lo = 0, pair_hi = 0, tile_lo = 0, tile_hi = 0;
+};
+
 struct Plan {
   int device = 0;
   int n = 0, depth = 0;
@@ -235,6 +239,9 @@ struct Plan {
   int64_t launches = 0;
   KTimer timer;
   bool partitioned = false;
+  // streaming: per part, per level (index d) the ranges of one group of
+  // level-3 subtrees; empty = single pass
+  std::vector<std::vector<StreamRange>> stream_parts;
   int part_t_lo = 0, part_t_hi = -1;         // owned targets (original order)
   int t_lo() const { return part_t_lo; }
   int t_hi() const { return part_t_hi < 0 ? n : part_t_hi; }

@@ -489,9 +489,26 @@ __global__ void unpermute(int n, int ncols, const int* __restrict__ perm,
 }
 
 // ------------------------------------------------------------ driver -----
+// Streaming: make part `part` the active per-level row / pair / tile ranges.
+static void apply_stream_part(Plan& p, int part) {
+  for (int d = 3; d <= p.depth; ++d) {
+    const StreamRange& r = p.stream_parts[part][d];
+    Level& L = p.levels[d];
+    L.part_seg_lo = r.seg_lo;
+    L.part_seg_hi = r.seg_hi;
+    L.part_pair_lo = r.pair_lo;
+    L.part_pair_hi = r.pair_hi;
+    L.part_tile_lo = r.tile_lo;
+    L.part_tile_hi = r.tile_hi;
+  }
+}
+
+int ensure_coef(Plan& p);
+
 template <int NK>
 static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
                        double* out, double* out_disp, cudaStream_t st) {
+  if (p.coef_cap == 0) IFGFB_RC(ensure_coef(p));
   constexpr int CH = NCOL / NK;
   const int n = p.n;
   const int threads = 256;
@@ -507,63 +524,76 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
   double ki[2] = {kap[1], NK > 1 ? kap[3] : 0.0};
   const int D = p.depth;
   if (D >= 3) {
-    int cur = 0;
-    {
-      Level& L = p.levels[D];
-      LeafArgs la{L.seg_box, L.seg_id, L.centers, L.pt_start, L.pt_count, L.tabs,
-                  L.n_s, L.n_a, L.h, p.points_tree,
-                  reinterpret_cast<const double2*>(p.wt), {kr[0], kr[1]},
-                  {ki[0], ki[1]}, p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
-                  L.seg_lo()};
-      if (L.seg_hi() > L.seg_lo()) {
-        const int tk = p.timer.begin(K_LEAF, st);
-        leaf_kernel<NK><<<L.seg_hi() - L.seg_lo(), 128, 0, st>>>(la);
-        p.timer.end(tk, st);
-        ++launches;
-      }
-    }
-    for (int d = D; d >= 3; --d) {
+    // re-centering ratios, once per apply and level (kappa dependent)
+    for (int d = 4; d <= D; ++d) {
       Level& L = p.levels[d];
-      if (L.tile_hi() > L.tile_lo()) {
-        EmitArgs ea{L.etiles, L.tile_lo(), L.tile_hi(), L.pair_id, L.geom,
-                    out_disp ? L.geom_disp : nullptr,
-                    p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
-                    {kr[0], kr[1]}, {ki[0], ki[1]},
-                    reinterpret_cast<double2*>(p.partial)};
-        int tk = p.timer.begin(K_EMIT, st);
-        emit_kernel<NK><<<(L.tile_hi() - L.tile_lo() + 3) / 4, 128, 0, st>>>(ea);
-        p.timer.end(tk, st);
-        tk = p.timer.begin(K_REDUCE, st);
-        emit_reduce<<<(n * NCOL + threads - 1) / threads, threads, 0, st>>>(
-            n, L.pair_lo(), L.pair_hi(), L.tgt_off, L.tgt_pairs, reinterpret_cast<const double2*>(p.partial),
-            reinterpret_cast<double2*>(p.out_tree),
-            out_disp ? reinterpret_cast<double2*>(p.out_disp_tree) : nullptr);
-        p.timer.end(tk, st);
-        launches += 2;
-      }
-      if (d > 3 && L.has_accum) {
-        Level& U = p.levels[d - 1];
-        if (U.seg_hi() > U.seg_lo()) {
-          const int64_t nr = L.n_types * NN;
-          int tk = p.timer.begin(K_OTHER, st);
-          ratio_kernel<NK><<<(unsigned)((nr + 255) / 256), 256, 0, st>>>(
-              nr, L.node_r, kr[0], ki[0], kr[1], ki[1],
-              reinterpret_cast<double2*>(L.ratio));
+      if (!L.has_accum) continue;
+      const int64_t nr = L.n_types * NN;
+      const int tk = p.timer.begin(K_OTHER, st);
+      ratio_kernel<NK><<<(unsigned)((nr + 255) / 256), 256, 0, st>>>(
+          nr, L.node_r, kr[0], ki[0], kr[1], ki[1], reinterpret_cast<double2*>(L.ratio));
+      p.timer.end(tk, st);
+      ++launches;
+    }
+    // one pass over the owned subtrees, or (streaming) one pass per group of
+    // Morton-contiguous level-3 subtrees, accumulating into out_tree
+    const int n_parts = p.stream_parts.empty() ? 1 : (int)p.stream_parts.size();
+    for (int part = 0; part < n_parts; ++part) {
+      if (!p.stream_parts.empty()) apply_stream_part(p, part);
+      int cur = 0;
+      {
+        Level& L = p.levels[D];
+        LeafArgs la{L.seg_box, L.seg_id, L.centers, L.pt_start, L.pt_count, L.tabs,
+                    L.n_s, L.n_a, L.h, p.points_tree,
+                    reinterpret_cast<const double2*>(p.wt), {kr[0], kr[1]},
+                    {ki[0], ki[1]}, p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
+                    L.seg_lo()};
+        if (L.seg_hi() > L.seg_lo()) {
+          const int tk = p.timer.begin(K_LEAF, st);
+          leaf_kernel<NK><<<L.seg_hi() - L.seg_lo(), 128, 0, st>>>(la);
           p.timer.end(tk, st);
-          AccArgs aa{L.inst_off, L.inst_type, L.inst_crow_off, L.crow, L.tile_off,
-                     L.tiles, L.row_order, L.node_geom, reinterpret_cast<const double2*>(L.ratio),
-                     p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
-                     p.coef[cur ^ 1] - (size_t)U.seg_lo() * SEG_DOUBLES, U.seg_lo()};
-          tk = p.timer.begin(K_ACCUM, st);
-          aa.row_end = U.seg_hi();
-          aa.rows_per_cta = IFGFB_ACC_ROWS;
-          const int nrows = U.seg_hi() - U.seg_lo();
-          accum_kernel<NK><<<(nrows + IFGFB_ACC_ROWS - 1) / IFGFB_ACC_ROWS, 32 * WARP_PARTS,
-                             0, st>>>(aa);
+          ++launches;
+        }
+      }
+      for (int d = D; d >= 3; --d) {
+        Level& L = p.levels[d];
+        if (L.tile_hi() > L.tile_lo()) {
+          EmitArgs ea{L.etiles, L.tile_lo(), L.tile_hi(), L.pair_id, L.geom,
+                      out_disp ? L.geom_disp : nullptr,
+                      p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
+                      {kr[0], kr[1]}, {ki[0], ki[1]},
+                      reinterpret_cast<double2*>(p.partial)};
+          int tk = p.timer.begin(K_EMIT, st);
+          emit_kernel<NK><<<(L.tile_hi() - L.tile_lo() + 3) / 4, 128, 0, st>>>(ea);
+          p.timer.end(tk, st);
+          tk = p.timer.begin(K_REDUCE, st);
+          emit_reduce<<<(n * NCOL + threads - 1) / threads, threads, 0, st>>>(
+              n, L.pair_lo(), L.pair_hi(), L.tgt_off, L.tgt_pairs,
+              reinterpret_cast<const double2*>(p.partial),
+              reinterpret_cast<double2*>(p.out_tree),
+              out_disp ? reinterpret_cast<double2*>(p.out_disp_tree) : nullptr);
           p.timer.end(tk, st);
           launches += 2;
         }
-        cur ^= 1;
+        if (d > 3 && L.has_accum) {
+          Level& U = p.levels[d - 1];
+          if (U.seg_hi() > U.seg_lo()) {
+            AccArgs aa{L.inst_off, L.inst_type, L.inst_crow_off, L.crow, L.tile_off,
+                       L.tiles, L.row_order, L.node_geom,
+                       reinterpret_cast<const double2*>(L.ratio),
+                       p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
+                       p.coef[cur ^ 1] - (size_t)U.seg_lo() * SEG_DOUBLES, U.seg_lo()};
+            aa.row_end = U.seg_hi();
+            aa.rows_per_cta = IFGFB_ACC_ROWS;
+            const int nrows = U.seg_hi() - U.seg_lo();
+            const int tk = p.timer.begin(K_ACCUM, st);
+            accum_kernel<NK><<<(nrows + IFGFB_ACC_ROWS - 1) / IFGFB_ACC_ROWS,
+                               32 * WARP_PARTS, 0, st>>>(aa);
+            p.timer.end(tk, st);
+            ++launches;
+          }
+          cur ^= 1;
+        }
       }
     }
   }

@@ -32,6 +32,37 @@ static bool to_i32(const int64_t* src, size_t n, std::vector<int>& out,
 #define CHECK_ARG IFGFB_CHECK_ARG
 #define RC IFGFB_RC
 
+// (re)size the two coefficient ping-pong buffers to exactly `need` segments
+static int resize_coef(Plan& p, size_t need) {
+  if (need == p.coef_cap) return IFGFB_OK;
+  for (int i = 0; i < 2; ++i) {
+    if (p.coef[i]) {
+      auto it = std::find(p.allocations.begin(), p.allocations.end(), (void*)p.coef[i]);
+      if (it != p.allocations.end()) p.allocations.erase(it);
+      IFGFB_CUDA(cudaFree(p.coef[i]));
+      p.bytes -= p.coef_cap * SEG_DOUBLES * sizeof(double);
+      p.coef[i] = nullptr;
+    }
+  }
+  for (int i = 0; i < 2; ++i) IFGFB_RC(dev_alloc(p, &p.coef[i], need * SEG_DOUBLES));
+  p.coef_cap = need;
+  return IFGFB_OK;
+}
+
+// size of the coefficient buffers the current mode needs
+int ensure_coef(Plan& p) {
+  size_t need = 1;
+  if (!p.stream_parts.empty()) {
+    for (const auto& part : p.stream_parts)
+      for (int d = 3; d <= p.depth; ++d)
+        need = std::max(need, (size_t)(part[d].seg_hi - part[d].seg_lo));
+  } else {
+    for (int d = 3; d <= p.depth; ++d)
+      need = std::max(need, (size_t)(p.levels[d].seg_hi() - p.levels[d].seg_lo()));
+  }
+  return resize_coef(p, need);
+}
+
 }  // namespace ifgfb
 
 using namespace ifgfb;
@@ -244,8 +275,9 @@ int ifgfb_plan_finalize(ifgfb_plan* h) {
   }
   const size_t n = p.n;
   RC(dev_alloc(p, &p.wt, n * NCOL * 2));
-  p.coef_cap = std::max(p.max_seg, 1);
-  for (int i = 0; i < 2; ++i) RC(dev_alloc(p, &p.coef[i], p.coef_cap * SEG_DOUBLES));
+  // coefficient ping-pong buffers are sized on first use (ensure_coef):
+  // full levels, a rank's owned rows, or the largest streaming part
+  p.coef_cap = 0;
   RC(dev_alloc(p, &p.partial, std::max<int64_t>(p.max_pairs, 1) * 2 * NCOL * 2));
   RC(dev_alloc(p, &p.out_tree, n * NCOL * 2));
   RC(dev_alloc(p, &p.out_disp_tree, n * NCOL * 2));
@@ -253,10 +285,48 @@ int ifgfb_plan_finalize(ifgfb_plan* h) {
   return IFGFB_OK;
 }
 
+int ifgfb_plan_set_streaming(ifgfb_plan* h, const ifgfb_partition_desc* parts,
+                             int n_parts) {
+  CHECK_ARG(h && parts && n_parts >= 1, "bad argument");
+  Plan& p = h->p;
+  CHECK_ARG(p.finalized, "finalize the plan before setting streaming");
+  CHECK_ARG(!p.partitioned, "streaming and a multi-GPU partition are exclusive");
+  std::vector<std::vector<StreamRange>> sp(n_parts, std::vector<StreamRange>(p.depth + 1));
+  size_t need = 1;
+  for (int q = 0; q < n_parts; ++q) {
+    const ifgfb_partition_desc& d = parts[q];
+    CHECK_ARG(d.n_levels == std::max(0, p.depth - 2), "need one entry per level 3..depth");
+    for (int i = 0; i < d.n_levels; ++i) {
+      const ifgfb_level_part& lp = d.levels[i];
+      CHECK_ARG(lp.level >= 3 && lp.level <= p.depth, "stream level out of range");
+      Level& L = p.levels[lp.level];
+      CHECK_ARG(0 <= lp.seg_lo && lp.seg_lo <= lp.seg_hi && lp.seg_hi <= L.n_seg,
+                "segment range out of bounds");
+      CHECK_ARG(0 <= lp.pair_lo && lp.pair_lo <= lp.pair_hi && lp.pair_hi <= L.n_pairs,
+                "pair range out of bounds");
+      StreamRange& r = sp[q][lp.level];
+      r.seg_lo = (int)lp.seg_lo;
+      r.seg_hi = (int)lp.seg_hi;
+      r.pair_lo = (int)lp.pair_lo;
+      r.pair_hi = (int)lp.pair_hi;
+      r.tile_lo = (int)(std::lower_bound(L.etile_rows.begin(), L.etile_rows.end(),
+                                         (int)lp.seg_lo) - L.etile_rows.begin());
+      r.tile_hi = (int)(std::lower_bound(L.etile_rows.begin(), L.etile_rows.end(),
+                                         (int)lp.seg_hi) - L.etile_rows.begin());
+      need = std::max(need, (size_t)(lp.seg_hi - lp.seg_lo));
+    }
+  }
+  p.stream_parts.swap(sp);
+  (void)need;
+  RC(ensure_coef(p));
+  return IFGFB_OK;
+}
+
 int ifgfb_plan_set_partition(ifgfb_plan* h, const ifgfb_partition_desc* d) {
   CHECK_ARG(h && d, "null argument");
   Plan& p = h->p;
   CHECK_ARG(p.finalized, "finalize the plan before setting a partition");
+  CHECK_ARG(p.stream_parts.empty(), "streaming and a multi-GPU partition are exclusive");
   CHECK_ARG(d->n_levels == std::max(0, p.depth - 2), "need one entry per level 3..depth");
   for (int i = 0; i < d->n_levels; ++i) {
     const ifgfb_level_part& lp = d->levels[i];
@@ -284,20 +354,7 @@ int ifgfb_plan_set_partition(ifgfb_plan* h, const ifgfb_partition_desc* d) {
   p.part_t_lo = (int)d->target_lo;
   p.part_t_hi = (int)d->target_hi;
   p.partitioned = true;
-  // coefficient buffers only need the owned rows of any level
-  size_t need = 1;
-  for (int dd = 3; dd <= p.depth; ++dd)
-    need = std::max(need, (size_t)(p.levels[dd].seg_hi() - p.levels[dd].seg_lo()));
-  if (need < p.coef_cap) {
-    for (int i = 0; i < 2; ++i) {
-      auto it = std::find(p.allocations.begin(), p.allocations.end(), (void*)p.coef[i]);
-      if (it != p.allocations.end()) p.allocations.erase(it);
-      IFGFB_CUDA(cudaFree(p.coef[i]));
-      p.bytes -= p.coef_cap * SEG_DOUBLES * sizeof(double);
-      RC(dev_alloc(p, &p.coef[i], need * SEG_DOUBLES));
-    }
-    p.coef_cap = need;
-  }
+  RC(ensure_coef(p));   // coefficient buffers: owned rows only
   return IFGFB_OK;
 }
 

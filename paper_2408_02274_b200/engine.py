@@ -70,6 +70,7 @@ class FarFieldPlan:
                 _lib.check(lib.ifgfb_plan_set_near(self._h, near),
                            "ifgfb_plan_set_near")
             _lib.check(lib.ifgfb_plan_finalize(self._h), "ifgfb_plan_finalize")
+            self.stream_parts = 1
         except Exception:
             lib.ifgfb_plan_destroy(self._h)
             self._h = None
@@ -151,6 +152,43 @@ class FarFieldPlan:
     @property
     def handle(self):
         return self._h
+
+    def coefficient_bytes_full(self) -> int:
+        """Bytes of the two coefficient buffers without streaming."""
+        mx = max((self.hier.level(d).n_segments
+                  for d in range(3, self.depth + 1)), default=0)
+        return 2 * mx * 2560 * 8
+
+    def set_streaming(self, n_parts: int) -> None:
+        """Run the upward pass as n_parts sequential passes over Morton
+        groups of level-3 subtrees (ifgfb_plan_set_streaming)."""
+        from .partition import level3_partition
+        n_parts = max(1, min(int(n_parts), self.tree.level(3).n_boxes))
+        parts = level3_partition(self.tree, self.hier, n_parts, n_parts, 1)
+        depth = self.depth
+        keep, descs = [], (_lib.PartitionDesc * n_parts)()
+        for q, part in enumerate(parts):
+            lv = (_lib.LevelPart * (depth - 2))()
+            for i, d in enumerate(range(3, depth + 1)):
+                L = part.levels[d]
+                lv[i] = _lib.LevelPart(d, L["seg"][0], L["seg"][1],
+                                       L["pair"][0], L["pair"][1])
+            keep.append(lv)
+            descs[q] = _lib.PartitionDesc(depth - 2, lv, 0, 0)
+        _lib.check(_lib.load().ifgfb_plan_set_streaming(self._h, descs, n_parts),
+                   "ifgfb_plan_set_streaming")
+        self.stream_parts = n_parts
+
+    def auto_stream(self, fraction: float = 0.45) -> int:
+        """Stream when two full coefficient levels exceed `fraction` of the
+        free device memory; returns the number of parts (1 = no streaming)."""
+        free, _ = torch.cuda.mem_get_info()
+        need = self.coefficient_bytes_full()
+        if self.depth < 3 or need <= fraction * free:
+            return 1
+        n = int(np.ceil(need / (fraction * free))) + 1
+        self.set_streaming(n)
+        return n
 
     def device_bytes(self) -> int:
         return int(_lib.load().ifgfb_plan_device_bytes(self._h))

@@ -236,7 +236,7 @@ class MullerOperator:
 
     def __init__(self, disc, materials, smap, moments, corrections,
                  config: OperatorConfig = OperatorConfig(), tree=None,
-                 hierarchy=None):
+                 hierarchy=None, stream_parts=None):
         self.disc = disc
         self.materials = materials
         self.smap = smap
@@ -255,6 +255,12 @@ class MullerOperator:
         self.plan = FarFieldPlan(tree, hierarchy, disc.normals,
                                  config.fd_step, surface=surf, near=near,
                                  kappas=materials.kappas)
+        # memory: stream the upward pass over groups of level-3 subtrees when
+        # two full coefficient levels do not fit (None = automatic)
+        if stream_parts is None:
+            self.plan.auto_stream()
+        elif stream_parts > 1:
+            self.plan.set_streaming(stream_parts)
         del keep
         self._dev = torch.device("cuda")
 

@@ -77,3 +77,20 @@ def test_one_rank_partition_is_identity():
     y = torch.from_numpy(z["y"]).cuda()
     got = ops[0].apply_device(y).cpu().numpy()
     assert np.array_equal(got, ops[0].op.apply(z["y"]))
+
+
+@pytest.mark.parametrize("name,n_parts", [("s1", 3), ("c1", 4)])
+def test_streaming_equals_single_pass(name, n_parts):
+    """Single-GPU streaming (sequential level-3 subtree groups, smaller
+    coefficient buffers) gives the single-pass result."""
+    inp, z = inputs(name), golden(name)
+    args = (inp["disc"], inp["mats"], inp["smap"], inp["moments"],
+            (inp["corr"].ell_idx, inp["corr"].src_idx))
+    full = MullerOperator(*args, tree=inp["tree"], hierarchy=inp["hier"], stream_parts=1)
+    st = MullerOperator(*args, tree=inp["tree"], hierarchy=inp["hier"],
+                        stream_parts=n_parts)
+    a, b = full.apply(z["y"]), st.apply(z["y"])
+    assert rel(b, a) < 1e-10
+    assert st.plan.device_bytes() < full.plan.device_bytes()
+    if plan_matches_golden(name):
+        assert rel(b, z["apply_y"]) < 1e-10
