@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--n-refine", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
+    ap.add_argument("--max-rss-gb", type=float, default=0.0,
+                    help="abort (kill this process) if host RSS exceeds this")
     ap.add_argument("--force-partition", action="store_true",
                     help="use the partitioned (multi-GPU) operator even at N=1")
     return ap.parse_args()
@@ -399,8 +401,32 @@ def gmres_cfg1():
             rep.iterations, "final_residual": rep.residuals[-1], "solve_s": rep.wall_time}
 
 
+def rss_watchdog(limit_gb: float):
+    """Kill this process (only) before the host runs out of memory."""
+    import threading
+
+    def watch():
+        while True:
+            try:
+                with open(f"/proc/{os.getpid()}/status") as fh:
+                    for line in fh:
+                        if line.startswith("VmRSS:"):
+                            kb = int(line.split()[1])
+                            if kb > limit_gb * 1024 * 1024:
+                                sys.stderr.write(f"RSS {kb / 1e6:.1f} GB > limit, abort\n")
+                                sys.stderr.flush()
+                                os.kill(os.getpid(), 9)
+            except Exception:
+                pass
+            time.sleep(0.5)
+
+    threading.Thread(target=watch, daemon=True).start()
+
+
 def main():
     args = parse()
+    if args.max_rss_gb > 0:
+        rss_watchdog(args.max_rss_gb)
     if args.impl == "reference":
         run_reference(args)
     else:
