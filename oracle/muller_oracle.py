@@ -117,12 +117,17 @@ def _row_keys(cl):
 
 def _coeffs(vals, ps, pa):
     """Node values (nseg, ps*pa*pa, C) -> tensor Chebyshev coefficients
-    (ifgf.py:502-522)."""
+    (ifgf.py:502-522): one real matrix per axis applied to the interleaved
+    real view of the complex data."""
     n, _, c = vals.shape
-    v = vals.reshape(n, ps, pa, pa, c)
-    v = np.einsum("ia,nabcx->nibcx", _fwd(ps), v)
-    v = np.einsum("jb,nabcx->najcx", _fwd(pa), v)
-    v = np.einsum("kc,nabcx->nabkx", _fwd(pa), v)
+
+    def axis(mat, arr, left, m, right):
+        a = np.ascontiguousarray(arr).reshape(left, m, right).view(np.float64)
+        return np.matmul(mat[None], a).view(complex)
+
+    v = axis(_fwd(ps), vals, n, ps, pa * pa * c)
+    v = axis(_fwd(pa), v, n * ps, pa, pa * c)
+    v = axis(_fwd(pa), v, n * ps * pa, pa, c)
     return v.reshape(n, ps * pa * pa, c)
 
 
@@ -234,7 +239,10 @@ def _emit(tree, hier, d, coef, kap, nch, out, outd, disp, box_stride,
         for a in range(0, tg.size, chunk):
             z = slice(a, min(tg.size, a + chunk))
             bas = _basis(cfg.p_s, cfg.p_a, xs[z], xt[z], xp[z])
-            v = np.matmul(bas[:, None, :].astype(complex), coef[rows[z]])[:, 0].reshape(-1, nch, nk)
+            # real basis against the interleaved real view of the complex
+            # coefficients (the reference's dgemm trick, ifgf.py:594-611)
+            cv = coef[rows[z]].view(np.float64)
+            v = np.matmul(bas[:, None, :], cv)[:, 0].view(complex).reshape(-1, nch, nk)
             v *= fac[z][:, None, :]
             np.add.at(dst, tg[z], v)
 
@@ -275,8 +283,8 @@ def _propagate(tree, hier, d, coef, kap, nch, box_stride, box_ranges=None,
         for sig in np.unique(f):
             nodes = np.nonzero(f == sig)[0]
             rows = np.searchsorted(keys, kids * stride + sig) - row_base
-            blk = flat_c[rows]                                   # (inst, nn, C)
-            v = np.matmul(bas[nodes].astype(complex), blk).reshape(len(lst), nodes.size, nch, nk)
+            blk = flat_c[rows].view(np.float64)                  # (inst, nn, 2C)
+            v = np.matmul(bas[nodes], blk).view(complex).reshape(len(lst), nodes.size, nch, nk)
             v *= ratio[nodes][None, :, None, :]
             pvals[prow[:, None] - plo, nodes[None, :]] += v
     return pvals
