@@ -365,7 +365,12 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
       const double* ng = a.node_geom + ((size_t)t * NN + node) * 3;
       const BasisA B = make_basis<false>(ng[0], ng[1], ng[2], tig);
       double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
-      basis_times_block<false, IFGFB_ACC_QUNROLL>(B, a.coef_child + (size_t)cr[g] * SEG_DOUBLES, lane,
+#ifdef IFGFB_ACC_FAKEB   // diagnostic only: every tile reads the first owned child row
+      const int crow_used = (cr[g] & 0);      // row 0: always an L1 hit
+#else
+      const int crow_used = cr[g];
+#endif
+      basis_times_block<false, IFGFB_ACC_QUNROLL>(B, a.coef_child + (size_t)crow_used * SEG_DOUBLES, lane,
                                c0, c1);
       if (valid) {
         const double2* rt = a.ratio + ((size_t)t * NN + node) * NK;
