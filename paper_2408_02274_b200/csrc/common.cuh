@@ -15,9 +15,11 @@ constexpr int NN = PS * PA * PA;  // 75 nodes per cone segment
 constexpr int NCOL = 16;       // complex columns carried per traversal
 constexpr int NRCOL = 2 * NCOL;   // 32 real columns
 // Coefficients of one segment are stored in DMMA B-fragment order:
-// [ks 0..19][lane 0..31][column tile 0..3] doubles, ks = 5q + c covering the
-// coefficient rows i = (4q + (lane&3))*5 + c (zero when 4q + (lane&3) >= 15),
-// column = 8*tile + (lane>>2) of the 32 real columns (re/im of 16 complex).
+// [ks 0..19][half 0..1][lane 0..31][2] doubles, column tile nt = 2*half + j,
+// ks = 5q + c covering the coefficient rows i = (4q + (lane&3))*5 + c (zero
+// when 4q + (lane&3) >= 15), column = 8*nt + (lane>>2) of the 32 real
+// columns (re/im of 16 complex).  A k-step's fragments are two fully
+// contiguous 512-byte warp loads (16 bytes per lane).
 constexpr int KSTEPS = 20;
 constexpr int SEG_DOUBLES = KSTEPS * 32 * 4;  // 2560 doubles = 20 KB per segment
 constexpr int WARP_PARTS = 5;                 // propagation: node owners per CTA

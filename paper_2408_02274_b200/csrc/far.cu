@@ -123,7 +123,7 @@ __device__ __forceinline__ void store_segment(double* dst, const double2* V,
                                               const unsigned char* inv, int tid,
                                               int nthr) {
   for (int idx = tid; idx < SEG_DOUBLES; idx += nthr) {
-    const int ks = idx >> 7, lane = (idx >> 2) & 31, nt = idx & 3;
+    const int ks = idx >> 7, lane = (idx >> 1) & 31, nt = ((idx >> 5) & 2) | (idx & 1);
     const int q = ks / PA, c = ks - PA * q;
     const int ab = 4 * q + (lane & 3);
     double v = 0.0;
@@ -262,13 +262,13 @@ __device__ __forceinline__ BasisA make_basis(double xs, double xt, double xp,
 }
 
 // acc[nt] (+)= sum_i basis_i * C[i][8nt + grp]: 20 k-steps x 4 column tiles
-// of DMMA; the B fragments of a k-step are one coalesced 32-byte load per
-// lane from the fragment-ordered segment.
+// of DMMA; the B fragments of a k-step are two contiguous 512-byte warp
+// loads from the fragment-ordered segment.
 #ifndef IFGFB_ACC_QUNROLL
 #define IFGFB_ACC_QUNROLL 4
 #endif
 #ifndef IFGFB_ACC_MINB
-#define IFGFB_ACC_MINB 6
+#define IFGFB_ACC_MINB 5
 #endif
 #ifndef IFGFB_ACC_ROWS
 #define IFGFB_ACC_ROWS 1
@@ -279,12 +279,13 @@ __device__ __forceinline__ void basis_times_block(const BasisA& B,
                                                   const double* __restrict__ C,
                                                   int lane, double (&c0)[4],
                                                   double (&c1)[4]) {
-  const double4* F = reinterpret_cast<const double4*>(C) + lane;
+  const double2* F = reinterpret_cast<const double2*>(C) + lane;
 #pragma unroll QU
   for (int q = 0; q < 4; ++q) {
 #pragma unroll
     for (int c = 0; c < PA; ++c) {
-      const double4 b = F[(5 * q + c) * 32];
+      const double2 b01 = F[(5 * q + c) * 64], b23 = F[(5 * q + c) * 64 + 32];
+      const double4 b = make_double4(b01.x, b01.y, b23.x, b23.y);
       const double av = EXACT ? mul_rn(B.tst[q], B.tp[c]) : B.tst[q] * B.tp[c];
       dmma(c0[0], c1[0], av, b.x);
       dmma(c0[1], c1[1], av, b.y);
@@ -324,58 +325,126 @@ struct AccArgs {
   int rows_per_cta;      // consecutive parent rows per CTA
 };
 
+// cp.async (LDGSTS) helpers: global -> shared without a register round trip
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n"
+               :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n"
+               :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n"
+               :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" :: "n"(N));
+}
+
+// Per-warp staging of one (instance, warp): everything the warp's tiles read
+// besides the child coefficients, indexed by the warp-set slot.
+constexpr int MAX_GROUPS = 32;        // child segments per instance (checked at plan time)
+struct __align__(16) WarpStage {
+  uint4 tiles[PART_NODES];            // <= 15 row tiles (one node each at worst)
+  double2 ratio[PART_NODES * 2];      // [slot][kappa]
+  double geom[PART_NODES * 3];        // [slot][xs, xt, xp]
+  int crow[MAX_GROUPS];
+};
+
+// Row (lane group grp) of a K4 row tile: the warp-set slot it owns; rows past
+// the tile's count duplicate slot 0 and are dropped.
+__device__ __forceinline__ int tile_slot(const uint4& tl, int grp, bool& valid) {
+  const int nrows = (tl.x >> 8) & 0xff;
+  const int byte = 2 + grp;
+  const unsigned word = byte < 4 ? tl.x : byte < 8 ? tl.y : tl.z;
+  valid = grp < nrows;
+  return valid ? (int)((word >> (8 * (byte & 3))) & 0xff) : (int)((tl.x >> 16) & 0xff);
+}
+
 // One CTA (5 warps) per parent segment row, owner computes: warp w owns the
-// 15 parent nodes with theta index b == w and keeps their 16-column
-// accumulators in its own shared slice (no atomics, no inter-warp hazards,
-// every warp walks every (parent segment, child) instance -> balanced).
-// Per instance each warp re-interpolates the child's coefficients at its
-// nodes: row tiles of <= 8 nodes sharing a child segment sigma, 20 k-steps x
-// 4 column tiles of FP64 DMMA, times the re-centering ratio.  The summed
-// values are transformed to coefficients (K3) and written once.
+// 15 parent nodes at positions 15w..15w+14 of the row's signature order
+// (octree.row_tiles) and keeps their 16-column accumulators in its own shared
+// slice (no atomics, no inter-warp hazards; every warp walks every (parent
+// segment, child) instance).  Per instance each warp re-interpolates the
+// child's coefficients at its nodes: row tiles of <= 8 nodes sharing a child
+// segment sigma, 20 k-steps x 4 column tiles of FP64 DMMA, times the
+// re-centering ratio.  The instance's tile records, child rows, node
+// geometry and ratios are staged by cp.async one instance ahead, so the
+// only global loads on a tile's critical path are the B fragments.  The
+// summed values are transformed to coefficients (K3) and written once.
 template <int NK>
 __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
   __shared__ double2 acc[WARP_PARTS * PART_NODES * NCOL];   // 19.2 KB
+  __shared__ WarpStage stage[WARP_PARTS][2];                // 12.3 KB
   __shared__ unsigned char ord[NN], inv[NN];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, tig = lane & 3;
   double2* mine = acc + warp * PART_NODES * NCOL;
+  const unsigned char* word = ord + warp * PART_NODES;
   const int pbeg = a.row0 + blockIdx.x * a.rows_per_cta;
   const int pend = min(pbeg + a.rows_per_cta, a.row_end);
-  // consecutive parent rows (mostly of one parent box: shared children)
   for (int p = pbeg; p < pend; ++p) {
   if (lane < PART_NODES)         // each warp loads its own part of the order
     ord[warp * PART_NODES + lane] = a.row_order[(size_t)p * NN + warp * PART_NODES + lane];
   for (int i = lane; i < PART_NODES * NCOL; i += 32) mine[i] = make_double2(0.0, 0.0);
+  // the row's instance scalars, lane j <-> instance i0 + j (<= 8 per row)
+  const int i0 = a.inst_off[p], ni = a.inst_off[p + 1] - i0;
+  int my_t = 0, my_ks = 0, my_ke = 0, my_co = 0;
+  if (lane < ni) {
+    my_t = a.inst_type[i0 + lane];
+    my_ks = a.tile_off[(i0 + lane) * WARP_PARTS + warp];
+    my_ke = a.tile_off[(i0 + lane) * WARP_PARTS + warp + 1];
+  }
+  if (lane <= ni) my_co = a.inst_crow_off[i0 + lane];
   __syncwarp();
-  const int i0 = a.inst_off[p], i1 = a.inst_off[p + 1];
-  for (int inst = i0; inst < i1; ++inst) {
-    const int t = a.inst_type[inst];
-    const int* cr = a.crow + a.inst_crow_off[inst];
-    const int k0 = a.tile_off[inst * WARP_PARTS + warp];
-    const int k1 = a.tile_off[inst * WARP_PARTS + warp + 1];
-    for (int k = k0; k < k1; ++k) {
-      const uint4 tl = a.tiles[k];
-      const int g = tl.x & 0xff, nrows = (tl.x >> 8) & 0xff;
-      const int byte = 2 + grp;                    // slot byte of this row
-      const unsigned word = byte < 4 ? tl.x : byte < 8 ? tl.y : tl.z;
-      const int slot0 = (tl.x >> 16) & 0xff;
-      const bool valid = grp < nrows;
-      const int slot = valid ? (int)((word >> (8 * (byte & 3))) & 0xff) : slot0;
-      const int node = ord[warp * PART_NODES + slot];
-      const double* ng = a.node_geom + ((size_t)t * NN + node) * 3;
+  auto stage_inst = [&](int j, WarpStage& S) {
+    const int t = __shfl_sync(0xffffffffu, my_t, j);
+    const int ks = __shfl_sync(0xffffffffu, my_ks, j);
+    const int ke = __shfl_sync(0xffffffffu, my_ke, j);
+    const int cs = __shfl_sync(0xffffffffu, my_co, j);
+    const int ce = __shfl_sync(0xffffffffu, my_co, j + 1);
+    const size_t tb = (size_t)t * NN;
+    for (int e = lane; e < PART_NODES * 3; e += 32)
+      cp_async8(&S.geom[e], a.node_geom + (tb + word[e / 3]) * 3 + e % 3);
+    if (lane < PART_NODES * NK)
+      cp_async16(&S.ratio[lane], a.ratio + (tb + word[lane / NK]) * NK + lane % NK);
+    if (lane < ke - ks) cp_async16(&S.tiles[lane], a.tiles + ks + lane);
+    if (lane < ce - cs) cp_async4(&S.crow[lane], a.crow + cs + lane);
+    cp_async_commit();
+  };
+  if (ni > 0) stage_inst(0, stage[warp][0]);
+  for (int j = 0; j < ni; ++j) {
+    const WarpStage& S = stage[warp][j & 1];
+    if (j + 1 < ni) {
+      stage_inst(j + 1, stage[warp][(j + 1) & 1]);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    const int ntile = __shfl_sync(0xffffffffu, my_ke - my_ks, j);
+    for (int k = 0; k < ntile; ++k) {
+      const uint4 tl = S.tiles[k];
+      bool valid;
+      const int slot = tile_slot(tl, grp, valid);
+#ifdef IFGFB_ACC_FAKEB   // diagnostic only: every tile reads the first owned child row
+      const int crow_used = S.crow[0] & 0;
+#else
+      const int crow_used = S.crow[tl.x & 0xff];
+#endif
+      const double* ng = S.geom + slot * 3;
       const BasisA B = make_basis<false>(ng[0], ng[1], ng[2], tig);
       double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
-#ifdef IFGFB_ACC_FAKEB   // diagnostic only: every tile reads the first owned child row
-      const int crow_used = (cr[g] & 0);      // row 0: always an L1 hit
-#else
-      const int crow_used = cr[g];
-#endif
-      basis_times_block<false, IFGFB_ACC_QUNROLL>(B, a.coef_child + (size_t)crow_used * SEG_DOUBLES, lane,
-                               c0, c1);
+      basis_times_block<false, IFGFB_ACC_QUNROLL>(
+          B, a.coef_child + (size_t)crow_used * SEG_DOUBLES, lane, c0, c1);
       if (valid) {
-        const double2* rt = a.ratio + ((size_t)t * NN + node) * NK;
-        const double2 r0 = rt[0];
-        const double2 r1 = NK > 1 ? rt[NK - 1] : r0;
+        const double2 r0 = S.ratio[slot * NK];
+        const double2 r1 = NK > 1 ? S.ratio[slot * NK + NK - 1] : r0;
         double2* dst = mine + slot * NCOL;
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {

@@ -255,6 +255,19 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
     CHECK_ARG(a->crow[i] >= 0 && a->crow[i] < L.n_seg, "crow out of range");
   if (!to_i32(a->crow, ncrow, tmp, "crow")) return IFGFB_ERR_ARG;
   RC(dev_upload(p, &L.crow, tmp.data(), tmp.size()));
+  // capacities of the kernel's per-warp staging (far.cu WarpStage)
+  for (int64_t r = 0; r < a->n_parent_rows; ++r)
+    CHECK_ARG(a->inst_off[r + 1] - a->inst_off[r] <= 31, "more than 31 instances per row");
+  for (int64_t i = 0; i < ni; ++i) {
+    const int64_t ng = a->inst_crow_off[i + 1] - a->inst_crow_off[i];
+    CHECK_ARG(ng >= 0 && ng <= 32, "more than 32 child segments in one instance");
+    for (int w = 0; w < WARP_PARTS; ++w) {
+      const int64_t k0 = a->tile_off[i * WARP_PARTS + w], k1 = a->tile_off[i * WARP_PARTS + w + 1];
+      CHECK_ARG(k1 - k0 >= 0 && k1 - k0 <= PART_NODES, "more than 15 tiles per (instance, warp)");
+      for (int64_t k = k0; k < k1; ++k)
+        CHECK_ARG(a->tiles[16 * k] < ng, "tile group out of range for its instance");
+    }
+  }
   L.has_accum = true;
   return IFGFB_OK;
 }
