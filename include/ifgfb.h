@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define IFGFB_ABI_VERSION 1
+#define IFGFB_ABI_VERSION 2
 
 enum {
   IFGFB_OK = 0,
@@ -100,10 +100,12 @@ typedef struct {
 /* ---- propagation child level d -> parent level d-1 (reference _AccumType /
  *      _accum_types / _accumulate_level, ifgf.py:676-785), regrouped per
  *      parent segment row (owner computes).  Each CTA owns one parent
- *      segment row; its 75 nodes are split into 5 warp-owned sets of 15
- *      (row_order: node at set position, warp w owns positions 15w..15w+14).
- *      Per (instance, warp) the owned nodes are grouped by child segment
- *      into MMA row tiles of <= 8 nodes. */
+ *      segment row; its 75 nodes, in row_order, are split into 5 contiguous
+ *      warp-owned sets (warp w owns positions row_cuts[w] .. row_cuts[w+1]-1,
+ *      at most 23 nodes).  Per (instance, warp) the owned nodes are grouped
+ *      by child segment into MMA row tiles of <= 8 nodes.  row_order,
+ *      row_cuts, tile_off and tiles are what ifgfb_row_tiles_plan/_fill
+ *      produce. */
 typedef struct {
   int32_t level;             /* child level d */
   int64_t n_types;
@@ -112,6 +114,7 @@ typedef struct {
   const double* node_r;      /* n_types*75*2: r_parent, r_child */
   int64_t n_parent_rows;     /* segments of level d-1 */
   const uint8_t* row_order;  /* n_parent_rows*75 */
+  const uint8_t* row_cuts;   /* n_parent_rows*6: 0 = c0 < c1 < ... < c5 = 75 */
   const int64_t* inst_off;   /* n_parent_rows+1 */
   int64_t n_instances;
   const int64_t* inst_type;  /* n_instances */
@@ -163,6 +166,26 @@ typedef struct {
 int ifgfb_abi_version(void);
 const char* ifgfb_last_error(void);
 int ifgfb_device_info(char* buf, size_t len);
+
+/* Plan-time owner partition and MMA row tiles of one propagation level
+ * (host only; octree.row_tiles; csrc/tiles.cpp).  Inputs are the
+ * accumulation plan regrouped per parent row (reference _accum_types,
+ * ifgf.py:705-749): inst_off (n_rows+1), inst_type (instances), group_id
+ * (n_types*75: sigma group of each parent node under the type, < 32).
+ * _plan writes row_order (n_rows*75), row_cuts (n_rows*6) and tile_off
+ * (n_instances*5+1; tile_off[n_instances*5] = number of tiles);
+ * cut_radius 0..4 (0 = equal sets of 15).  _fill then writes the 16-byte
+ * tile records.  n_threads <= 0: all hardware threads. */
+int ifgfb_row_tiles_plan(int64_t n_rows, const int64_t* inst_off,
+                         const int64_t* inst_type, int64_t n_types,
+                         const uint8_t* group_id, uint8_t* row_order,
+                         uint8_t* row_cuts, int64_t* tile_off,
+                         int32_t cut_radius, int32_t n_threads);
+int ifgfb_row_tiles_fill(int64_t n_rows, const int64_t* inst_off,
+                         const int64_t* inst_type, int64_t n_types,
+                         const uint8_t* group_id, const uint8_t* row_order,
+                         const uint8_t* row_cuts, const int64_t* tile_off,
+                         uint8_t* tiles, int32_t n_threads);
 
 int ifgfb_plan_create(const ifgfb_tree_desc* tree, ifgfb_plan** out);
 int ifgfb_plan_add_level(ifgfb_plan* plan, const ifgfb_level_desc* lvl);

@@ -26,6 +26,7 @@ IFGFB_ERR_ARG = -1
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int64)
+_u8p = C.POINTER(C.c_uint8)
 
 
 class TreeDesc(C.Structure):
@@ -56,6 +57,7 @@ class AccumDesc(C.Structure):
                 ("node_geom", _dp), ("node_r", _dp),
                 ("n_parent_rows", C.c_int64),
                 ("row_order", C.POINTER(C.c_uint8)),
+                ("row_cuts", C.POINTER(C.c_uint8)),
                 ("inst_off", _ip), ("n_instances", C.c_int64),
                 ("inst_type", _ip), ("inst_crow_off", _ip), ("crow", _ip),
                 ("tile_off", _ip), ("n_tiles", C.c_int64),
@@ -133,6 +135,10 @@ EXPORTS = {
     "ifgfb_plan_far_buffers": ([C.c_void_p, C.POINTER(C.c_void_p),
                                 C.POINTER(C.c_void_p), C.POINTER(C.c_int64)],
                                C.c_int),
+    "ifgfb_row_tiles_plan": ([C.c_int64, _ip, _ip, C.c_int64, _u8p, _u8p, _u8p,
+                              _ip, C.c_int32, C.c_int32], C.c_int),
+    "ifgfb_row_tiles_fill": ([C.c_int64, _ip, _ip, C.c_int64, _u8p, _u8p, _u8p,
+                              _ip, _u8p, C.c_int32], C.c_int),
     "ifgfb_zscal_div": ([C.c_void_p, C.c_void_p, C.c_double, C.c_int64,
                          C.c_void_p], C.c_int),
 }
@@ -154,7 +160,7 @@ def load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.ifgfb_abi_version() != 1:
+    if lib.ifgfb_abi_version() != 2:
         raise RuntimeError("libifgfb200 ABI version mismatch")
     _lib = lib
     return lib
@@ -175,6 +181,13 @@ def dptr(a: np.ndarray):
         return None
     assert a.flags.c_contiguous and a.dtype in (np.float64, np.complex128)
     return a.ctypes.data_as(_dp)
+
+
+def u8ptr(a: np.ndarray):
+    if a is None:
+        return None
+    assert a.flags.c_contiguous and a.dtype == np.uint8
+    return a.ctypes.data_as(_u8p)
 
 
 def iptr(a: np.ndarray):

@@ -23,7 +23,8 @@ constexpr int NRCOL = 2 * NCOL;   // 32 real columns
 constexpr int KSTEPS = 20;
 constexpr int SEG_DOUBLES = KSTEPS * 32 * 4;  // 2560 doubles = 20 KB per segment
 constexpr int WARP_PARTS = 5;                 // propagation: node owners per CTA
-constexpr int PART_NODES = NN / WARP_PARTS;   // 15 parent nodes per warp
+constexpr int PART_NODES = NN / WARP_PARTS;   // 15 parent nodes per warp (mean)
+constexpr int MAX_SET = 23;                   // largest warp-owned node set
 
 void set_error(const std::string& msg);
 
@@ -171,6 +172,7 @@ struct Level {
   int64_t n_types = 0;
   int* tile_off = nullptr;     // n_instances*WARP_PARTS+1
   unsigned char* row_order = nullptr;  // parent rows x NN
+  unsigned char* row_cuts = nullptr;   // parent rows x (WARP_PARTS+1)
   uint4* tiles = nullptr;      // 16-byte tile records
   double* node_geom = nullptr; // n_types*NN*3 (parent node order)
   double* node_r = nullptr;    // n_types*NN*2 (r_parent, r_child)

@@ -317,7 +317,7 @@ __global__ void ratio_kernel(int64_t n, const double* __restrict__ node_r,
 struct AccArgs {
   const int* inst_off; const int* inst_type; const int* inst_crow_off;
   const int* crow; const int* tile_off; const uint4* tiles;
-  const unsigned char* row_order;
+  const unsigned char* row_order; const unsigned char* row_cuts;
   const double* node_geom; const double2* ratio;
   const double* coef_child; double* coef_parent;
   int row0;              // first parent row handled (partition)
@@ -346,14 +346,16 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" :: "n"(N));
 }
 
-// Per-warp staging of one (instance, warp): everything the warp's tiles read
-// besides the child coefficients, indexed by the warp-set slot.
+// Staging of one instance for the CTA: everything the tiles read besides the
+// child coefficients.  Indexed by node position in the row order, so warp w
+// fills and reads only its own slice [cuts[w], cuts[w+1]) (a warp has at
+// most as many tiles as nodes) and no cross-warp synchronisation is needed.
 constexpr int MAX_GROUPS = 32;        // child segments per instance (checked at plan time)
-struct __align__(16) WarpStage {
-  uint4 tiles[PART_NODES];            // <= 15 row tiles (one node each at worst)
-  double2 ratio[PART_NODES * 2];      // [slot][kappa]
-  double geom[PART_NODES * 3];        // [slot][xs, xt, xp]
-  int crow[MAX_GROUPS];
+struct __align__(16) RowStage {
+  uint4 tiles[NN];                    // warp w: tiles[cuts[w] ..]
+  double2 ratio[NN * 2];              // [position][kappa]
+  double geom[NN * 3];                // [position][xs, xt, xp]
+  int crow[WARP_PARTS][MAX_GROUPS];   // per-warp copy of the instance's child rows
 };
 
 // Row (lane group grp) of a K4 row tile: the warp-set slot it owns; rows past
@@ -367,9 +369,9 @@ __device__ __forceinline__ int tile_slot(const uint4& tl, int grp, bool& valid) 
 }
 
 // One CTA (5 warps) per parent segment row, owner computes: warp w owns the
-// 15 parent nodes at positions 15w..15w+14 of the row's signature order
-// (octree.row_tiles) and keeps their 16-column accumulators in its own shared
-// slice (no atomics, no inter-warp hazards; every warp walks every (parent
+// parent nodes at positions row_cuts[w]..row_cuts[w+1]-1 (7..23 nodes) of the
+// row's signature order (octree.row_tiles, csrc/tiles.cpp) and keeps their
+// 16-column accumulators in its own shared slice (no atomics, no inter-warp hazards; every warp walks every (parent
 // segment, child) instance).  Per instance each warp re-interpolates the
 // child's coefficients at its nodes: row tiles of <= 8 nodes sharing a child
 // segment sigma, 20 k-steps x 4 column tiles of FP64 DMMA, times the
@@ -379,19 +381,21 @@ __device__ __forceinline__ int tile_slot(const uint4& tl, int grp, bool& valid) 
 // summed values are transformed to coefficients (K3) and written once.
 template <int NK>
 __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
-  __shared__ double2 acc[WARP_PARTS * PART_NODES * NCOL];   // 19.2 KB
-  __shared__ WarpStage stage[WARP_PARTS][2];                // 12.3 KB
+  __shared__ double2 acc[NN * NCOL];                        // 19.2 KB
+  __shared__ RowStage stage[2];                             // 11.8 KB
   __shared__ unsigned char ord[NN], inv[NN];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, tig = lane & 3;
-  double2* mine = acc + warp * PART_NODES * NCOL;
-  const unsigned char* word = ord + warp * PART_NODES;
   const int pbeg = a.row0 + blockIdx.x * a.rows_per_cta;
   const int pend = min(pbeg + a.rows_per_cta, a.row_end);
   for (int p = pbeg; p < pend; ++p) {
-  if (lane < PART_NODES)         // each warp loads its own part of the order
-    ord[warp * PART_NODES + lane] = a.row_order[(size_t)p * NN + warp * PART_NODES + lane];
-  for (int i = lane; i < PART_NODES * NCOL; i += 32) mine[i] = make_double2(0.0, 0.0);
+  const int pos0 = a.row_cuts[(size_t)p * (WARP_PARTS + 1) + warp];
+  const int nset = a.row_cuts[(size_t)p * (WARP_PARTS + 1) + warp + 1] - pos0;
+  double2* mine = acc + pos0 * NCOL;
+  const unsigned char* word = ord + pos0;
+  if (lane < nset)               // each warp loads its own part of the order
+    ord[pos0 + lane] = a.row_order[(size_t)p * NN + pos0 + lane];
+  for (int i = lane; i < nset * NCOL; i += 32) mine[i] = make_double2(0.0, 0.0);
   // the row's instance scalars, lane j <-> instance i0 + j (<= 8 per row)
   const int i0 = a.inst_off[p], ni = a.inst_off[p + 1] - i0;
   int my_t = 0, my_ks = 0, my_ke = 0, my_co = 0;
@@ -402,26 +406,26 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
   }
   if (lane <= ni) my_co = a.inst_crow_off[i0 + lane];
   __syncwarp();
-  auto stage_inst = [&](int j, WarpStage& S) {
+  auto stage_inst = [&](int j, RowStage& S) {
     const int t = __shfl_sync(0xffffffffu, my_t, j);
     const int ks = __shfl_sync(0xffffffffu, my_ks, j);
     const int ke = __shfl_sync(0xffffffffu, my_ke, j);
     const int cs = __shfl_sync(0xffffffffu, my_co, j);
     const int ce = __shfl_sync(0xffffffffu, my_co, j + 1);
     const size_t tb = (size_t)t * NN;
-    for (int e = lane; e < PART_NODES * 3; e += 32)
-      cp_async8(&S.geom[e], a.node_geom + (tb + word[e / 3]) * 3 + e % 3);
-    if (lane < PART_NODES * NK)
-      cp_async16(&S.ratio[lane], a.ratio + (tb + word[lane / NK]) * NK + lane % NK);
-    if (lane < ke - ks) cp_async16(&S.tiles[lane], a.tiles + ks + lane);
-    if (lane < ce - cs) cp_async4(&S.crow[lane], a.crow + cs + lane);
+    for (int e = lane; e < nset * 3; e += 32)
+      cp_async8(&S.geom[3 * pos0 + e], a.node_geom + (tb + word[e / 3]) * 3 + e % 3);
+    for (int e = lane; e < nset * NK; e += 32)
+      cp_async16(&S.ratio[NK * pos0 + e], a.ratio + (tb + word[e / NK]) * NK + e % NK);
+    if (lane < ke - ks) cp_async16(&S.tiles[pos0 + lane], a.tiles + ks + lane);
+    if (lane < ce - cs) cp_async4(&S.crow[warp][lane], a.crow + cs + lane);
     cp_async_commit();
   };
-  if (ni > 0) stage_inst(0, stage[warp][0]);
+  if (ni > 0) stage_inst(0, stage[0]);
   for (int j = 0; j < ni; ++j) {
-    const WarpStage& S = stage[warp][j & 1];
+    const RowStage& S = stage[j & 1];
     if (j + 1 < ni) {
-      stage_inst(j + 1, stage[warp][(j + 1) & 1]);
+      stage_inst(j + 1, stage[(j + 1) & 1]);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -429,22 +433,22 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
     __syncwarp();
     const int ntile = __shfl_sync(0xffffffffu, my_ke - my_ks, j);
     for (int k = 0; k < ntile; ++k) {
-      const uint4 tl = S.tiles[k];
+      const uint4 tl = S.tiles[pos0 + k];
       bool valid;
       const int slot = tile_slot(tl, grp, valid);
 #ifdef IFGFB_ACC_FAKEB   // diagnostic only: every tile reads the first owned child row
-      const int crow_used = S.crow[0] & 0;
+      const int crow_used = S.crow[warp][0] & 0;
 #else
-      const int crow_used = S.crow[tl.x & 0xff];
+      const int crow_used = S.crow[warp][tl.x & 0xff];
 #endif
-      const double* ng = S.geom + slot * 3;
+      const double* ng = S.geom + (pos0 + slot) * 3;
       const BasisA B = make_basis<false>(ng[0], ng[1], ng[2], tig);
       double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
       basis_times_block<false, IFGFB_ACC_QUNROLL>(
           B, a.coef_child + (size_t)crow_used * SEG_DOUBLES, lane, c0, c1);
       if (valid) {
-        const double2 r0 = S.ratio[slot * NK];
-        const double2 r1 = NK > 1 ? S.ratio[slot * NK + NK - 1] : r0;
+        const double2 r0 = S.ratio[(pos0 + slot) * NK];
+        const double2 r1 = NK > 1 ? S.ratio[(pos0 + slot) * NK + NK - 1] : r0;
         double2* dst = mine + slot * NCOL;
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
@@ -653,7 +657,7 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
           Level& U = p.levels[d - 1];
           if (U.seg_hi() > U.seg_lo()) {
             AccArgs aa{L.inst_off, L.inst_type, L.inst_crow_off, L.crow, L.tile_off,
-                       L.tiles, L.row_order, L.node_geom,
+                       L.tiles, L.row_order, L.row_cuts, L.node_geom,
                        reinterpret_cast<const double2*>(L.ratio),
                        p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
                        p.coef[cur ^ 1] - (size_t)U.seg_lo() * SEG_DOUBLES, U.seg_lo()};

@@ -232,12 +232,20 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
     const uint8_t* t = a->tiles + 16 * i;
     CHECK_ARG(t[1] >= 1 && t[1] <= 8, "tile row count out of range");
     for (int r = 0; r < t[1]; ++r)
-      CHECK_ARG(t[2 + r] < PART_NODES, "tile slot out of range");
+      CHECK_ARG(t[2 + r] < MAX_SET, "tile slot out of range");
   }
   RC(dev_upload(p, &L.tiles, reinterpret_cast<const uint4*>(a->tiles), (size_t)a->n_tiles));
   for (int64_t i = 0; i < a->n_parent_rows * NN; ++i)
     CHECK_ARG(a->row_order[i] < NN, "row_order entry out of range");
   RC(dev_upload(p, &L.row_order, a->row_order, (size_t)a->n_parent_rows * NN));
+  CHECK_ARG(a->row_cuts != nullptr, "row_cuts missing");
+  for (int64_t r = 0; r < a->n_parent_rows; ++r) {
+    const uint8_t* c = a->row_cuts + r * (WARP_PARTS + 1);
+    CHECK_ARG(c[0] == 0 && c[WARP_PARTS] == NN, "row_cuts must start at 0 and end at 75");
+    for (int w = 0; w < WARP_PARTS; ++w)
+      CHECK_ARG(c[w + 1] > c[w] && c[w + 1] - c[w] <= MAX_SET, "row_cuts: warp set size out of 1..23");
+  }
+  RC(dev_upload(p, &L.row_cuts, a->row_cuts, (size_t)a->n_parent_rows * (WARP_PARTS + 1)));
   RC(dev_upload(p, &L.node_geom, a->node_geom, (size_t)nt * NN * 3));
   RC(dev_upload(p, &L.node_r, a->node_r, (size_t)nt * NN * 2));
   RC(dev_alloc(p, &L.ratio, (size_t)nt * NN * 4));
@@ -263,7 +271,7 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
     CHECK_ARG(ng >= 0 && ng <= 32, "more than 32 child segments in one instance");
     for (int w = 0; w < WARP_PARTS; ++w) {
       const int64_t k0 = a->tile_off[i * WARP_PARTS + w], k1 = a->tile_off[i * WARP_PARTS + w + 1];
-      CHECK_ARG(k1 - k0 >= 0 && k1 - k0 <= PART_NODES, "more than 15 tiles per (instance, warp)");
+      CHECK_ARG(k1 - k0 >= 0 && k1 - k0 <= MAX_SET, "more than 23 tiles per (instance, warp)");
       for (int64_t k = k0; k < k1; ++k)
         CHECK_ARG(a->tiles[16 * k] < ng, "tile group out of range for its instance");
     }

@@ -1,0 +1,249 @@
+// Host-side (plan time) owner partition and MMA row tiles of one propagation
+// level: the native builder behind octree.row_tiles.  Pure integer work on
+// the accumulation plan (reference _accum_types, ifgf.py:705-749), threaded
+// over parent rows.
+//
+// Per parent segment row (<= 8 instances, one per child box):
+//  1. signature order: nodes stably sorted by the key that packs, 4 bits per
+//     instance slot, the node's sigma group under each child (0xF for absent
+//     slots), so nodes that share child segments under every child are
+//     adjacent;
+//  2. warp cuts: the order is split into WARP_PARTS contiguous sets, cut k in
+//     [15k - R, 15k + R] (sets of 7..23 nodes), chosen by a small DP that
+//     minimises the largest per-warp tile count over the row's instances
+//     (the CTA waits for its slowest warp before the K3 transform), ties by
+//     the row's total tile count, then by the earliest cut;
+//  3. tiles: per (instance, warp) the owned slots are stably grouped by sigma
+//     group and cut into runs of <= 8 rows.
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/ifgfb.h"
+
+namespace ifgfb {
+void set_error(const std::string& msg);
+}
+
+namespace {
+
+constexpr int NN = 75, WP = 5, PER = 15, MAX_R = 4, MAX_SET = 24, MAX_INST = 8;
+constexpr int MAX_GROUPS = 32;
+
+struct RowIn {
+  const int64_t* inst_off;
+  const int64_t* inst_type;
+  const uint8_t* group_id;   // (n_types, 75)
+};
+
+// order + cuts of row r; returns false on malformed input
+bool row_partition(const RowIn& in, int64_t r, int R, uint8_t* order, uint8_t* cuts) {
+  const int64_t i0 = in.inst_off[r], ni = in.inst_off[r + 1] - i0;
+  if (ni < 0 || ni > MAX_INST) return false;
+  int64_t key[NN];
+  for (int n = 0; n < NN; ++n) {
+    int64_t k = 0;
+    for (int i = 0; i < MAX_INST; ++i) {
+      const int64_t g = i < ni ? in.group_id[in.inst_type[i0 + i] * NN + n] : 0xF;
+      k |= g << (4 * (7 - i));
+    }
+    key[n] = k;
+  }
+  int idx[NN];
+  std::iota(idx, idx + NN, 0);
+  std::stable_sort(idx, idx + NN, [&](int a, int b) { return key[a] < key[b]; });
+  for (int n = 0; n < NN; ++n) order[n] = (uint8_t)idx[n];
+  // groups in row order per instance
+  uint8_t gs[MAX_INST][NN];
+  for (int i = 0; i < ni; ++i) {
+    const uint8_t* g = in.group_id + in.inst_type[i0 + i] * NN;
+    for (int n = 0; n < NN; ++n) gs[i][n] = g[idx[n]];
+  }
+  // tiles of [a, b) summed over instances, for b swept upward from a
+  auto sweep = [&](int a, int bmax, int* tiles_upto /* index b - a */) {
+    uint8_t cnt[MAX_INST][MAX_GROUPS];
+    std::memset(cnt, 0, sizeof(cnt));
+    int tot = 0;
+    tiles_upto[0] = 0;
+    for (int b = a; b < bmax; ++b) {
+      for (int i = 0; i < ni; ++i)
+        if (cnt[i][gs[i][b]]++ % 8 == 0) ++tot;
+      tiles_upto[b + 1 - a] = tot;
+    }
+  };
+  // DP over cut positions: stage k chooses cut c_k (c_0 = 0, c_5 = 75)
+  constexpr int NO = 2 * MAX_R + 1;
+  int best_max[NO], best_tot[NO], from[WP][NO];
+  int prev_pos[NO], n_prev = 1;
+  prev_pos[0] = 0;
+  int pmax[NO] = {0}, ptot[NO] = {0};
+  for (int k = 1; k <= WP; ++k) {
+    int cur_pos[NO], n_cur = 0;
+    if (k < WP) {
+      for (int o = -R; o <= R; ++o) cur_pos[n_cur++] = PER * k + o;
+    } else {
+      cur_pos[n_cur++] = NN;
+    }
+    for (int c = 0; c < n_cur; ++c) { best_max[c] = INT32_MAX; best_tot[c] = INT32_MAX; }
+    for (int p = 0; p < n_prev; ++p) {
+      const int a = prev_pos[p], bmax = cur_pos[n_cur - 1];
+      int upto[NN + 1];
+      sweep(a, bmax, upto);
+      for (int c = 0; c < n_cur; ++c) {
+        const int b = cur_pos[c];
+        if (b - a < 1 || b - a > MAX_SET - 1) continue;
+        const int t = upto[b - a];
+        const int m = std::max(pmax[p], t), tt = ptot[p] + t;
+        if (m < best_max[c] || (m == best_max[c] && tt < best_tot[c])) {
+          best_max[c] = m;
+          best_tot[c] = tt;
+          from[k - 1][c] = p;
+        }
+      }
+    }
+    for (int c = 0; c < n_cur; ++c) {
+      prev_pos[c] = cur_pos[c];
+      pmax[c] = best_max[c];
+      ptot[c] = best_tot[c];
+    }
+    n_prev = n_cur;
+  }
+  // backtrack: from[k-1][c] = index of the stage k-1 cut; stage positions
+  // are PER*k + (index - R)
+  cuts[0] = 0;
+  cuts[WP] = NN;
+  int c = 0;
+  for (int k = WP; k >= 2; --k) {
+    c = from[k - 1][c];
+    cuts[k - 1] = (uint8_t)(PER * (k - 1) + c - R);
+  }
+  return true;
+}
+
+// tiles of (instance i of row r, warp w): writes up to MAX_SET records when
+// out != nullptr; returns the count
+int warp_tiles(const RowIn& in, int64_t inst, const uint8_t* order, const uint8_t* cuts,
+               int w, uint8_t* out) {
+  const int lo = cuts[w], hi = cuts[w + 1];
+  const uint8_t* g = in.group_id + in.inst_type[inst] * NN;
+  int slots[MAX_SET];
+  const int n = hi - lo;
+  for (int s = 0; s < n; ++s) slots[s] = s;
+  std::stable_sort(slots, slots + n,
+                   [&](int a, int b) { return g[order[lo + a]] < g[order[lo + b]]; });
+  int count = 0, run = 0, prev = -1;
+  uint8_t* rec = nullptr;
+  for (int s = 0; s < n; ++s) {
+    const int gr = g[order[lo + slots[s]]];
+    if (gr != prev || run == 8) {
+      if (out) {
+        rec = out + 16 * count;
+        std::memset(rec, 0xFF, 16);
+        rec[0] = (uint8_t)gr;
+        rec[1] = 0;
+      }
+      ++count;
+      run = 0;
+      prev = gr;
+    }
+    if (out) {
+      rec[2 + run] = (uint8_t)slots[s];
+      rec[1] = (uint8_t)(run + 1);
+    }
+    ++run;
+  }
+  return count;
+}
+
+template <class F>
+void parallel_rows(int64_t n_rows, int n_threads, F&& f) {
+  if (n_threads <= 0) n_threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  n_threads = (int)std::min<int64_t>(n_threads, std::max<int64_t>(1, n_rows / 256));
+  std::vector<std::thread> pool;
+  const int64_t chunk = (n_rows + n_threads - 1) / n_threads;
+  for (int t = 0; t < n_threads; ++t) {
+    const int64_t r0 = t * chunk, r1 = std::min(n_rows, r0 + chunk);
+    if (r0 >= r1) break;
+    pool.emplace_back([=, &f] { f(r0, r1); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+bool check_groups(const uint8_t* group_id, int64_t n_types) {
+  for (int64_t i = 0; i < n_types * NN; ++i)
+    if (group_id[i] >= MAX_GROUPS) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ifgfb_row_tiles_plan(int64_t n_rows, const int64_t* inst_off, const int64_t* inst_type,
+                         int64_t n_types, const uint8_t* group_id, uint8_t* row_order,
+                         uint8_t* row_cuts, int64_t* tile_off, int32_t cut_radius,
+                         int32_t n_threads) {
+  if (n_rows < 0 || !inst_off || (n_rows && (!row_order || !row_cuts || !tile_off)) ||
+      cut_radius < 0 || cut_radius > MAX_R) {
+    ifgfb::set_error("ifgfb_row_tiles_plan: bad arguments");
+    return IFGFB_ERR_ARG;
+  }
+  if (!check_groups(group_id, n_types)) {
+    ifgfb::set_error("ifgfb_row_tiles_plan: sigma group id >= 32");
+    return IFGFB_ERR_ARG;
+  }
+  const int64_t ni = inst_off[n_rows] - inst_off[0];
+  for (int64_t i = 0; i < ni; ++i)
+    if (inst_type[inst_off[0] + i] < 0 || inst_type[inst_off[0] + i] >= n_types) {
+      ifgfb::set_error("ifgfb_row_tiles_plan: inst_type out of range");
+      return IFGFB_ERR_ARG;
+    }
+  RowIn in{inst_off, inst_type, group_id};
+  std::atomic<bool> bad{false};
+  // pass 1: order, cuts and per-(instance, warp) tile counts into tile_off[1..]
+  parallel_rows(n_rows, n_threads, [&](int64_t r0, int64_t r1) {
+    for (int64_t r = r0; r < r1; ++r) {
+      uint8_t* ord = row_order + r * NN;
+      uint8_t* cut = row_cuts + r * (WP + 1);
+      if (!row_partition(in, r, cut_radius, ord, cut)) { bad = true; continue; }
+      for (int64_t i = inst_off[r]; i < inst_off[r + 1]; ++i)
+        for (int w = 0; w < WP; ++w)
+          tile_off[(i - inst_off[0]) * WP + w + 1] = warp_tiles(in, i, ord, cut, w, nullptr);
+    }
+  });
+  if (bad) {
+    ifgfb::set_error("ifgfb_row_tiles_plan: more than 8 instances in a parent row");
+    return IFGFB_ERR_ARG;
+  }
+  tile_off[0] = 0;
+  for (int64_t k = 1; k <= ni * WP; ++k) tile_off[k] += tile_off[k - 1];
+  return IFGFB_OK;
+}
+
+int ifgfb_row_tiles_fill(int64_t n_rows, const int64_t* inst_off, const int64_t* inst_type,
+                         int64_t n_types, const uint8_t* group_id, const uint8_t* row_order,
+                         const uint8_t* row_cuts, const int64_t* tile_off, uint8_t* tiles,
+                         int32_t n_threads) {
+  if (n_rows < 0 || !inst_off || !check_groups(group_id, n_types)) {
+    ifgfb::set_error("ifgfb_row_tiles_fill: bad arguments");
+    return IFGFB_ERR_ARG;
+  }
+  RowIn in{inst_off, inst_type, group_id};
+  parallel_rows(n_rows, n_threads, [&](int64_t r0, int64_t r1) {
+    for (int64_t r = r0; r < r1; ++r)
+      for (int64_t i = inst_off[r]; i < inst_off[r + 1]; ++i)
+        for (int w = 0; w < WP; ++w) {
+          const int64_t k = (i - inst_off[0]) * WP + w;
+          warp_tiles(in, i, row_order + r * NN, row_cuts + r * (WP + 1), w,
+                     tiles + 16 * tile_off[k]);
+        }
+  });
+  return IFGFB_OK;
+}
+
+}  // extern "C"

@@ -112,11 +112,12 @@ class FarFieldPlan:
         ap = accumulation_plan(self.tree, self.hier, d)
         # crow rows are reproduced exactly as the reference's searchsorted
         # picks them (ifgf.py:743-746), including any inexact hit.
-        row_order, tile_off, tiles = row_tiles(ap)
+        row_order, row_cuts, tile_off, tiles = row_tiles(ap)
         node_geom, node_r = node_tables(ap)
         u8 = __import__("ctypes").POINTER(__import__("ctypes").c_uint8)
         a = dict(ng=_c(node_geom, np.float64), nr=_c(node_r, np.float64),
-                 ro=np.ascontiguousarray(row_order), to=_c(tile_off, np.int64),
+                 ro=np.ascontiguousarray(row_order),
+                 rc=np.ascontiguousarray(row_cuts), to=_c(tile_off, np.int64),
                  tl=np.ascontiguousarray(tiles),
                  io=_c(ap.inst_off, np.int64), it=_c(ap.inst_type, np.int64),
                  ico=_c(ap.inst_crow_off, np.int64), cr=_c(ap.crow, np.int64))
@@ -124,6 +125,7 @@ class FarFieldPlan:
         desc = _lib.AccumDesc(
             d, ap.n_types, _lib.dptr(a["ng"]), _lib.dptr(a["nr"]),
             self.hier.level(d - 1).n_segments, a["ro"].ctypes.data_as(u8),
+            a["rc"].ctypes.data_as(u8),
             _lib.iptr(a["io"]), ap.n_instances, _lib.iptr(a["it"]),
             _lib.iptr(a["ico"]), _lib.iptr(a["cr"]), _lib.iptr(a["to"]),
             tiles.shape[0], a["tl"].ctypes.data_as(u8))

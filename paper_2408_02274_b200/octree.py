@@ -757,10 +757,52 @@ def _warp_set_tiles(gid, t, orow, w, per):
     return tid, tid[:, -1] + 1, gs, order, pos
 
 
-def row_tiles(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5,
-              chunk: int = 1 << 17):
-    """Per parent row partition of its 75 nodes into 5 warp-owned sets of 15
-    and the MMA row tiles of every (instance, warp).
+def row_tiles(ap: AccumulationPlan, cut_radius: int = 4, n_threads: int = 0):
+    """Per parent row partition of its 75 nodes into 5 contiguous warp-owned
+    sets and the MMA row tiles of every (instance, warp); native builder
+    (csrc/tiles.cpp, ``ifgfb_row_tiles_plan`` / ``_fill``).
+
+    Nodes are sorted by their child-segment signature over the row's
+    instances; the 4 cuts of that order are chosen per row within +-cut_radius
+    of 15k to minimise the largest per-warp tile count (cut_radius 0 gives
+    ``row_tiles_equal_split``, bit for bit).
+
+    Returns
+      row_order (n_rows, 75) uint8  node at set position
+      row_cuts  (n_rows, 6) uint8   warp w owns positions cuts[w]..cuts[w+1]-1
+      tile_off  (n_instances*5+1,)  tiles of (instance, warp)
+      tiles     (n_tiles, 16) uint8 [local group, rows, slot0..7, pad];
+                                    slot = position within the warp's set
+    """
+    from . import _lib
+    lib = _lib.load()
+    nn = 75
+    gid = _local_group_ids(ap, nn)
+    if gid.size and (gid.min() < 0 or gid.max() > 31):
+        raise ValueError("sigma group id outside 0..31")
+    gid = np.ascontiguousarray(gid, dtype=np.uint8)
+    n_rows = ap.inst_off.size - 1
+    io = np.ascontiguousarray(ap.inst_off, dtype=np.int64)
+    it = np.ascontiguousarray(ap.inst_type, dtype=np.int64)
+    row_order = np.empty((n_rows, nn), dtype=np.uint8)
+    row_cuts = np.empty((n_rows, WARP_PARTS + 1), dtype=np.uint8)
+    tile_off = np.zeros(ap.n_instances * WARP_PARTS + 1, dtype=np.int64)
+    _lib.check(lib.ifgfb_row_tiles_plan(
+        n_rows, _lib.iptr(io), _lib.iptr(it), ap.n_types, _lib.u8ptr(gid),
+        _lib.u8ptr(row_order), _lib.u8ptr(row_cuts), _lib.iptr(tile_off),
+        cut_radius, n_threads), "ifgfb_row_tiles_plan")
+    tiles = np.empty((int(tile_off[-1]), 16), dtype=np.uint8)
+    _lib.check(lib.ifgfb_row_tiles_fill(
+        n_rows, _lib.iptr(io), _lib.iptr(it), ap.n_types, _lib.u8ptr(gid),
+        _lib.u8ptr(row_order), _lib.u8ptr(row_cuts), _lib.iptr(tile_off),
+        _lib.u8ptr(tiles), n_threads), "ifgfb_row_tiles_fill")
+    return row_order, row_cuts, tile_off, tiles
+
+
+def row_tiles_equal_split(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5,
+                          chunk: int = 1 << 17):
+    """Numpy statement of ``row_tiles(ap, cut_radius=0)`` (equal sets of 15),
+    kept to cross-check the native builder (tests/test_plan.py).
 
     Nodes are sorted by their child-segment signature over the row's
     instances (the sigma group of the node under each child), so nodes that
@@ -825,7 +867,8 @@ def row_tiles(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5,
             tiles[lo + nz, 1] = rows_per[nz].astype(np.uint8)
 
     list(_pool().map(fill, blocks))
-    return row_order, tile_off, tiles
+    cuts = np.tile(np.arange(0, nn + 1, per, dtype=np.uint8), (n_rows, 1))
+    return row_order, cuts, tile_off, tiles
 
 
 def node_tables(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5):

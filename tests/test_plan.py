@@ -137,3 +137,67 @@ def test_cone_count_doubling_follows_code():
     hier = inp["hier"]
     ns = [hier.level(d).n_s for d in sorted(hier.cone_levels)]
     assert ns == sorted(ns, reverse=True)
+
+
+def _tile_invariants(ap, order, cuts, tile_off, tiles):
+    """Every (instance, warp) tile list covers exactly the warp's node set,
+    each tile holds <= 8 nodes of one sigma group; returns per-row warp
+    tile totals."""
+    gid = octree._local_group_ids(ap, 75)
+    n_rows = ap.inst_off.size - 1
+    per_row = np.zeros((n_rows, 5), dtype=np.int64)
+    assert np.all(cuts[:, 0] == 0) and np.all(cuts[:, 5] == 75)
+    assert np.all(np.diff(cuts.astype(int), axis=1) >= 7)
+    assert np.all(np.diff(cuts.astype(int), axis=1) <= 23)
+    for r in range(n_rows):
+        assert sorted(order[r]) == list(range(75))
+        for i in range(ap.inst_off[r], ap.inst_off[r + 1]):
+            g = gid[ap.inst_type[i]]
+            for w in range(5):
+                lo, hi = int(cuts[r, w]), int(cuts[r, w + 1])
+                seen = []
+                for k in range(tile_off[i * 5 + w], tile_off[i * 5 + w + 1]):
+                    t = tiles[k]
+                    rows = int(t[1])
+                    assert 1 <= rows <= 8 and np.all(t[2 + rows:] == 0xFF)
+                    slots = t[2:2 + rows].astype(int)
+                    assert np.all(g[order[r, lo + slots]] == t[0])
+                    seen += list(slots)
+                assert sorted(seen) == list(range(hi - lo))
+                per_row[r, w] += tile_off[i * 5 + w + 1] - tile_off[i * 5 + w]
+    return per_row
+
+
+def test_row_tiles_native_equal_split_matches_numpy():
+    """cut radius 0: the native builder (csrc/tiles.cpp) reproduces the
+    numpy statement bit for bit."""
+    inp = inputs("s1")
+    for d in range(4, inp["tree"].depth + 1):
+        ap = octree.accumulation_plan(inp["tree"], inp["hier"], d)
+        a = octree.row_tiles(ap, cut_radius=0, n_threads=3)
+        b = octree.row_tiles_equal_split(ap)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y), d
+
+
+def test_row_tiles_balanced_cuts_valid_and_no_worse():
+    inp = inputs("s1")
+    for d in range(4, inp["tree"].depth + 1):
+        ap = octree.accumulation_plan(inp["tree"], inp["hier"], d)
+        eq = _tile_invariants(ap, *octree.row_tiles(ap, cut_radius=0))
+        bal = _tile_invariants(ap, *octree.row_tiles(ap, cut_radius=4))
+        # the equal split is one of the DP's candidates
+        assert np.all(bal.max(1) <= eq.max(1))
+        assert bal.max(1).sum() < eq.max(1).sum()
+        # deterministic across thread counts
+        x = octree.row_tiles(ap, n_threads=1)
+        y = octree.row_tiles(ap, n_threads=4)
+        for u, v in zip(x, y):
+            assert np.array_equal(u, v)
+
+
+def test_row_tiles_rejects_bad_radius():
+    inp = inputs("s1")
+    ap = octree.accumulation_plan(inp["tree"], inp["hier"], 4)
+    with pytest.raises(ValueError):
+        octree.row_tiles(ap, cut_radius=5)
