@@ -171,7 +171,7 @@ int ifgfb_device_info(char* buf, size_t len);
  * (host only; octree.row_tiles; csrc/tiles.cpp).  Inputs are the
  * accumulation plan regrouped per parent row (reference _accum_types,
  * ifgf.py:705-749): inst_off (n_rows+1), inst_type (instances), group_id
- * (n_types*75: sigma group of each parent node under the type, < 32).
+ * (n_types*75: sigma group of each parent node under the type, < 75).
  * _plan writes row_order (n_rows*75), row_cuts (n_rows*6) and tile_off
  * (n_instances*5+1; tile_off[n_instances*5] = number of tiles);
  * cut_radius 0..4 (0 = equal sets of 15).  _fill then writes the 16-byte

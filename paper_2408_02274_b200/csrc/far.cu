@@ -350,7 +350,10 @@ __device__ __forceinline__ void cp_async_wait() {
 // child coefficients.  Indexed by node position in the row order, so warp w
 // fills and reads only its own slice [cuts[w], cuts[w+1]) (a warp has at
 // most as many tiles as nodes) and no cross-warp synchronisation is needed.
-constexpr int MAX_GROUPS = 32;        // child segments per instance (checked at plan time)
+#ifndef IFGFB_STAGE_GROUPS
+#define IFGFB_STAGE_GROUPS 32
+#endif
+constexpr int MAX_GROUPS = IFGFB_STAGE_GROUPS;  // staged child rows per instance (more: global)
 struct __align__(16) RowStage {
   uint4 tiles[NN];                    // warp w: tiles[cuts[w] ..]
   double2 ratio[NN * 2];              // [position][kappa]
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
     for (int e = lane; e < nset * NK; e += 32)
       cp_async16(&S.ratio[NK * pos0 + e], a.ratio + (tb + word[e / NK]) * NK + e % NK);
     if (lane < ke - ks) cp_async16(&S.tiles[pos0 + lane], a.tiles + ks + lane);
-    if (lane < ce - cs) cp_async4(&S.crow[warp][lane], a.crow + cs + lane);
+    if (lane < min(ce - cs, MAX_GROUPS)) cp_async4(&S.crow[warp][lane], a.crow + cs + lane);
     cp_async_commit();
   };
   if (ni > 0) stage_inst(0, stage[0]);
@@ -432,6 +435,7 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
     }
     __syncwarp();
     const int ntile = __shfl_sync(0xffffffffu, my_ke - my_ks, j);
+    const int* crow_g = a.crow + __shfl_sync(0xffffffffu, my_co, j);
     for (int k = 0; k < ntile; ++k) {
       const uint4 tl = S.tiles[pos0 + k];
       bool valid;
@@ -439,7 +443,8 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
 #ifdef IFGFB_ACC_FAKEB   // diagnostic only: every tile reads the first owned child row
       const int crow_used = S.crow[warp][0] & 0;
 #else
-      const int crow_used = S.crow[warp][tl.x & 0xff];
+      const int g = tl.x & 0xff;
+      const int crow_used = g < MAX_GROUPS ? S.crow[warp][g] : crow_g[g];
 #endif
       const double* ng = S.geom + (pos0 + slot) * 3;
       const BasisA B = make_basis<false>(ng[0], ng[1], ng[2], tig);

@@ -33,7 +33,7 @@ void set_error(const std::string& msg);
 namespace {
 
 constexpr int NN = 75, WP = 5, PER = 15, MAX_R = 4, MAX_SET = 24, MAX_INST = 8;
-constexpr int MAX_GROUPS = 32;
+constexpr int MAX_GROUPS = NN;   // a type's 75 nodes fall into <= 75 child segments
 
 struct RowIn {
   const int64_t* inst_off;
@@ -194,7 +194,7 @@ int ifgfb_row_tiles_plan(int64_t n_rows, const int64_t* inst_off, const int64_t*
     return IFGFB_ERR_ARG;
   }
   if (!check_groups(group_id, n_types)) {
-    ifgfb::set_error("ifgfb_row_tiles_plan: sigma group id >= 32");
+    ifgfb::set_error("ifgfb_row_tiles_plan: sigma group id >= 75");
     return IFGFB_ERR_ARG;
   }
   const int64_t ni = inst_off[n_rows] - inst_off[0];

@@ -778,8 +778,8 @@ def row_tiles(ap: AccumulationPlan, cut_radius: int = 4, n_threads: int = 0):
     lib = _lib.load()
     nn = 75
     gid = _local_group_ids(ap, nn)
-    if gid.size and (gid.min() < 0 or gid.max() > 31):
-        raise ValueError("sigma group id outside 0..31")
+    if gid.size and (gid.min() < 0 or gid.max() >= nn):
+        raise ValueError("sigma group id outside 0..74")
     gid = np.ascontiguousarray(gid, dtype=np.uint8)
     n_rows = ap.inst_off.size - 1
     io = np.ascontiguousarray(ap.inst_off, dtype=np.int64)
