@@ -173,6 +173,7 @@ struct Level {
   int* tile_off = nullptr;     // n_instances*WARP_PARTS+1
   unsigned char* row_order = nullptr;  // parent rows x NN
   unsigned char* row_cuts = nullptr;   // parent rows x (WARP_PARTS+1)
+  int max_groups = 0;                  // most child segments of one instance
   uint4* tiles = nullptr;      // 16-byte tile records
   double* node_geom = nullptr; // n_types*NN*3 (parent node order)
   double* node_r = nullptr;    // n_types*NN*2 (r_parent, r_child)

@@ -56,16 +56,16 @@ __device__ __forceinline__ int node_row(const unsigned char* inv, int a, int b, 
 }
 
 // In-place node values -> coefficients for one segment held in shared memory
-// (rows per node_row<OWNER>, NCOL complex columns): three axis transforms
-// (reference ifgf.py:502-522).
-template <bool OWNER>
+// (rows per node_row<OWNER>, NCOL complex columns, row stride RS complex):
+// three axis transforms (reference ifgf.py:502-522).
+template <bool OWNER, int RS = NCOL>
 __device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, int nthr) {
   for (int task = tid; task < PA * PA * NCOL; task += nthr) {
     const int bc = task / NCOL, m = task % NCOL;
     const int b = bc / PA, c = bc % PA;
     double2 v[PS];
 #pragma unroll
-    for (int a = 0; a < PS; ++a) v[a] = V[node_row<OWNER>(inv, a, b, c) * NCOL + m];
+    for (int a = 0; a < PS; ++a) v[a] = V[node_row<OWNER>(inv, a, b, c) * RS + m];
 #pragma unroll
     for (int a = 0; a < PS; ++a) {
       double2 s = make_double2(0.0, 0.0);
@@ -74,7 +74,7 @@ __device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, in
         s.x += c_ms[a * PS + q] * v[q].x;
         s.y += c_ms[a * PS + q] * v[q].y;
       }
-      V[node_row<OWNER>(inv, a, b, c) * NCOL + m] = s;
+      V[node_row<OWNER>(inv, a, b, c) * RS + m] = s;
     }
   }
   __syncthreads();
@@ -83,7 +83,7 @@ __device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, in
     const int a = ac / PA, c = ac % PA;
     double2 v[PA];
 #pragma unroll
-    for (int b = 0; b < PA; ++b) v[b] = V[node_row<OWNER>(inv, a, b, c) * NCOL + m];
+    for (int b = 0; b < PA; ++b) v[b] = V[node_row<OWNER>(inv, a, b, c) * RS + m];
 #pragma unroll
     for (int b = 0; b < PA; ++b) {
       double2 s = make_double2(0.0, 0.0);
@@ -92,7 +92,7 @@ __device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, in
         s.x += c_ma[b * PA + q] * v[q].x;
         s.y += c_ma[b * PA + q] * v[q].y;
       }
-      V[node_row<OWNER>(inv, a, b, c) * NCOL + m] = s;
+      V[node_row<OWNER>(inv, a, b, c) * RS + m] = s;
     }
   }
   __syncthreads();
@@ -101,7 +101,7 @@ __device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, in
     const int a = ab / PA, b = ab % PA;
     double2 v[PA];
 #pragma unroll
-    for (int c = 0; c < PA; ++c) v[c] = V[node_row<OWNER>(inv, a, b, c) * NCOL + m];
+    for (int c = 0; c < PA; ++c) v[c] = V[node_row<OWNER>(inv, a, b, c) * RS + m];
 #pragma unroll
     for (int c = 0; c < PA; ++c) {
       double2 s = make_double2(0.0, 0.0);
@@ -110,15 +110,17 @@ __device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, in
         s.x += c_ma[c * PA + q] * v[q].x;
         s.y += c_ma[c * PA + q] * v[q].y;
       }
-      V[node_row<OWNER>(inv, a, b, c) * NCOL + m] = s;
+      V[node_row<OWNER>(inv, a, b, c) * RS + m] = s;
     }
   }
   __syncthreads();
 }
 
-// Write one segment's coefficients V[i][m] (rows per node_row<OWNER>) in
-// DMMA B-fragment order (see SEG_DOUBLES): coalesced stores, padding zeroed.
-template <bool OWNER>
+// Write one segment's coefficients V[i][m] (rows per node_row<OWNER>, row
+// stride RS complex) in DMMA B-fragment order (see SEG_DOUBLES): coalesced
+// stores, padding zeroed.  RS = 20 spreads the 4 rows a warp reads over both
+// bank halves (conflict-free); the K4 accumulators keep RS = NCOL.
+template <bool OWNER, int RS = NCOL>
 __device__ __forceinline__ void store_segment(double* dst, const double2* V,
                                               const unsigned char* inv, int tid,
                                               int nthr) {
@@ -129,7 +131,7 @@ __device__ __forceinline__ void store_segment(double* dst, const double2* V,
     double v = 0.0;
     if (ab < PS * PA) {
       const int col = 8 * nt + (lane >> 2);
-      const double2 z = V[node_row<OWNER>(inv, ab / PA, ab % PA, c) * NCOL + (col >> 1)];
+      const double2 z = V[node_row<OWNER>(inv, ab / PA, ab % PA, c) * RS + (col >> 1)];
       v = (col & 1) ? z.y : z.x;
     }
     dst[idx] = v;
@@ -162,17 +164,28 @@ struct LeafArgs {
 // One CTA per finest-level segment: node values
 //   F[node][c*NK+k] = sum_{src in box} (r/d) exp(i kappa_k (d - r)) w[c][src]
 // (reference _direct_spectra_box, ifgf.py:535-554), then the K3 transform.
+// Thread (node, k) owns the CH columns of one wavenumber: 75*NK busy threads,
+// CH accumulators each (the per-value arithmetic and source order are those
+// of one thread per node, so the result does not depend on the split).
+constexpr int LEAF_RS = 20;   // padded row stride of the leaf's node values
 template <int NK>
-__global__ void __launch_bounds__(128) leaf_kernel(LeafArgs a) {
+constexpr int leaf_threads() { return ((NN * NK + 31) / 32) * 32; }
+
+#ifndef IFGFB_LEAF_MINB
+#define IFGFB_LEAF_MINB 5
+#endif
+template <int NK>
+__global__ void __launch_bounds__(leaf_threads<NK>(), IFGFB_LEAF_MINB) leaf_kernel(LeafArgs a) {
   constexpr int CH = NCOL / NK;
-  __shared__ double2 V[NN * NCOL];
+  __shared__ double2 V[NN * LEAF_RS];
   const int row = blockIdx.x + a.row0, tid = threadIdx.x;
   const int box = a.seg_box[row], id = a.seg_id[row];
-  if (tid < NN) {
+  if (tid < NN * NK) {
+    const int node = tid / NK, k = NK > 1 ? tid % NK : 0;
     const int two_na = 2 * a.n_a;
     const int i_p = id % two_na, rest = id / two_na;
     const int i_t = rest % a.n_a, i_s = rest / a.n_a;
-    const int na = tid / (PA * PA), nb = (tid / PA) % PA, nc = tid % PA;
+    const int na = node / (PA * PA), nb = (node / PA) % PA, nc = node % PA;
     const double* s_nodes = a.tabs;
     const double* sin_t = s_nodes + a.n_s * PS;
     const double* cos_t = sin_t + a.n_a * PA;
@@ -184,39 +197,34 @@ __global__ void __launch_bounds__(128) leaf_kernel(LeafArgs a) {
     const double x = add_rn(a.centers[3 * box + 0], mul_rn(r, mul_rn(st, cp)));
     const double y = add_rn(a.centers[3 * box + 1], mul_rn(r, mul_rn(st, sp)));
     const double z = add_rn(a.centers[3 * box + 2], mul_rn(r, ct));
-    double2 acc[NCOL];
+    const double kr = (NK > 1 && k) ? a.kr[1] : a.kr[0];
+    const double ki = (NK > 1 && k) ? a.ki[1] : a.ki[0];
+    double2 acc[CH];
 #pragma unroll
-    for (int m = 0; m < NCOL; ++m) acc[m] = make_double2(0.0, 0.0);
+    for (int c = 0; c < CH; ++c) acc[c] = make_double2(0.0, 0.0);
     const int s0 = a.pt_start[box], s1 = s0 + a.pt_count[box];
     for (int s = s0; s < s1; ++s) {
       const double dx = x - a.points[3 * s], dy = y - a.points[3 * s + 1],
                    dz = z - a.points[3 * s + 2];
       const double d = sqrt(dx * dx + dy * dy + dz * dz);
       const double q = r / d;
-      double2 g[NK];
-#pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        const double2 e = cexp_ikx(a.kr[k], a.ki[k], d - r);
-        g[k] = make_double2(q * e.x, q * e.y);
-      }
+      const double2 e = cexp_ikx(kr, ki, d - r);
+      const double2 g = make_double2(q * e.x, q * e.y);
       const double2* wv = a.wt + (size_t)s * CH;
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
-        const double2 wc = wv[c];
-#pragma unroll
-        for (int k = 0; k < NK; ++k) {
-          const double2 p = cmul(g[k], wc);
-          acc[c * NK + k].x += p.x;
-          acc[c * NK + k].y += p.y;
-        }
+        const double2 p = cmul(g, wv[c]);
+        acc[c].x += p.x;
+        acc[c].y += p.y;
       }
     }
 #pragma unroll
-    for (int m = 0; m < NCOL; ++m) V[tid * NCOL + m] = acc[m];
+    for (int c = 0; c < CH; ++c) V[node * LEAF_RS + c * NK + k] = acc[c];
   }
   __syncthreads();
-  to_coeffs_smem<false>(V, nullptr, tid, blockDim.x);
-  store_segment<false>(a.coef + (size_t)row * SEG_DOUBLES, V, nullptr, tid, blockDim.x);
+  to_coeffs_smem<false, LEAF_RS>(V, nullptr, tid, blockDim.x);
+  store_segment<false, LEAF_RS>(a.coef + (size_t)row * SEG_DOUBLES, V, nullptr, tid,
+                                blockDim.x);
 }
 
 // ------------------------------------------------------- DMMA helpers ----
@@ -382,7 +390,10 @@ __device__ __forceinline__ int tile_slot(const uint4& tl, int grp, bool& valid) 
 // geometry and ratios are staged by cp.async one instance ahead, so the
 // only global loads on a tile's critical path are the B fragments.  The
 // summed values are transformed to coefficients (K3) and written once.
-template <int NK>
+// WIDE: some instance of the level has more than MAX_GROUPS child segments
+// (coarse levels of large configurations); the extra rows are read from
+// global memory.  Kept out of the common instantiation (costs ~2%).
+template <int NK, bool WIDE>
 __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
   __shared__ double2 acc[NN * NCOL];                        // 19.2 KB
   __shared__ RowStage stage[2];                             // 11.8 KB
@@ -444,7 +455,7 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
       const int crow_used = S.crow[warp][0] & 0;
 #else
       const int g = tl.x & 0xff;
-      const int crow_used = g < MAX_GROUPS ? S.crow[warp][g] : crow_g[g];
+      const int crow_used = (!WIDE || g < MAX_GROUPS) ? S.crow[warp][g] : crow_g[g];
 #endif
       const double* ng = S.geom + (pos0 + slot) * 3;
       const BasisA B = make_basis<false>(ng[0], ng[1], ng[2], tig);
@@ -633,7 +644,7 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
                     L.seg_lo()};
         if (L.seg_hi() > L.seg_lo()) {
           const int tk = p.timer.begin(K_LEAF, st);
-          leaf_kernel<NK><<<L.seg_hi() - L.seg_lo(), 128, 0, st>>>(la);
+          leaf_kernel<NK><<<L.seg_hi() - L.seg_lo(), leaf_threads<NK>(), 0, st>>>(la);
           p.timer.end(tk, st);
           ++launches;
         }
@@ -670,8 +681,11 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
             aa.rows_per_cta = IFGFB_ACC_ROWS;
             const int nrows = U.seg_hi() - U.seg_lo();
             const int tk = p.timer.begin(K_ACCUM, st);
-            accum_kernel<NK><<<(nrows + IFGFB_ACC_ROWS - 1) / IFGFB_ACC_ROWS,
-                               32 * WARP_PARTS, 0, st>>>(aa);
+            const int grid = (nrows + IFGFB_ACC_ROWS - 1) / IFGFB_ACC_ROWS;
+            if (L.max_groups > MAX_GROUPS)
+              accum_kernel<NK, true><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
+            else
+              accum_kernel<NK, false><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
             p.timer.end(tk, st);
             ++launches;
           }

@@ -269,6 +269,7 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
   for (int64_t i = 0; i < ni; ++i) {
     const int64_t ng = a->inst_crow_off[i + 1] - a->inst_crow_off[i];
     CHECK_ARG(ng >= 0 && ng <= NN, "more than 75 child segments in one instance");
+    L.max_groups = std::max(L.max_groups, (int)ng);
     for (int w = 0; w < WARP_PARTS; ++w) {
       const int64_t k0 = a->tile_off[i * WARP_PARTS + w], k1 = a->tile_off[i * WARP_PARTS + w + 1];
       CHECK_ARG(k1 - k0 >= 0 && k1 - k0 <= MAX_SET, "more than 23 tiles per (instance, warp)");
