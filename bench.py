@@ -98,7 +98,7 @@ def work_counts(tree, hier):
     D = tree.depth
     prop = {}
     for d in range(4, D + 1):
-        ap = octree.accumulation_plan(tree, hier, d)
+        ap = octree.accumulation_plan(tree, hier, d, geometry=False)
         prop[d] = W_PROP * ap.n_instances + W_COEF * hier.level(d - 1).n_segments
     cl, lvl = hier.level(D), tree.level(D)
     leaf = W_LEAF * 75 * int((cl.seg_off[1:] - cl.seg_off[:-1]) @ lvl.pt_count)
@@ -257,7 +257,7 @@ def run_b200(args):
         runner = DistributedMullerOperator(op, parts[rank])
         mine = 0
         for d in range(4, tree.depth + 1):
-            ap = accumulation_plan(tree, hier, d)
+            ap = accumulation_plan(tree, hier, d, geometry=False)
             lo, hi = parts[rank].levels[d - 1]["seg"]
             mine += W_PROP * int(ap.inst_off[hi] - ap.inst_off[lo]) + W_COEF * (hi - lo)
         counts = dict(counts, prop=mine)

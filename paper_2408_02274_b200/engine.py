@@ -13,6 +13,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from . import octree
 from .octree import accumulation_plan, emission_plan, node_tables, row_tiles
 
 __all__ = ["FarFieldPlan", "ifgf_apply", "device_stream"]
@@ -31,7 +32,7 @@ class FarFieldPlan:
 
     def __init__(self, tree, hier, displaced_normals=None,
                  displaced_step: float = 1e-6, surface=None, near=None,
-                 kappas=None):
+                 kappas=None, trim_host: bool = True):
         lib = _lib.load()
         if not torch.cuda.is_available():
             raise RuntimeError("CUDA device required (no CPU fallback)")
@@ -57,12 +58,16 @@ class FarFieldPlan:
         self._h = h
         self.stats = {"levels": {}}
         try:
+            # uploads are synchronous: host staging arrays are dropped per call
             for d in range(3, self.depth + 1):
                 self._add_level(lib, d)
+                self._keep = []
             for d in range(4, self.depth + 1):
                 self._add_accum(lib, d)
+                self._keep = []
             for d in range(3, self.depth + 1):
                 self._add_emission(lib, d, disp_t)
+                self._keep = []
             if surface is not None:
                 _lib.check(lib.ifgfb_plan_set_surface(self._h, surface),
                            "ifgfb_plan_set_surface")
@@ -76,6 +81,8 @@ class FarFieldPlan:
             self._h = None
             raise
         self._keep = []
+        if trim_host:       # the device plan owns the per-type geometry now
+            octree.trim_accumulation_plans(hier)
 
     # ------------------------------------------------------------ upload --
     def _hold(self, *arrs):

@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import json
 from dataclasses import dataclass, field
+from functools import cached_property
 
 import numpy as np
 
@@ -526,12 +527,16 @@ class AccumulationPlan:
     """Types (parent segment id, child octant) with shared child-frame
     geometry, and instances regrouped per parent segment row.
 
-    Per type t (nodes sorted by child segment, as the reference's
-    ``_AccumType``): ``sig_off[t]:sig_off[t+1]`` child segment groups, group
-    g covering sorted node slots ``bounds[g]:bounds[g+1]`` (local to the
-    type); ``scatter[t, j]`` = parent node slot of sorted node j;
-    ``xs/xt/xp[t, j]`` = local coordinates in the child segment;
-    ``r_parent/r_child[t, j]`` = node radius about parent / child centre.
+    Stored per type t, in PARENT node order (what the device consumes; about
+    3.2 KB per type): ``gid[t, n]`` = sigma group (local to t) of parent node
+    n, ``node_geom[t, n]`` = (xs, xt, xp) local coordinates in its child
+    segment, ``node_r[t, n]`` = (r_parent, r_child); ``scatter[t, j]`` =
+    parent node at sorted slot j (nodes sorted by child segment, as the
+    reference's ``_AccumType``).  ``sig_off[t]:sig_off[t+1]`` index the
+    type's groups in ``group_sigma`` (child segment id per group).  The
+    reference-layout views (sorted order) ``xs``, ``xt``, ``xp``,
+    ``r_parent``, ``r_child``, ``group_bounds``, ``group_end`` are computed
+    on demand.
 
     Instances (one per (parent segment row, child box)) sorted by parent
     row then child box: ``inst_off`` (per parent row), ``inst_type``,
@@ -544,25 +549,63 @@ class AccumulationPlan:
     type_gamma: np.ndarray
     type_octant: np.ndarray
     sig_off: np.ndarray
-    group_bounds: np.ndarray      # flat, per group: start slot (len n_groups)
-    group_end: np.ndarray
     group_sigma: np.ndarray       # child segment id of each group
-    scatter: np.ndarray
-    xs: np.ndarray
-    xt: np.ndarray
-    xp: np.ndarray
-    r_parent: np.ndarray
-    r_child: np.ndarray
+    gid: np.ndarray               # (n_types, 75) uint8, parent order
+    scatter: np.ndarray           # (n_types, 75) uint8, sorted slot -> node
+    node_geom: np.ndarray         # (n_types, 75, 3) f64, parent order
+    node_r: np.ndarray            # (n_types, 75, 2) f64, parent order
     inst_off: np.ndarray
     inst_type: np.ndarray
     inst_child: np.ndarray
     inst_crow_off: np.ndarray
     crow: np.ndarray
     crow_misses: int = 0
+    trimmed: bool = False         # per-type arrays released (trim_...)
 
     @property
     def n_instances(self) -> int:
         return self.inst_type.size
+
+    def _sorted(self, arr):
+        return np.take_along_axis(arr, self.scatter.astype(np.int64), axis=1)
+
+    @cached_property
+    def xs(self):
+        return self._sorted(self.node_geom[..., 0])
+
+    @cached_property
+    def xt(self):
+        return self._sorted(self.node_geom[..., 1])
+
+    @cached_property
+    def xp(self):
+        return self._sorted(self.node_geom[..., 2])
+
+    @cached_property
+    def r_parent(self):
+        return self._sorted(self.node_r[..., 0])
+
+    @cached_property
+    def r_child(self):
+        return self._sorted(self.node_r[..., 1])
+
+    @cached_property
+    def group_end(self):
+        """Per group (flat): one past its last sorted slot (local to the
+        type; groups are contiguous in sorted order, local ids ascending)."""
+        nn = self.gid.shape[1]
+        flat = (self.sig_off[:-1, None] + self.gid).ravel()
+        size = np.bincount(flat, minlength=self.group_sigma.size)
+        owner = np.repeat(np.arange(self.n_types), np.diff(self.sig_off))
+        return np.cumsum(size) - nn * owner
+
+    @cached_property
+    def group_bounds(self):
+        """Per group (flat): its first sorted slot (local to the type)."""
+        end = self.group_end
+        nn = self.gid.shape[1]
+        flat = (self.sig_off[:-1, None] + self.gid).ravel()
+        return end - np.bincount(flat, minlength=self.group_sigma.size)
 
 
 def _type_geometry(pcl: ConeLevel, cl: ConeLevel, gamma, octant, child_side):
@@ -582,11 +625,14 @@ def _type_geometry(pcl: ConeLevel, cl: ConeLevel, gamma, octant, child_side):
     return fs, order, xs, xt, xp, take(rp), take(rc)
 
 
-def accumulation_plan(tree: BoxTree, hier: ConeHierarchy,
-                      d: int) -> AccumulationPlan:
-    """Plan for folding level-d child interpolants into level d-1."""
+def accumulation_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
+                      geometry: bool = True) -> AccumulationPlan:
+    """Plan for folding level-d child interpolants into level d-1, cached
+    on the hierarchy.  ``geometry=False`` accepts a cached plan whose
+    per-type arrays were released by ``trim_accumulation_plans`` (instance
+    counts and child rows only); otherwise a trimmed plan is rebuilt."""
     cache = hier.__dict__.setdefault("_b200_accum", {})
-    if d in cache:
+    if d in cache and (not geometry or not cache[d].trimmed):
         return cache[d]
     cl, pcl = hier.level(d), hier.level(d - 1)
     lvl = tree.level(d)
@@ -596,53 +642,64 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy,
                                  pcl.seg_off[lvl.parent + 1])
     key = pcl.seg_ids[prow] * 8 + octant[child]
     ukeys, inst_type = np.unique(key, return_inverse=True)
+    del key
     inst_type = inst_type.astype(np.int64)
     gamma, toct = ukeys >> 3, ukeys & 7
     n_t = ukeys.size
-    fs_all = np.empty((n_t, nn), dtype=np.int64)
-    order_all = np.empty((n_t, nn), dtype=np.int64)
-    geo = {k: np.empty((n_t, nn)) for k in ("xs", "xt", "xp", "rp", "rc")}
+    gid = np.empty((n_t, nn), dtype=np.uint8)
+    scatter = np.empty((n_t, nn), dtype=np.uint8)
+    node_geom = np.empty((n_t, nn, 3))
+    node_r = np.empty((n_t, nn, 2))
     step = max(1, 250_000 // nn)
+    blocks = list(range(0, n_t, step))
+    sig_parts = [None] * len(blocks)
 
-    def chunk(t0):
+    def chunk(ib):
+        t0 = blocks[ib]
         t1 = min(n_t, t0 + step)
         fs, order, xs, xt, xp, rp, rc = _type_geometry(
             pcl, cl, gamma[t0:t1], toct[t0:t1], lvl.side)
-        fs_all[t0:t1], order_all[t0:t1] = fs, order
-        for k, v in zip(("xs", "xt", "xp", "rp", "rc"), (xs, xt, xp, rp, rc)):
-            geo[k][t0:t1] = v
+        rows = np.arange(t1 - t0)[:, None]
+        newgrp = np.ones(fs.shape, dtype=bool)
+        newgrp[:, 1:] = fs[:, 1:] != fs[:, :-1]
+        local = np.cumsum(newgrp, axis=1) - 1           # group of sorted slot
+        if local.size and local.max() >= nn:
+            raise ValueError("more than 75 sigma groups in a type")
+        gid[t0:t1][rows, order] = local
+        scatter[t0:t1] = order
+        for k, v in enumerate((xs, xt, xp)):
+            node_geom[t0:t1, :, k][rows, order] = v
+        node_r[t0:t1, :, 0][rows, order] = rp
+        node_r[t0:t1, :, 1][rows, order] = rc
+        sig_parts[ib] = (newgrp.sum(axis=1), fs[newgrp])
 
-    list(_pool().map(chunk, range(0, n_t, step)))   # disjoint row blocks
-    # sigma groups per type
-    newgrp = np.ones((n_t, nn), dtype=bool)
-    newgrp[:, 1:] = fs_all[:, 1:] != fs_all[:, :-1]
-    g_type, g_start = np.nonzero(newgrp)
-    n_groups = g_type.size
-    sig_off = _offsets_from_owner(g_type, n_t)
-    g_end = np.empty(n_groups, dtype=np.int64)
-    g_end[:-1] = g_start[1:]
-    last = sig_off[1:] - 1
-    g_end[last] = nn
-    g_sigma = fs_all[g_type, g_start]
+    list(_pool().map(chunk, range(len(blocks))))   # disjoint row blocks
+    n_sig = np.concatenate([c for c, _ in sig_parts]) if blocks else np.zeros(0, np.int64)
+    g_sigma = (np.concatenate([g for _, g in sig_parts]) if blocks
+               else np.zeros(0, np.int64)).astype(np.int64)
+    del sig_parts
+    sig_off = np.zeros(n_t + 1, dtype=np.int64)
+    np.cumsum(n_sig, out=sig_off[1:])
     # instances sorted by (parent row, child): prow/child are generated
     # child-major, so re-sort
     order = np.lexsort((child, prow))
     prow, child, inst_type = prow[order], child[order], inst_type[order]
+    del order
     nsig = np.diff(sig_off)[inst_type]
     crow_off = np.zeros(prow.size + 1, dtype=np.int64)
     np.cumsum(nsig, out=crow_off[1:])
     gidx, g_own = _expand_ranges(sig_off[inst_type], sig_off[inst_type + 1])
     bkeys = box_keys(cl)
     want = child[g_own] * np.int64(id_stride(cl)) + g_sigma[gidx]
+    del gidx, g_own
     crow = np.searchsorted(bkeys, want).astype(np.int64)
     misses = int(np.count_nonzero(
         bkeys[np.minimum(crow, bkeys.size - 1)] != want))
+    del want
     plan = AccumulationPlan(
         level=d, n_types=n_t, type_gamma=gamma, type_octant=toct,
-        sig_off=sig_off, group_bounds=g_start, group_end=g_end,
-        group_sigma=g_sigma,
-        scatter=order_all, xs=geo["xs"], xt=geo["xt"], xp=geo["xp"],
-        r_parent=geo["rp"], r_child=geo["rc"],
+        sig_off=sig_off, group_sigma=g_sigma, gid=gid, scatter=scatter,
+        node_geom=node_geom, node_r=node_r,
         inst_off=_offsets_from_owner(prow, pcl.n_segments),
         inst_type=inst_type, inst_child=child, inst_crow_off=crow_off,
         crow=crow, crow_misses=misses)
@@ -650,94 +707,23 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy,
     return plan
 
 
+def trim_accumulation_plans(hier: ConeHierarchy) -> None:
+    """Release the per-type arrays (gid, scatter, node_geom, node_r: about
+    3.2 KB per type) of the cached plans once the device plan holds them;
+    instance arrays stay for work counts and partitioning."""
+    for ap in hier.__dict__.get("_b200_accum", {}).values():
+        ap.gid = ap.scatter = ap.node_geom = ap.node_r = None
+        for k in ("xs", "xt", "xp", "r_parent", "r_child", "group_end", "group_bounds"):
+            ap.__dict__.pop(k, None)
+        ap.trimmed = True
+
+
 WARP_PARTS = 5          # parent nodes owned per warp: fixed theta index b
-
-
-def warp_tiles(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5):
-    """Device tiling of every propagation type for the node-owner kernel.
-
-    The 75 parent nodes (a, b, c) are split into 5 fixed sets by the theta
-    index b (warp w owns the 15 nodes with b == w).  Per type and warp the
-    owned nodes are grouped by child segment (sigma group) and chunked into
-    MMA row tiles of <= 8 nodes.  Returns
-
-      tile_off   (n_types*5 + 1,) int64  tile range of (type, warp)
-      tiles      (n_tiles, 16)    uint8  [local group, n_rows, slot0..7, pad]
-                                         slot = a*p_a + c (0..14), 0xFF = pad
-      node_geom  (n_types, 75, 3) f64    xs, xt, xp in PARENT node order
-      node_r     (n_types, 75, 2) f64    r_parent, r_child in parent order
-    """
-    nn = p_s * p_a * p_a
-    nt = ap.n_types
-    gid = np.empty((nt, nn), dtype=np.int64)
-    node_geom = np.empty((nt, nn, 3))
-    node_r = np.empty((nt, nn, 2))
-    rows = np.arange(nt)[:, None]
-    # sorted slot j of type t holds parent node scatter[t, j]
-    gsorted = np.repeat(np.arange(ap.group_sigma.size) -
-                        np.repeat(ap.sig_off[:-1], np.diff(ap.sig_off)),
-                        ap.group_end - ap.group_bounds)
-    gid[rows, ap.scatter] = gsorted.reshape(nt, nn)
-    for k, arr in enumerate((ap.xs, ap.xt, ap.xp)):
-        node_geom[rows, ap.scatter, k] = arr
-    node_r[rows, ap.scatter, 0] = ap.r_parent
-    node_r[rows, ap.scatter, 1] = ap.r_child
-    b_of = (np.arange(nn) // p_a) % p_a
-    slot_of = (np.arange(nn) // (p_a * p_a)) * p_a + np.arange(nn) % p_a
-    tiles = []
-    counts = np.zeros(nt * WARP_PARTS, dtype=np.int64)
-    for w in range(WARP_PARTS):
-        nodes = np.nonzero(b_of == w)[0]               # parent order
-        g = gid[:, nodes]                              # (nt, 15)
-        order = np.argsort(g, axis=1, kind="stable")
-        gs = np.take_along_axis(g, order, axis=1)
-        sl = slot_of[nodes][order]                     # (nt, 15)
-        # run starts and positions inside each run
-        new = np.ones_like(gs, dtype=bool)
-        new[:, 1:] = gs[:, 1:] != gs[:, :-1]
-        run_id = np.cumsum(new, axis=1) - 1
-        start = np.zeros_like(gs)
-        idx = np.arange(gs.shape[1])[None, :].repeat(nt, 0)
-        start_pos = np.where(new, idx, 0)
-        start = np.maximum.accumulate(start_pos, axis=1)
-        pos = idx - start                              # position in run
-        tile_in_run = pos // 8
-        # tile key per element: (run_id, tile_in_run) -> consecutive ids
-        key = run_id * 2 + tile_in_run                 # runs are <= 15 long
-        newt = np.ones_like(key, dtype=bool)
-        newt[:, 1:] = key[:, 1:] != key[:, :-1]
-        tid = np.cumsum(newt, axis=1) - 1              # tile index per type
-        ntile = tid[:, -1] + 1
-        counts[np.arange(nt) * WARP_PARTS + w] = ntile
-        arr = np.full((nt, int(ntile.max()), 16), 0xFF, dtype=np.uint8)
-        arr[:, :, 1] = 0
-        tt, jj = np.nonzero(np.ones_like(gs, dtype=bool))
-        t_ = tid[tt, jj]
-        arr[tt, t_, 0] = gs[tt, jj].astype(np.uint8)      # local group
-        arr[tt, t_, 2 + (pos[tt, jj] % 8)] = sl[tt, jj].astype(np.uint8)
-        np.add.at(arr[:, :, 1], (tt, t_), 1)
-        tiles.append((arr, ntile))
-    # interleave into (type, warp)-major order
-    tile_off = np.zeros(nt * WARP_PARTS + 1, dtype=np.int64)
-    np.cumsum(counts, out=tile_off[1:])
-    out = np.empty((int(tile_off[-1]), 16), dtype=np.uint8)
-    for w, (arr, ntile) in enumerate(tiles):
-        m = np.arange(arr.shape[1])[None, :] < ntile[:, None]
-        t_idx, k_idx = np.nonzero(m)
-        dst = tile_off[t_idx * WARP_PARTS + w] + k_idx
-        out[dst] = arr[t_idx, k_idx]
-    return tile_off, out, node_geom, node_r
 
 
 def _local_group_ids(ap: AccumulationPlan, nn: int) -> np.ndarray:
     """gid[t, node] = sigma group (local to type t) of parent node `node`."""
-    nt = ap.n_types
-    gid = np.empty((nt, nn), dtype=np.int16)
-    local = np.repeat(np.arange(ap.group_sigma.size) -
-                      np.repeat(ap.sig_off[:-1], np.diff(ap.sig_off)),
-                      ap.group_end - ap.group_bounds)
-    gid[np.arange(nt)[:, None], ap.scatter] = local.reshape(nt, nn)
-    return gid
+    return ap.gid
 
 
 def _warp_set_tiles(gid, t, orow, w, per):
@@ -874,16 +860,7 @@ def row_tiles_equal_split(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5,
 def node_tables(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5):
     """Per type and PARENT node: local coordinates in its child segment
     (xs, xt, xp) and the radii (r_parent, r_child)."""
-    nn = p_s * p_a * p_a
-    nt = ap.n_types
-    rows = np.arange(nt)[:, None]
-    geom = np.empty((nt, nn, 3))
-    rad = np.empty((nt, nn, 2))
-    for k, arr in enumerate((ap.xs, ap.xt, ap.xp)):
-        geom[rows, ap.scatter, k] = arr
-    rad[rows, ap.scatter, 0] = ap.r_parent
-    rad[rows, ap.scatter, 1] = ap.r_child
-    return geom, rad
+    return ap.node_geom, ap.node_r
 
 
 # ---------------------------------------------------------------------------

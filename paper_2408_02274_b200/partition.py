@@ -21,7 +21,6 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .octree import accumulation_plan
 
 __all__ = ["RankPart", "level3_partition", "DistributedMullerOperator"]
 
