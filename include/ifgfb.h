@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define IFGFB_ABI_VERSION 2
+#define IFGFB_ABI_VERSION 3
 
 enum {
   IFGFB_OK = 0,
@@ -125,6 +125,13 @@ typedef struct {
   const uint8_t* tiles;      /* n_tiles*16: [local sigma group, n_rows,
                                 slot0..slot7 (position in the warp's set,
                                 0xFF pad), 6 pad] */
+  int32_t geometry_on_device;/* 1: node_geom / node_r unused (may be NULL);
+                                the kernel recomputes each node's local
+                                coordinates and radii from the parent
+                                segment, node and child octant (memory-lean
+                                coarse levels of large configurations) */
+  const uint8_t* type_octant;/* n_types: child octant of each type (used
+                                when geometry_on_device) */
 } ifgfb_accum_desc;
 
 /* ---- surface + operator data (reference SurfaceDiscretization,

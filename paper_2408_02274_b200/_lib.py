@@ -61,7 +61,9 @@ class AccumDesc(C.Structure):
                 ("inst_off", _ip), ("n_instances", C.c_int64),
                 ("inst_type", _ip), ("inst_crow_off", _ip), ("crow", _ip),
                 ("tile_off", _ip), ("n_tiles", C.c_int64),
-                ("tiles", C.POINTER(C.c_uint8))]
+                ("tiles", C.POINTER(C.c_uint8)),
+                ("geometry_on_device", C.c_int32),
+                ("type_octant", C.POINTER(C.c_uint8))]
 
 
 class SurfaceDesc(C.Structure):
@@ -160,7 +162,7 @@ def load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.ifgfb_abi_version() != 2:
+    if lib.ifgfb_abi_version() != 3:
         raise RuntimeError("libifgfb200 ABI version mismatch")
     _lib = lib
     return lib

@@ -174,6 +174,8 @@ struct Level {
   unsigned char* row_order = nullptr;  // parent rows x NN
   unsigned char* row_cuts = nullptr;   // parent rows x (WARP_PARTS+1)
   int max_groups = 0;                  // most child segments of one instance
+  bool otf = false;                    // node geometry computed on the device
+  unsigned char* type_octant = nullptr;  // per type (otf levels)
   uint4* tiles = nullptr;      // 16-byte tile records
   double* node_geom = nullptr; // n_types*NN*3 (parent node order)
   double* node_r = nullptr;    // n_types*NN*2 (r_parent, r_child)

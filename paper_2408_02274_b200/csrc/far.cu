@@ -322,6 +322,73 @@ __global__ void ratio_kernel(int64_t n, const double* __restrict__ node_r,
   }
 }
 
+// Node geometry computed on the device per (instance, node) instead of the
+// per-type tables node_geom / ratio (levels whose type tables do not fit;
+// coarse levels of large configurations have about one type per instance).
+// Continuous values only: the sigma assignment of every node stays the
+// host's (exact, reference expressions); these coordinates differ from the
+// host's by a few ulps (libdevice acos/atan2 vs numpy), far inside the
+// interpolation accuracy.
+struct OtfGeom {
+  const unsigned char* type_octant;   // per type: child octant
+  const int* parent_seg_id;           // per parent row: flat segment id
+  const double* ptabs;                // parent level node tables (see LeafArgs)
+  int pn_s, pn_a;
+  double ph;                          // parent level h
+  const int* child_seg_id;            // per child row: flat segment id
+  int cn_a;
+  double c_delta_s, c_delta_a, child_side;
+  double kr[2], ki[2];
+};
+
+// Parent node `node` of parent segment `pseg` seen from the centre of the
+// child in octant `oct` (reference _AccumType, ifgf.py:686-702; node layout
+// ifgf.py:369-387; cone_coords ifgf.py:305-317; local_coords ifgf.py:361-367)
+// -> local coordinates in child segment `csid` and the re-centering ratio
+// (r_p / r_c) exp(i kappa (r_c - r_p)) (ifgf.py:772-773).
+template <int NK>
+__device__ __forceinline__ void otf_node(const OtfGeom& o, int pseg, int oct, int node,
+                                         int csid, double* geom, double2* ratio) {
+  const int two_na = 2 * o.pn_a;
+  const int i_p = pseg % two_na, rest = pseg / two_na;
+  const int i_t = rest % o.pn_a, i_s = rest / o.pn_a;
+  const int na = node / (PA * PA), nb = (node / PA) % PA, nc = node % PA;
+  const double* s_nodes = o.ptabs;
+  const double* sin_t = s_nodes + o.pn_s * PS;
+  const double* cos_t = sin_t + o.pn_a * PA;
+  const double* sin_p = cos_t + o.pn_a * PA;
+  const double* cos_p = sin_p + two_na * PA;
+  const double rp = o.ph / s_nodes[i_s * PS + na];
+  const double st = sin_t[i_t * PA + nb], ct = cos_t[i_t * PA + nb];
+  const double sp = sin_p[i_p * PA + nc], cp = cos_p[i_p * PA + nc];
+  const double half = 0.5 * o.child_side;
+  const double x = ((oct >> 2) & 1 ? -half : half) + rp * (st * cp);
+  const double y = ((oct >> 1) & 1 ? -half : half) + rp * (st * sp);
+  const double z = (oct & 1 ? -half : half) + rp * ct;
+  const double rc = sqrt((x * x + y * y) + z * z);
+  const double sv = (0.8660254037844386 * o.child_side) / rc;
+  const double th = acos(fmin(fmax(z / rc, -1.0), 1.0));
+  double ph = atan2(y, x);
+  const int two_cna = 2 * o.cn_a;
+  const int j_p = csid % two_cna, crest = csid / two_cna;
+  const int j_t = crest % o.cn_a, j_s = crest / o.cn_a;
+  // phi in [0, 2 pi) as np.mod does; across the seam take the branch of the
+  // host-assigned interval
+  if (ph < 0.0) ph += 2.0 * M_PI;
+  const double lp = ph / o.c_delta_a - j_p;
+  if (lp > o.cn_a) ph -= 2.0 * M_PI;
+  else if (lp < -o.cn_a) ph += 2.0 * M_PI;
+  geom[0] = 2.0 * (sv / o.c_delta_s - j_s) - 1.0;
+  geom[1] = 2.0 * (th / o.c_delta_a - j_t) - 1.0;
+  geom[2] = 2.0 * (ph / o.c_delta_a - j_p) - 1.0;
+  const double q = rp / rc;
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    const double2 e = cexp_ikx(o.kr[k], o.ki[k], rc - rp);
+    ratio[k] = make_double2(q * e.x, q * e.y);
+  }
+}
+
 struct AccArgs {
   const int* inst_off; const int* inst_type; const int* inst_crow_off;
   const int* crow; const int* tile_off; const uint4* tiles;
@@ -331,6 +398,7 @@ struct AccArgs {
   int row0;              // first parent row handled (partition)
   int row_end;           // one past the last parent row handled
   int rows_per_cta;      // consecutive parent rows per CTA
+  OtfGeom o;             // OTF instantiation only
 };
 
 // cp.async (LDGSTS) helpers: global -> shared without a register round trip
@@ -393,11 +461,11 @@ __device__ __forceinline__ int tile_slot(const uint4& tl, int grp, bool& valid) 
 // WIDE: some instance of the level has more than MAX_GROUPS child segments
 // (coarse levels of large configurations); the extra rows are read from
 // global memory.  Kept out of the common instantiation (costs ~2%).
-template <int NK, bool WIDE>
+template <int NK, bool WIDE, bool OTF>
 __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
   __shared__ double2 acc[NN * NCOL];                        // 19.2 KB
   __shared__ RowStage stage[2];                             // 11.8 KB
-  __shared__ unsigned char ord[NN], inv[NN];
+  __shared__ unsigned char ord[NN], inv[NN], sgrp[NN];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane >> 2, tig = lane & 3;
   const int pbeg = a.row0 + blockIdx.x * a.rows_per_cta;
@@ -427,17 +495,19 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
     const int cs = __shfl_sync(0xffffffffu, my_co, j);
     const int ce = __shfl_sync(0xffffffffu, my_co, j + 1);
     const size_t tb = (size_t)t * NN;
-    for (int e = lane; e < nset * 3; e += 32)
-      cp_async8(&S.geom[3 * pos0 + e], a.node_geom + (tb + word[e / 3]) * 3 + e % 3);
-    for (int e = lane; e < nset * NK; e += 32)
-      cp_async16(&S.ratio[NK * pos0 + e], a.ratio + (tb + word[e / NK]) * NK + e % NK);
+    if (!OTF) {
+      for (int e = lane; e < nset * 3; e += 32)
+        cp_async8(&S.geom[3 * pos0 + e], a.node_geom + (tb + word[e / 3]) * 3 + e % 3);
+      for (int e = lane; e < nset * NK; e += 32)
+        cp_async16(&S.ratio[NK * pos0 + e], a.ratio + (tb + word[e / NK]) * NK + e % NK);
+    }
     if (lane < ke - ks) cp_async16(&S.tiles[pos0 + lane], a.tiles + ks + lane);
     if (lane < min(ce - cs, MAX_GROUPS)) cp_async4(&S.crow[warp][lane], a.crow + cs + lane);
     cp_async_commit();
   };
   if (ni > 0) stage_inst(0, stage[0]);
   for (int j = 0; j < ni; ++j) {
-    const RowStage& S = stage[j & 1];
+    RowStage& S = stage[j & 1];
     if (j + 1 < ni) {
       stage_inst(j + 1, stage[(j + 1) & 1]);
       cp_async_wait<1>();
@@ -447,6 +517,27 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
     __syncwarp();
     const int ntile = __shfl_sync(0xffffffffu, my_ke - my_ks, j);
     const int* crow_g = a.crow + __shfl_sync(0xffffffffu, my_co, j);
+    if (OTF) {   // slot -> sigma group from the tile records, then geometry
+      for (int e = lane; e < ntile * 8; e += 32) {
+        const uint4 tl = S.tiles[pos0 + (e >> 3)];
+        const int r = e & 7;
+        if (r < (int)((tl.x >> 8) & 0xff)) {
+          const int byte = 2 + r;
+          const unsigned w = byte < 4 ? tl.x : byte < 8 ? tl.y : tl.z;
+          sgrp[pos0 + ((w >> (8 * (byte & 3))) & 0xff)] = (unsigned char)(tl.x & 0xff);
+        }
+      }
+      __syncwarp();
+      const int pseg = a.o.parent_seg_id[p];
+      const int oct = a.o.type_octant[__shfl_sync(0xffffffffu, my_t, j)];
+      for (int e = lane; e < nset; e += 32) {
+        const int g = sgrp[pos0 + e];
+        const int cr = (!WIDE || g < MAX_GROUPS) ? S.crow[warp][g] : crow_g[g];
+        otf_node<NK>(a.o, pseg, oct, word[e], a.o.child_seg_id[cr], &S.geom[(pos0 + e) * 3],
+                     &S.ratio[(pos0 + e) * NK]);
+      }
+      __syncwarp();
+    }
     for (int k = 0; k < ntile; ++k) {
       const uint4 tl = S.tiles[pos0 + k];
       bool valid;
@@ -621,7 +712,7 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
     // re-centering ratios, once per apply and level (kappa dependent)
     for (int d = 4; d <= D; ++d) {
       Level& L = p.levels[d];
-      if (!L.has_accum) continue;
+      if (!L.has_accum || L.otf) continue;
       const int64_t nr = L.n_types * NN;
       const int tk = p.timer.begin(K_OTHER, st);
       ratio_kernel<NK><<<(unsigned)((nr + 255) / 256), 256, 0, st>>>(
@@ -682,10 +773,16 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
             const int nrows = U.seg_hi() - U.seg_lo();
             const int tk = p.timer.begin(K_ACCUM, st);
             const int grid = (nrows + IFGFB_ACC_ROWS - 1) / IFGFB_ACC_ROWS;
-            if (L.max_groups > MAX_GROUPS)
-              accum_kernel<NK, true><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
-            else
-              accum_kernel<NK, false><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
+            const bool wide = L.max_groups > MAX_GROUPS;
+            if (L.otf) {
+              aa.o = OtfGeom{L.type_octant, U.seg_id, U.tabs, U.n_s, U.n_a, U.h, L.seg_id,
+                             L.n_a, L.delta_s, L.delta_a, L.side, {kr[0], kr[1]}, {ki[0], ki[1]}};
+              if (wide) accum_kernel<NK, true, true><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
+              else accum_kernel<NK, false, true><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
+            } else {
+              if (wide) accum_kernel<NK, true, false><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
+              else accum_kernel<NK, false, false><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
+            }
             p.timer.end(tk, st);
             ++launches;
           }

@@ -246,9 +246,17 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
       CHECK_ARG(c[w + 1] > c[w] && c[w + 1] - c[w] <= MAX_SET, "row_cuts: warp set size out of 1..23");
   }
   RC(dev_upload(p, &L.row_cuts, a->row_cuts, (size_t)a->n_parent_rows * (WARP_PARTS + 1)));
-  RC(dev_upload(p, &L.node_geom, a->node_geom, (size_t)nt * NN * 3));
-  RC(dev_upload(p, &L.node_r, a->node_r, (size_t)nt * NN * 2));
-  RC(dev_alloc(p, &L.ratio, (size_t)nt * NN * 4));
+  L.otf = a->geometry_on_device != 0;
+  if (L.otf) {
+    CHECK_ARG(a->type_octant != nullptr, "geometry_on_device needs type_octant");
+    for (int64_t t = 0; t < nt; ++t) CHECK_ARG(a->type_octant[t] < 8, "type_octant out of range");
+    RC(dev_upload(p, &L.type_octant, a->type_octant, (size_t)nt));
+  } else {
+    CHECK_ARG(a->node_geom != nullptr && a->node_r != nullptr, "node_geom / node_r missing");
+    RC(dev_upload(p, &L.node_geom, a->node_geom, (size_t)nt * NN * 3));
+    RC(dev_upload(p, &L.node_r, a->node_r, (size_t)nt * NN * 2));
+    RC(dev_alloc(p, &L.ratio, (size_t)nt * NN * 4));
+  }
   if (!to_i32(a->inst_off, a->n_parent_rows + 1, tmp, "inst_off")) return IFGFB_ERR_ARG;
   RC(dev_upload(p, &L.inst_off, tmp.data(), tmp.size()));
   L.n_instances = a->n_instances;

@@ -32,7 +32,8 @@ class FarFieldPlan:
 
     def __init__(self, tree, hier, displaced_normals=None,
                  displaced_step: float = 1e-6, surface=None, near=None,
-                 kappas=None, trim_host: bool = True):
+                 kappas=None, trim_host: bool = True,
+                 geometry_on_device: str | None = None):
         lib = _lib.load()
         if not torch.cuda.is_available():
             raise RuntimeError("CUDA device required (no CPU fallback)")
@@ -62,8 +63,9 @@ class FarFieldPlan:
             for d in range(3, self.depth + 1):
                 self._add_level(lib, d)
                 self._keep = []
+            self.otf_levels = self._choose_otf(geometry_on_device)
             for d in range(4, self.depth + 1):
-                self._add_accum(lib, d)
+                self._add_accum(lib, d, d in self.otf_levels)
                 self._keep = []
             for d in range(3, self.depth + 1):
                 self._add_emission(lib, d, disp_t)
@@ -115,14 +117,54 @@ class FarFieldPlan:
                    f"ifgfb_plan_add_level({d})")
         self.stats["levels"].setdefault(d, {})["segments"] = int(cl.n_segments)
 
-    def _add_accum(self, lib, d):
+    # bytes of device plan per propagation type (node_geom, node_r, ratio)
+    TYPE_TABLE_BYTES = 75 * (3 + 2 + 4) * 8
+
+    def _choose_otf(self, policy):
+        """Levels whose node geometry is computed on the device instead of
+        uploaded as per-type tables.  policy "none" / "all" / "auto" (default,
+        env IFGFB_GEOM_ON_DEVICE): auto keeps the tables unless the estimated
+        device plan exceeds 55% of the device memory, then moves levels to
+        on-device geometry, most types per instance first (there the tables
+        save the least work)."""
+        import os
+        policy = policy or os.environ.get("IFGFB_GEOM_ON_DEVICE", "auto")
+        levels = list(range(4, self.depth + 1))
+        if policy == "none":
+            return set()
+        if policy == "all":
+            return set(levels)
+        if policy != "auto":
+            raise ValueError(f"geometry_on_device: unknown policy {policy!r}")
+        info = {}
+        fixed = 0
+        for d in levels:
+            ap = accumulation_plan(self.tree, self.hier, d)
+            info[d] = (ap.n_types * self.TYPE_TABLE_BYTES, ap.n_types / max(1, ap.n_instances))
+            fixed += ap.n_instances * (12 * 16 + 16) + int(ap.inst_crow_off[-1]) * 4
+        pairs = [self.hier.level(d).cpt_idx.size for d in range(3, self.depth + 1)]
+        fixed += sum(pairs) * 80 + max(pairs, default=0) * 2 * 16 * 16
+        budget = 0.55 * torch.cuda.get_device_properties(
+            torch.cuda.current_device()).total_memory
+        tables = sum(b for b, _ in info.values())
+        chosen = set()
+        for d in sorted(levels, key=lambda d: -info[d][1]):
+            if fixed + tables <= budget:
+                break
+            chosen.add(d)
+            tables -= info[d][0]
+        return chosen
+
+    def _add_accum(self, lib, d, otf=False):
         ap = accumulation_plan(self.tree, self.hier, d)
         # crow rows are reproduced exactly as the reference's searchsorted
         # picks them (ifgf.py:743-746), including any inexact hit.
         row_order, row_cuts, tile_off, tiles = row_tiles(ap)
-        node_geom, node_r = node_tables(ap)
+        node_geom, node_r = (None, None) if otf else node_tables(ap)
         u8 = __import__("ctypes").POINTER(__import__("ctypes").c_uint8)
-        a = dict(ng=_c(node_geom, np.float64), nr=_c(node_r, np.float64),
+        a = dict(ng=None if otf else _c(node_geom, np.float64),
+                 nr=None if otf else _c(node_r, np.float64),
+                 oc=np.ascontiguousarray(ap.type_octant, dtype=np.uint8),
                  ro=np.ascontiguousarray(row_order),
                  rc=np.ascontiguousarray(row_cuts), to=_c(tile_off, np.int64),
                  tl=np.ascontiguousarray(tiles),
@@ -135,12 +177,14 @@ class FarFieldPlan:
             a["rc"].ctypes.data_as(u8),
             _lib.iptr(a["io"]), ap.n_instances, _lib.iptr(a["it"]),
             _lib.iptr(a["ico"]), _lib.iptr(a["cr"]), _lib.iptr(a["to"]),
-            tiles.shape[0], a["tl"].ctypes.data_as(u8))
+            tiles.shape[0], a["tl"].ctypes.data_as(u8), int(otf),
+            a["oc"].ctypes.data_as(u8))
         _lib.check(lib.ifgfb_plan_add_accum(self._h, desc),
                    f"ifgfb_plan_add_accum({d})")
         st = self.stats["levels"].setdefault(d, {})
         st.update(types=int(ap.n_types), instances=int(ap.n_instances),
-                  crow_misses=int(ap.crow_misses), tiles=int(tiles.shape[0]))
+                  crow_misses=int(ap.crow_misses), tiles=int(tiles.shape[0]),
+                  geometry_on_device=bool(otf))
 
     def _add_emission(self, lib, d, disp_t):
         ep = emission_plan(self.tree, self.hier, d, disp_t)

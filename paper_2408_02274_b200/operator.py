@@ -236,7 +236,8 @@ class MullerOperator:
 
     def __init__(self, disc, materials, smap, moments, corrections,
                  config: OperatorConfig = OperatorConfig(), tree=None,
-                 hierarchy=None, stream_parts=None):
+                 hierarchy=None, stream_parts=None,
+                 geometry_on_device: str | None = None):
         self.disc = disc
         self.materials = materials
         self.smap = smap
@@ -254,7 +255,8 @@ class MullerOperator:
                                            corr_ell, corr_src, keep)
         self.plan = FarFieldPlan(tree, hierarchy, disc.normals,
                                  config.fd_step, surface=surf, near=near,
-                                 kappas=materials.kappas)
+                                 kappas=materials.kappas,
+                                 geometry_on_device=geometry_on_device)
         # memory: stream the upward pass over groups of level-3 subtrees when
         # two full coefficient levels do not fit (None = automatic)
         if stream_parts is None:

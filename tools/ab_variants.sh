@@ -4,5 +4,5 @@ for lib in variants/*.so; do
   IFGFB_LIB=$PWD/$lib python bench.py --n-refine ${1:-4} --steps 10 --warmup 3 --no-cpu-baseline --no-gmres > gpurun_out/ab.json 2> gpurun_out/ab.err || { echo "$lib FAILED"; tail -3 gpurun_out/ab.err; continue; }
   python -c "
 import json; d=json.load(open('gpurun_out/ab.json')); r=d['roofline']; k=d['kernels']
-print('%-28s ms %.3f prop %.3f leaf %.3f emit %.3f near %.3f ms %.2f TF frac %.3f' % ('$lib', d['ms_per_step'], k['propagate']['ms_per_step'], k['leaf']['ms_per_step'], k['emit']['ms_per_step'], k['near']['ms_per_step'], r['achieved'], r['frac']))"
+print('%-28s ms %.3f prop %.3f leaf %.3f emit %.3f near %.3f ms %.2f TF frac %.3f' % ('$lib', d['ms_per_step'], k['propagate']['ms_per_step'], k['leaf']['ms_per_step'], k.get('emit', {}).get('ms_per_step', 0.0), k['near']['ms_per_step'], r['achieved'], r['frac']))"
 done

@@ -35,9 +35,21 @@ t = time.time()
 mom = nearfield.compute_moments(disc, smap, nearfield.SingularQuadratureConfig(), mats.kappas)
 mark("moments", t)
 t = time.time(); cp = nearfield.correction_pairs(disc, tree, smap); mark("corrections", t)
+dev = 0
 for d in range(4, tree.depth + 1):
     t = time.time(); ap = octree.accumulation_plan(tree, hier, d)
     mark(f"accum plan {d} ({ap.n_types} types)", t)
+    ng = int(ap.inst_crow_off[-1])
+    est = ap.n_types * 75 * 72 + ap.n_instances * (12 * 16 + 4 * 4) + ng * 4 + \
+        hier.level(d - 1).n_segments * (75 + 6)
+    dev += est
+    print(f"   level {d}: types {ap.n_types} instances {ap.n_instances} groups {ng}"
+          f" types/inst {ap.n_types / max(1, ap.n_instances):.2f}  device est {est / 1e9:.1f} GB",
+          flush=True)
+pairs = [hier.level(d).cpt_idx.size for d in range(3, tree.depth + 1)]
+print(f"emission pairs per level {pairs}; device est {sum(pairs) * 72 / 1e9:.1f} GB + partial "
+      f"{max(pairs) * 512 / 1e9:.1f} GB; segments {[hier.level(d).n_segments for d in range(3, tree.depth + 1)]}")
+print(f"propagation device estimate {dev / 1e9:.1f} GB", flush=True)
 if "--op" in sys.argv:
     from paper_2408_02274_b200.operator import MullerOperator
     t = time.time()
