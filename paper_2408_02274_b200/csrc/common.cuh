@@ -15,13 +15,18 @@ constexpr int NN = PS * PA * PA;  // 75 nodes per cone segment
 constexpr int NCOL = 16;       // complex columns carried per traversal
 constexpr int NRCOL = 2 * NCOL;   // 32 real columns
 // Coefficients of one segment are stored in DMMA B-fragment order:
-// [ks 0..19][half 0..1][lane 0..31][2] doubles, column tile nt = 2*half + j,
-// ks = 5q + c covering the coefficient rows i = (4q + (lane&3))*5 + c (zero
-// when 4q + (lane&3) >= 15), column = 8*nt + (lane>>2) of the 32 real
-// columns (re/im of 16 complex).  A k-step's fragments are two fully
-// contiguous 512-byte warp loads (16 bytes per lane).
-constexpr int KSTEPS = 20;
-constexpr int SEG_DOUBLES = KSTEPS * 32 * 4;  // 2560 doubles = 20 KB per segment
+// [ks 0..18][half 0..1][lane 0..31][2] doubles, column tile nt = 2*half + j,
+// column = 8*nt + (lane>>2) of the 32 real columns (re/im of 16 complex).
+// K dimension: the 75 coefficients i = (a*PA + b)*PA + c = ab*PA + c packed
+// into 19 k-steps of 4 (76 rows, one zero row), tig = lane&3:
+//   ks = 5q + c (q < 3, c < 5): ab = 4q + tig, this c;
+//   ks = 15 + s (s < 4):        (ab, c) = (12 + tig, s) for tig < 3,
+//                               (12 + s, 4) for tig = 3 (s = 3: zero row).
+// A k-step's fragments are two fully contiguous 512-byte warp loads (16
+// bytes per lane).
+constexpr int KSTEPS = 19;
+constexpr int KMAIN = 15;                     // k-steps of the (q, c) block
+constexpr int SEG_DOUBLES = KSTEPS * 32 * 4;  // 2432 doubles = 19 KB per segment
 constexpr int WARP_PARTS = 5;                 // propagation: node owners per CTA
 constexpr int PART_NODES = NN / WARP_PARTS;   // 15 parent nodes per warp (mean)
 constexpr int MAX_SET = 23;                   // largest warp-owned node set

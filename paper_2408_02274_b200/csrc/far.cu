@@ -6,7 +6,7 @@
 // Reference: ifgf.py:788-882 (propagate_and_emit), ifgf.py:535-554 (K2),
 // ifgf.py:502-522 (K3), ifgf.py:752-785 (K4), ifgf.py:630-673 (K5).
 //
-// Data layout in HBM: per level one coefficient array of 20 KB segments in
+// Data layout in HBM: per level one coefficient array of 19 KB segments in
 // DMMA fragment order (see SEG_DOUBLES), holding the rows this rank owns
 // (all rows without a partition; buffers are addressed through a base
 // pointer shifted by the first owned row); two arrays are live (child level
@@ -126,8 +126,16 @@ __device__ __forceinline__ void store_segment(double* dst, const double2* V,
                                               int nthr) {
   for (int idx = tid; idx < SEG_DOUBLES; idx += nthr) {
     const int ks = idx >> 7, lane = (idx >> 1) & 31, nt = ((idx >> 5) & 2) | (idx & 1);
-    const int q = ks / PA, c = ks - PA * q;
-    const int ab = 4 * q + (lane & 3);
+    int ab, c;
+    if (ks < KMAIN) {
+      const int q = ks / PA;
+      c = ks - PA * q;
+      ab = 4 * q + (lane & 3);
+    } else {
+      const int t = lane & 3, st = ks - KMAIN;
+      ab = t < 3 ? 12 + t : (st < 3 ? 12 + st : PS * PA);   // (s=3, tig=3): zero row
+      c = t < 3 ? st : PA - 1;
+    }
     double v = 0.0;
     if (ab < PS * PA) {
       const int col = 8 * nt + (lane >> 2);
@@ -229,13 +237,17 @@ __global__ void __launch_bounds__(leaf_threads<NK>(), IFGFB_LEAF_MINB) leaf_kern
 
 // ------------------------------------------------------- DMMA helpers ----
 // Tensor-product Chebyshev basis of one interpolation point, consumed as the
-// A operand of m8n8k4 f64 MMAs.  The K dimension (75 coefficients) is padded
-// to 80 = 16 (a,b) pairs x 5 c values; k-step ks = 5q + c covers the
-// coefficients i = (4q + tig)*5 + c, tig = lane & 3.  A thread then needs
-// only tst[q] = T_a(xs) T_b(xt) for ab = 4q + tig and T_c(xp).
+// A operand of m8n8k4 f64 MMAs (K = 75 coefficients in 19 k-steps, see
+// SEG_DOUBLES).  Main block, k-step 5q + c (q < 3): coefficient
+// (ab = 4q + tig, c), A value tst[q] * tp[c] with tst[q] = T_a(xs) T_b(xt).
+// Tail, k-step 15 + s: tig < 3 holds (ab, c) = (12 + tig, s), tig = 3 holds
+// (12 + s, 4) (s < 3; s = 3 is the zero row); u = T_2(xs) T_{2+min(tig,2)}(xt)
+// and the tig = 3 lanes take T_{12+s} from lane s of their group by shuffle.
+// Products in numpy's order (T_a T_b) T_c.
 struct BasisA {
-  double tst[4];
+  double tst[3];
   double tp[PA];
+  double u;
 };
 
 template <bool EXACT>
@@ -258,48 +270,60 @@ __device__ __forceinline__ BasisA make_basis(double xs, double xt, double xp,
     }
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 3; ++q) {
     const int ab = 4 * q + tig;
     const int ia = ab / PA, ib = ab - PA * ia;
     const double va = (ia == 0) ? ts[0] : (ia == 1) ? ts[1] : ts[2];
     const double vb = (ib == 0) ? tt[0] : (ib == 1) ? tt[1] : (ib == 2) ? tt[2]
                     : (ib == 3) ? tt[3] : tt[4];
-    B.tst[q] = (ab < PS * PA) ? (EXACT ? mul_rn(va, vb) : va * vb) : 0.0;
+    B.tst[q] = EXACT ? mul_rn(va, vb) : va * vb;
   }
+  const double vu = (tig == 0) ? tt[2] : (tig == 1) ? tt[3] : tt[4];
+  B.u = EXACT ? mul_rn(ts[2], vu) : ts[2] * vu;
   return B;
 }
 
-// acc[nt] (+)= sum_i basis_i * C[i][8nt + grp]: 20 k-steps x 4 column tiles
+// acc[nt] (+)= sum_i basis_i * C[i][8nt + grp]: 19 k-steps x 4 column tiles
 // of DMMA; the B fragments of a k-step are two contiguous 512-byte warp
 // loads from the fragment-ordered segment.
 #ifndef IFGFB_ACC_QUNROLL
-#define IFGFB_ACC_QUNROLL 4
+#define IFGFB_ACC_QUNROLL 3
 #endif
 #ifndef IFGFB_ACC_MINB
-#define IFGFB_ACC_MINB 5
+#define IFGFB_ACC_MINB 6
 #endif
 #ifndef IFGFB_ACC_ROWS
 #define IFGFB_ACC_ROWS 1
 #endif
 
-template <bool EXACT, int QU = 4>
+__device__ __forceinline__ void dmma4(double (&c0)[4], double (&c1)[4], double av,
+                                      const double2* F, int ks) {
+  const double2 b01 = F[ks * 64], b23 = F[ks * 64 + 32];
+  dmma(c0[0], c1[0], av, b01.x);
+  dmma(c0[1], c1[1], av, b01.y);
+  dmma(c0[2], c1[2], av, b23.x);
+  dmma(c0[3], c1[3], av, b23.y);
+}
+
+template <bool EXACT, int QU = 3>
 __device__ __forceinline__ void basis_times_block(const BasisA& B,
                                                   const double* __restrict__ C,
                                                   int lane, double (&c0)[4],
                                                   double (&c1)[4]) {
   const double2* F = reinterpret_cast<const double2*>(C) + lane;
 #pragma unroll QU
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 3; ++q) {
 #pragma unroll
-    for (int c = 0; c < PA; ++c) {
-      const double2 b01 = F[(5 * q + c) * 64], b23 = F[(5 * q + c) * 64 + 32];
-      const double4 b = make_double4(b01.x, b01.y, b23.x, b23.y);
-      const double av = EXACT ? mul_rn(B.tst[q], B.tp[c]) : B.tst[q] * B.tp[c];
-      dmma(c0[0], c1[0], av, b.x);
-      dmma(c0[1], c1[1], av, b.y);
-      dmma(c0[2], c1[2], av, b.z);
-      dmma(c0[3], c1[3], av, b.w);
-    }
+    for (int c = 0; c < PA; ++c)
+      dmma4(c0, c1, EXACT ? mul_rn(B.tst[q], B.tp[c]) : B.tst[q] * B.tp[c], F, 5 * q + c);
+  }
+  const int tig = lane & 3;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const double us = __shfl_sync(0xffffffffu, B.u, (lane & ~3) | (s < 3 ? s : 0));
+    const double x = tig < 3 ? B.u : us, y = tig < 3 ? B.tp[s] : B.tp[PA - 1];
+    const double av = (tig < 3 || s < 3) ? (EXACT ? mul_rn(x, y) : x * y) : 0.0;
+    dmma4(c0, c1, av, F, KMAIN + s);
   }
 }
 

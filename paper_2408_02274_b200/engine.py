@@ -210,7 +210,7 @@ class FarFieldPlan:
         """Bytes of the two coefficient buffers without streaming."""
         mx = max((self.hier.level(d).n_segments
                   for d in range(3, self.depth + 1)), default=0)
-        return 2 * mx * 2560 * 8
+        return 2 * mx * 2432 * 8   # 19 KB per segment (csrc/common.cuh SEG_DOUBLES)
 
     def set_streaming(self, n_parts: int) -> None:
         """Run the upward pass as n_parts sequential passes over Morton
