@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--n-refine", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--device-moments", action="store_true",
+                    help="singular moments from the plan-time GPU kernel (large surfaces)")
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--max-rss-gb", type=float, default=0.0,
                     help="abort (kill this process) if host RSS exceeds this")
@@ -80,14 +82,17 @@ def workload(n_refine):
     return disc, mats, y, name
 
 
-def plan_inputs(disc, mats):
+def plan_inputs(disc, mats, device_moments=False):
     from paper_2408_02274_b200 import nearfield, octree
     kmax = max(abs(mats.kappa_e), abs(mats.kappa_i))
     tree = octree.build_box_tree(disc.points, kmax)
     hier = octree.build_cone_hierarchy(tree)
     smap = nearfield.classify_targets(disc)
-    mom = nearfield.compute_moments(disc, smap, nearfield.SingularQuadratureConfig(),
-                                    mats.kappas)
+    cfg = nearfield.SingularQuadratureConfig()
+    if device_moments:
+        mom = nearfield.compute_moments_device(disc, smap, cfg, mats.kappas, groups=False)
+    else:
+        mom = nearfield.compute_moments(disc, smap, cfg, mats.kappas)
     cp = nearfield.correction_pairs(disc, tree, smap)
     return tree, hier, smap, mom, cp
 
@@ -242,7 +247,7 @@ def run_b200(args):
         dist.barrier()
     disc, mats, y, name = workload(args.n_refine)
     t0 = time.time()
-    inputs = plan_inputs(disc, mats)
+    inputs = plan_inputs(disc, mats, args.device_moments)
     tree, hier, smap, mom, cp = inputs
     op = MullerOperator(disc, mats, smap, mom, (cp.ell_idx, cp.src_idx),
                         tree=tree, hierarchy=hier)
@@ -372,7 +377,7 @@ def run_b200(args):
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and not args.device_moments:
         line["cpu_baseline"] = cpu_baseline(disc, mats, y, inputs, 15.0, counts)
     if world == 1 and not args.no_gmres:
         line["gmres"] = gmres_cfg1()

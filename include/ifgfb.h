@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define IFGFB_ABI_VERSION 3
+#define IFGFB_ABI_VERSION 4
 
 enum {
   IFGFB_OK = 0,
@@ -193,6 +193,31 @@ int ifgfb_row_tiles_fill(int64_t n_rows, const int64_t* inst_off,
                          const uint8_t* group_id, const uint8_t* row_order,
                          const uint8_t* row_cuts, const int64_t* tile_off,
                          uint8_t* tiles, int32_t n_threads);
+
+/* Plan-time singular moments on the device (reference quadrature.py:271-331,
+ * compute_moments; graded clustered grid quadrature.py:163-228).  For each
+ * (target, singular patch) pair i: target point / normal (3 doubles each),
+ * patch index, closest (u0, v0).  patch_coeffs holds per patch 9 tensor
+ * Chebyshev coefficient blocks of n_p x n_p (position x,y,z; d/du x,y,z;
+ * d/dv x,y,z; reference Patch.coeffs / coeffs_du / coeffs_dv).  base /
+ * weights: the n_beta Chebyshev nodes and Fejer weights; grading: the map
+ * order d.  out (HOST, n_pairs*4*n_c*n_c complex) receives per pair
+ * beta_s[k=0], beta_s[k=1], beta_d[k=0], beta_d[k=1] (n_c x n_c each, row
+ * m = u-degree) -- the layout of ifgfb_near_desc.moments. */
+typedef struct {
+  int64_t n_pairs;
+  const double* target_xyz;     /* n_pairs*3 */
+  const double* target_nrm;     /* n_pairs*3 */
+  const int32_t* patch;         /* n_pairs */
+  const double* uv;             /* n_pairs*2 */
+  int32_t n_patches, n_p;
+  const double* patch_coeffs;   /* n_patches*9*n_p*n_p */
+  int32_t n_c, n_beta, grading;
+  const double* base;           /* n_beta */
+  const double* weights;        /* n_beta */
+  const double* kappas;         /* 2 complex */
+} ifgfb_moment_desc;
+int ifgfb_singular_moments(const ifgfb_moment_desc* desc, double* out);
 
 int ifgfb_plan_create(const ifgfb_tree_desc* tree, ifgfb_plan** out);
 int ifgfb_plan_add_level(ifgfb_plan* plan, const ifgfb_level_desc* lvl);

@@ -94,10 +94,20 @@ class PartitionDesc(C.Structure):
                 ("target_lo", C.c_int64), ("target_hi", C.c_int64)]
 
 
+class MomentDesc(C.Structure):
+    _fields_ = [("n_pairs", C.c_int64), ("target_xyz", _dp), ("target_nrm", _dp),
+                ("patch", C.POINTER(C.c_int32)), ("uv", _dp),
+                ("n_patches", C.c_int32), ("n_p", C.c_int32),
+                ("patch_coeffs", _dp), ("n_c", C.c_int32),
+                ("n_beta", C.c_int32), ("grading", C.c_int32),
+                ("base", _dp), ("weights", _dp), ("kappas", _dp)]
+
+
 EXPORTS = {
     "ifgfb_abi_version": ([], C.c_int),
     "ifgfb_last_error": ([], C.c_char_p),
     "ifgfb_device_info": ([C.c_char_p, C.c_size_t], C.c_int),
+    "ifgfb_singular_moments": ([C.POINTER(MomentDesc), _dp], C.c_int),
     "ifgfb_plan_create": ([C.POINTER(TreeDesc), C.POINTER(C.c_void_p)], C.c_int),
     "ifgfb_plan_add_level": ([C.c_void_p, C.POINTER(LevelDesc)], C.c_int),
     "ifgfb_plan_add_accum": ([C.c_void_p, C.POINTER(AccumDesc)], C.c_int),
@@ -162,7 +172,7 @@ def load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.ifgfb_abi_version() != 3:
+    if lib.ifgfb_abi_version() != 4:
         raise RuntimeError("libifgfb200 ABI version mismatch")
     _lib = lib
     return lib

@@ -9,6 +9,8 @@ runs standalone:
 * ``classify_targets``              -- reference ``quadrature.py:97-156``
 * ``graded_map`` / ``clustered_nodes`` -- reference ``quadrature.py:163-228``
 * ``compute_moments``               -- reference ``quadrature.py:271-331``
+* ``compute_moments_device``       -- the same moments from the sm_100a
+  kernel ``csrc/moments.cu`` (C ABI ``ifgfb_singular_moments``)
 * ``correction_pairs``              -- reference ``quadrature.py:490-525``
   (only the (target, source) index lists; the device recomputes the kernel
   values, so no CSR values are stored)
@@ -26,7 +28,8 @@ from .surface import SurfaceDiscretization, closest_point_batch
 
 __all__ = ["SingularQuadratureConfig", "SingularityMap", "MomentGroup",
            "SingularMomentTable", "classify_targets", "graded_map",
-           "clustered_nodes", "compute_moments", "correction_pairs"]
+           "clustered_nodes", "compute_moments", "compute_moments_device",
+           "correction_pairs"]
 
 
 @dataclass(frozen=True)
@@ -292,6 +295,71 @@ def compute_moments(disc: SurfaceDiscretization, smap: SingularityMap,
 
     for p, grp in _pool().map(one_patch, np.unique(smap.patch_ids)):
         table.groups[p] = grp
+    return table
+
+
+def compute_moments_device(disc: SurfaceDiscretization, smap: SingularityMap,
+                           config: SingularQuadratureConfig, kappas,
+                           target_points=None, target_normals=None,
+                           groups: bool = True):
+    """``compute_moments`` on the GPU (csrc/moments.cu): same table, the
+    pairs' moments computed by one CTA each.  beta_s agrees with the host
+    restatement to rounding; beta_d to the ~1e-7 conditioning of its
+    integrand at the clustered nodes (tests/test_gpu_moments.py).
+
+    groups=False skips the per-patch regrouping: the table then carries the
+    blocks in the singularity map's CSR order (``csr_blocks``, n_mom x 4 x
+    n_c^2, target-major with ascending patch ids -- the order the near-field
+    plan consumes) and an empty ``groups``."""
+    import ctypes
+
+    from . import _lib
+    kappas = tuple(kappas)
+    if len(kappas) != 2:
+        raise ValueError("compute_moments_device: two wavenumbers")
+    n_c = disc.n_c
+    nb = config.resolve_n_beta(n_c)
+    pts = disc.points if target_points is None else target_points
+    nrms = disc.normals if target_normals is None else target_normals
+    n_pairs = smap.patch_ids.size
+    tg = np.repeat(np.arange(smap.n_targets, dtype=np.int64),
+                   np.diff(smap.offsets))
+    npg = disc.patches[0].n
+    if any(p.n != npg for p in disc.patches):
+        raise ValueError("compute_moments_device: patches of mixed order")
+    cf = np.ascontiguousarray(np.stack(
+        [np.concatenate([p.coeffs, p.coeffs_du, p.coeffs_dv]) for p in disc.patches]),
+        dtype=np.float64)
+    txyz = np.ascontiguousarray(pts[tg], dtype=np.float64)
+    tnrm = np.ascontiguousarray(nrms[tg], dtype=np.float64)
+    pid = np.ascontiguousarray(smap.patch_ids, dtype=np.int32)
+    uv = np.ascontiguousarray(smap.closest_uv, dtype=np.float64)
+    base = np.ascontiguousarray(cheb.nodes(nb), dtype=np.float64)
+    wb = np.ascontiguousarray(cheb.fejer(nb), dtype=np.float64)
+    kap = np.array([complex(kappas[0]).real, complex(kappas[0]).imag,
+                    complex(kappas[1]).real, complex(kappas[1]).imag])
+    out = np.empty((n_pairs, 4, n_c, n_c), dtype=np.complex128)
+    dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    desc = _lib.MomentDesc(n_pairs, dp(txyz), dp(tnrm),
+                           pid.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                           dp(uv), disc.n_patches, npg, dp(cf), n_c, nb,
+                           int(config.d), dp(base), dp(wb), dp(kap))
+    lib = _lib.load()
+    _lib.check(lib.ifgfb_singular_moments(ctypes.byref(desc), dp(out.view(np.float64))),
+               "ifgfb_singular_moments")
+    table = SingularMomentTable(n_c, kappas)
+    if not groups:
+        table.csr_blocks = out.reshape(n_pairs, 4, n_c * n_c)
+        return table
+    order = np.argsort(smap.patch_ids, kind="stable")
+    bounds = np.searchsorted(smap.patch_ids[order], np.arange(disc.n_patches + 1))
+    for p in range(disc.n_patches):
+        sel = order[bounds[p]:bounds[p + 1]]
+        if sel.size == 0:
+            continue
+        blk = out[sel]
+        table.groups[p] = MomentGroup(tg[sel], np.ascontiguousarray(blk[:, 0:2].transpose(1, 0, 2, 3)),
+                                      np.ascontiguousarray(blk[:, 2:4].transpose(1, 0, 2, 3)))
     return table
 
 

@@ -25,7 +25,8 @@ import torch
 from . import _lib, cheb
 from .engine import FarFieldPlan, device_stream
 from .nearfield import (SingularQuadratureConfig, classify_targets,
-                        compute_moments, correction_pairs)
+                        compute_moments, compute_moments_device,
+                        correction_pairs)
 from .octree import IfgfConfig, build_box_tree, build_cone_hierarchy
 
 __all__ = ["MaterialPair", "DensityBlock", "OperatorConfig", "MullerOperator",
@@ -152,21 +153,28 @@ def _near_desc(disc, tree, smap, moments, corr_ell, corr_src, keep):
     n2 = n_c * n_c
     # ---- moments, per (target, patch) sorted by target then patch
     tg, pt, blocks = [], [], []
-    for p in sorted(moments.groups):
+    csr = getattr(moments, "csr_blocks", None)
+    if csr is not None:   # device moments, already in the map's CSR order
+        mom_off = _c(smap.offsets, np.int64)
+        pt = _c(smap.patch_ids, np.int64)
+        blocks = np.ascontiguousarray(csr)
+        tg = np.repeat(np.arange(n, dtype=np.int64), np.diff(mom_off))
+    for p in sorted(moments.groups) if csr is None else ():
         grp = moments.groups[p]
         tg.append(np.asarray(grp.targets, dtype=np.int64))
         pt.append(np.full(grp.targets.size, p, dtype=np.int64))
         blk = np.stack([grp.beta_s[0], grp.beta_s[1], grp.beta_d[0],
                         grp.beta_d[1]], axis=1).reshape(-1, 4, n2)
         blocks.append(blk)
-    tg = np.concatenate(tg) if tg else np.empty(0, np.int64)
-    pt = np.concatenate(pt) if pt else np.empty(0, np.int64)
-    blocks = (np.concatenate(blocks) if blocks
-              else np.empty((0, 4, n2), complex))
-    order = np.lexsort((pt, tg))
-    tg, pt, blocks = tg[order], pt[order], np.ascontiguousarray(blocks[order])
-    mom_off = np.zeros(n + 1, dtype=np.int64)
-    np.cumsum(np.bincount(tg, minlength=n), out=mom_off[1:])
+    if csr is None:
+        tg = np.concatenate(tg) if tg else np.empty(0, np.int64)
+        pt = np.concatenate(pt) if pt else np.empty(0, np.int64)
+        blocks = (np.concatenate(blocks) if blocks
+                  else np.empty((0, 4, n2), complex))
+        order = np.lexsort((pt, tg))
+        tg, pt, blocks = tg[order], pt[order], np.ascontiguousarray(blocks[order])
+        mom_off = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(np.bincount(tg, minlength=n), out=mom_off[1:])
     # ---- + neighbour-box sources not on the target's singular patches
     d = tree.depth
     lvl = tree.level(d)
@@ -346,9 +354,13 @@ class MullerOperator:
 
 def build_muller_operator(disc, materials, quad_config=None, ifgf_config=None,
                           op_config=None, accelerated: bool = True, smap=None,
-                          moments=None) -> MullerOperator:
+                          moments=None, device_moments: bool = False) -> MullerOperator:
     """Plan (classification, moments, octree, cones, corrections) on the
-    host, then the device plan (reference operators.py:415-441)."""
+    host, then the device plan (reference operators.py:415-441).
+    device_moments: singular moments from the GPU kernel (csrc/moments.cu)
+    instead of the host restatement -- much faster plan for large surfaces;
+    beta_d then differs from the reference's at its ~1e-7 conditioning, so
+    parity runs keep the host moments (tests/test_gpu_moments.py)."""
     if not accelerated:
         raise NotImplementedError(
             "the dense O(N^2) path is not part of the B200 build")
@@ -356,7 +368,10 @@ def build_muller_operator(disc, materials, quad_config=None, ifgf_config=None,
     op_config = op_config or OperatorConfig()
     if smap is None:
         smap = classify_targets(disc, quad_config)
-    if moments is None:
+    if moments is None and device_moments:
+        moments = compute_moments_device(disc, smap, quad_config, materials.kappas,
+                                         groups=False)
+    elif moments is None:
         moments = compute_moments(disc, smap, quad_config, materials.kappas)
     kmax = max(abs(materials.kappa_e), abs(materials.kappa_i))
     tree = build_box_tree(disc.points, kmax)

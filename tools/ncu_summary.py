@@ -33,7 +33,8 @@ if len(rows) > 2:
     hh = rows[1]
     si, so = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Source")
     body = rows[2:]
-    tot = sum(int(x[si]) for x in body) or 1
+    num = lambda s: int(s) if s.strip().isdigit() else 0
+    tot = sum(num(x[si]) for x in body) or 1
     print("-- hottest SASS (share of stall samples)")
-    for x in sorted(body, key=lambda x: -int(x[si]))[:int(sys.argv[2]) if len(sys.argv) > 2 else 12]:
-        print(f"   {int(x[si]) * 100.0 / tot:5.1f}%  {x[so].strip()[:80]}")
+    for x in sorted(body, key=lambda x: -num(x[si]))[:int(sys.argv[2]) if len(sys.argv) > 2 else 12]:
+        print(f"   {num(x[si]) * 100.0 / tot:5.1f}%  {x[so].strip()[:80]}")
