@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--n-refine", type=int, default=4)
+    ap.add_argument("--k0-pi", type=float, default=None,
+                    help="k0 / pi (default n_refine: ~10 points per wavelength; cfg 5 is 45 / 32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--device-moments", action="store_true",
                     help="singular moments from the plan-time GPU kernel (large surfaces)")
@@ -68,31 +70,39 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def workload(n_refine):
+def workload(n_refine, k0_pi=None):
     import numpy as np
     from paper_2408_02274_b200 import surface
     from paper_2408_02274_b200.operator import MaterialPair
     disc = surface.make_sphere_surface(n_refine, 10)
-    k0 = np.pi * n_refine
+    k0_pi = n_refine if k0_pi is None else k0_pi
+    k0 = np.pi * k0_pi
     mats = MaterialPair(1.0, 1.0, 2.25, 1.0, k0)
     n = disc.n_points
     rng = np.random.default_rng(0)
     y = rng.normal(size=4 * n) + 1j * rng.normal(size=4 * n)
-    name = f"sphere(n_refine={n_refine}, n_c=10) k0={n_refine}pi eps_r=2.25"
+    name = f"sphere(n_refine={n_refine}, n_c=10) k0={k0_pi:g}pi eps_r=2.25"
     return disc, mats, y, name
 
 
 def plan_inputs(disc, mats, device_moments=False):
     from paper_2408_02274_b200 import nearfield, octree
     kmax = max(abs(mats.kappa_e), abs(mats.kappa_i))
+    t0 = time.time()
+    stage = lambda what: print(f"[plan] {what} {time.time() - t0:.1f}s", file=sys.stderr,
+                               flush=True)
     tree = octree.build_box_tree(disc.points, kmax)
+    stage("tree")
     hier = octree.build_cone_hierarchy(tree)
+    stage("cones")
     smap = nearfield.classify_targets(disc)
+    stage("classify")
     cfg = nearfield.SingularQuadratureConfig()
     if device_moments:
         mom = nearfield.compute_moments_device(disc, smap, cfg, mats.kappas, groups=False)
     else:
         mom = nearfield.compute_moments(disc, smap, cfg, mats.kappas)
+    stage("moments")
     cp = nearfield.correction_pairs(disc, tree, smap)
     return tree, hier, smap, mom, cp
 
@@ -204,7 +214,7 @@ def run_reference(args):
     if rank != 0:
         return
     import numpy as np  # noqa: F401
-    disc, mats, y, name = workload(args.n_refine)
+    disc, mats, y, name = workload(args.n_refine, args.k0_pi)
     inputs = plan_inputs(disc, mats)
     counts = work_counts(inputs[0], inputs[1])
     per_step = min(15.0, 150.0 / max(1, args.steps + args.warmup))
@@ -245,7 +255,7 @@ def run_b200(args):
         build()
     if world > 1:
         dist.barrier()
-    disc, mats, y, name = workload(args.n_refine)
+    disc, mats, y, name = workload(args.n_refine, args.k0_pi)
     t0 = time.time()
     inputs = plan_inputs(disc, mats, args.device_moments)
     tree, hier, smap, mom, cp = inputs
@@ -341,7 +351,7 @@ def run_b200(args):
     achieved = prop_flop / (prop_ms * 1e-3) / 1e12 if prop_ms > 0 else None
     traffic = None
     tf = ROOT / "profiles" / f"traffic_n{args.n_refine}.json"
-    if tf.exists():
+    if tf.exists() and args.k0_pi is None:
         traffic = json.loads(tf.read_text()).get("propagate_bytes_per_launch")
     kern = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
             for k, v in ktimes.items() if v[1]}
