@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--n-refine", type=int, default=4)
     ap.add_argument("--k0-pi", type=float, default=None,
                     help="k0 / pi (default n_refine: ~10 points per wavelength; cfg 5 is 45 / 32)")
+    ap.add_argument("--geometry", choices=["sphere", "superellipsoid", "slab"],
+                    default="sphere", help="BASELINE cfg 1/2/5, cfg 3, cfg 4 bodies")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--device-moments", action="store_true",
                     help="singular moments from the plan-time GPU kernel (large surfaces)")
@@ -70,18 +72,43 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def workload(n_refine, k0_pi=None):
+def workload(n_refine, k0_pi=None, geometry="sphere"):
+    """BASELINE configs: 'sphere' = cfg 1/2/5 family (sphere(n, 10), k0 = pi n
+    by default, eps_r 2.25); 'superellipsoid' = cfg 3 (|x/2|^4 + |y|^4 +
+    |z/0.5|^4 = 1, n x n subpatches per face on 12 x 12 grids, eps_r 4,
+    2a = 8 wavelengths -> k0 = 4 pi); 'slab' = cfg 4 (exponent-8
+    superellipsoid with half-extents 20 x 0.25 x 0.11 wavelengths, eps_r
+    12.11, (16n, 2n, n) aspect-graded splits on 10 x 10 grids, wavelength 1
+    -> k0 = 2 pi)."""
     import numpy as np
     from paper_2408_02274_b200 import surface
     from paper_2408_02274_b200.operator import MaterialPair
-    disc = surface.make_sphere_surface(n_refine, 10)
-    k0_pi = n_refine if k0_pi is None else k0_pi
-    k0 = np.pi * k0_pi
-    mats = MaterialPair(1.0, 1.0, 2.25, 1.0, k0)
+    if geometry == "sphere":
+        disc = surface.make_sphere_surface(n_refine, 10)
+        k0_pi = n_refine if k0_pi is None else k0_pi
+        eps = 2.25
+        name = f"sphere(n_refine={n_refine}, n_c=10) k0={k0_pi:g}pi eps_r=2.25"
+    elif geometry == "superellipsoid":
+        disc = surface.make_superellipsoid_surface(n_refine, 12, (2.0, 1.0, 0.5), 4.0)
+        k0_pi = 4.0 if k0_pi is None else k0_pi
+        eps = 4.0
+        name = (f"superellipsoid(|x/2|^4+|y|^4+|z/0.5|^4=1, {n_refine}x{n_refine} "
+                f"subpatches/face, n_c=12) k0={k0_pi:g}pi eps_r=4")
+    elif geometry == "slab":
+        k0_pi = 2.0 if k0_pi is None else k0_pi
+        lam = 2.0 / k0_pi
+        splits = (16 * n_refine, 2 * n_refine, n_refine)
+        disc = surface.make_superellipsoid_surface(
+            splits, 10, (20.0 * lam, 0.25 * lam, 0.11 * lam), 8.0)
+        eps = 12.11
+        name = (f"slab(superellipsoid p=8, 20 x 0.25 x 0.11 wavelengths, splits "
+                f"{splits}, n_c=10) k0={k0_pi:g}pi eps_r=12.11")
+    else:
+        raise ValueError(f"unknown geometry {geometry}")
+    mats = MaterialPair(1.0, 1.0, eps, 1.0, np.pi * k0_pi)
     n = disc.n_points
     rng = np.random.default_rng(0)
     y = rng.normal(size=4 * n) + 1j * rng.normal(size=4 * n)
-    name = f"sphere(n_refine={n_refine}, n_c=10) k0={k0_pi:g}pi eps_r=2.25"
     return disc, mats, y, name
 
 
@@ -214,7 +241,7 @@ def run_reference(args):
     if rank != 0:
         return
     import numpy as np  # noqa: F401
-    disc, mats, y, name = workload(args.n_refine, args.k0_pi)
+    disc, mats, y, name = workload(args.n_refine, args.k0_pi, args.geometry)
     inputs = plan_inputs(disc, mats)
     counts = work_counts(inputs[0], inputs[1])
     per_step = min(15.0, 150.0 / max(1, args.steps + args.warmup))
@@ -255,7 +282,7 @@ def run_b200(args):
         build()
     if world > 1:
         dist.barrier()
-    disc, mats, y, name = workload(args.n_refine, args.k0_pi)
+    disc, mats, y, name = workload(args.n_refine, args.k0_pi, args.geometry)
     t0 = time.time()
     inputs = plan_inputs(disc, mats, args.device_moments)
     tree, hier, smap, mom, cp = inputs
@@ -351,6 +378,8 @@ def run_b200(args):
     achieved = prop_flop / (prop_ms * 1e-3) / 1e12 if prop_ms > 0 else None
     traffic = None
     tf = ROOT / "profiles" / f"traffic_n{args.n_refine}.json"
+    if args.geometry != "sphere":
+        tf = ROOT / "profiles" / f"traffic_{args.geometry}_n{args.n_refine}.json"
     if tf.exists() and args.k0_pi is None:
         traffic = json.loads(tf.read_text()).get("propagate_bytes_per_launch")
     kern = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define IFGFB_ABI_VERSION 4
+#define IFGFB_ABI_VERSION 5
 
 enum {
   IFGFB_OK = 0,
@@ -218,6 +218,19 @@ typedef struct {
   const double* kappas;         /* 2 complex */
 } ifgfb_moment_desc;
 int ifgfb_singular_moments(const ifgfb_moment_desc* desc, double* out);
+
+/* Off-surface layer fields (replaces reference reference.py:285-312
+ * _layer_fields, called by evaluate_fields :315-347): for n_tgt targets
+ * tgt[3*t] and n_src sources src[15*s] = (x, y, z, m_w[3] complex, j_w[3]
+ * complex) (densities already times the quadrature weights), with
+ * G = exp(i kappa r)/(4 pi r) and kappa = (kappa[0], kappa[1]) complex:
+ *   out[f][t][c] (complex, f = 0..3) = curl S[m], curl S[j],
+ *   curlcurl S[m], curlcurl S[j]  (reference row order);
+ * min_dist[t] (optional) = min_s |tgt_t - src_s| (the reference's
+ * near-surface guard).  Host buffers; deterministic summation order. */
+int ifgfb_layer_fields(int64_t n_src, const double* src, int64_t n_tgt,
+                       const double* tgt, const double* kappa, double* out,
+                       double* min_dist);
 
 int ifgfb_plan_create(const ifgfb_tree_desc* tree, ifgfb_plan** out);
 int ifgfb_plan_add_level(ifgfb_plan* plan, const ifgfb_level_desc* lvl);

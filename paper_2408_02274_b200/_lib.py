@@ -151,6 +151,8 @@ EXPORTS = {
                               _ip, C.c_int32, C.c_int32], C.c_int),
     "ifgfb_row_tiles_fill": ([C.c_int64, _ip, _ip, C.c_int64, _u8p, _u8p, _u8p,
                               _ip, _u8p, C.c_int32], C.c_int),
+    "ifgfb_layer_fields": ([C.c_int64, _dp, C.c_int64, _dp, _dp, _dp, _dp],
+                           C.c_int),
     "ifgfb_zscal_div": ([C.c_void_p, C.c_void_p, C.c_double, C.c_int64,
                          C.c_void_p], C.c_int),
 }
@@ -172,7 +174,7 @@ def load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.ifgfb_abi_version() != 4:
+    if lib.ifgfb_abi_version() != 5:
         raise RuntimeError("libifgfb200 ABI version mismatch")
     _lib = lib
     return lib

@@ -39,7 +39,10 @@ def inputs(name: str):
         hier = octree.build_cone_hierarchy(tree)
         return dict(disc=disc, kappas=kap, tree=tree, hier=hier)
     nr, nc, k0pi, eps = z["config"]
-    disc = surface.make_sphere_surface(int(nr), int(nc))
+    if (GOLDEN / f"{name}.patchgrid").exists():
+        disc = surface.load_surface(GOLDEN / f"{name}.patchgrid", int(nc))
+    else:
+        disc = surface.make_sphere_surface(int(nr), int(nc))
     mats = MaterialPair(1.0, 1.0, float(eps), 1.0, float(k0pi) * np.pi)
     kmax = max(abs(mats.kappa_e), abs(mats.kappa_i))
     tree = octree.build_box_tree(disc.points, kmax)

@@ -18,6 +18,11 @@ Fixtures (complex arrays stored as complex128):
     floor_*         reference self-consistency floors (linearity, vec/seq)
   c1_gmres.npz      GMRES tol 1e-6, plane wave exp(i k0 z) x-pol (cfg 1)
   rand_ifgf.npz     ifgf_apply on random (2, N) weights, kappas (2pi, 3pi)
+  fields.npz        off-surface fields (reference.py:285-347) on sphere(1,10)
+                    with smooth random tangential currents; Mie series
+                    (reference.py:240-269) coefficients and fields; dipole;
+                    the validate-sphere check (cli.py:258-289) on the
+                    reference's own cfg-1 GMRES solution (c1_gmres.npz)
 """
 
 from __future__ import annotations
@@ -36,7 +41,25 @@ CONFIGS = {
     # name: (n_refine, n_c, k0 / pi, eps_r)
     "s1": (1, 10, 2.0, 2.25),
     "c1": (2, 10, 2.0, 2.25),
+    # superellipsoid |x/2|^4 + |y|^4 + |z/0.5|^4 = 1 (BASELINE cfg 3's body at
+    # 2a = 2 wavelengths, eps_r 4): 1 x 1 subpatch per face, n_c = 8
+    "se1": (1, 8, 1.0, 4.0),
 }
+# non-sphere geometries: PATCHGRID files written by the framework's
+# generator (surface.make_superellipsoid_surface) and committed next to the
+# fixtures; both the reference and the framework load the same file with
+# their own load_surface (reference geometry.py:286-329)
+GEOMETRY = {"se1": dict(semi_axes=(2.0, 1.0, 0.5), exponent=4.0)}
+
+
+def geometry_file(name):
+    path = OUT / f"{name}.patchgrid"
+    if not path.exists():
+        sys.path.insert(0, str(OUT.parents[1]))
+        from paper_2408_02274_b200 import surface as fs
+        nr, nc = CONFIGS[name][:2]
+        fs.write_surface(fs.make_superellipsoid_surface(nr, nc, **GEOMETRY[name]), path)
+    return path
 
 
 def _h(a) -> str:
@@ -115,7 +138,10 @@ def build(name):
                                   build_muller_operator)
     nr, nc, k0pi, eps = CONFIGS[name]
     k0 = k0pi * np.pi
-    disc = rg.make_sphere_surface(nr, nc)
+    if name in GEOMETRY:
+        disc = rg.load_surface(geometry_file(name), nc)
+    else:
+        disc = rg.make_sphere_surface(nr, nc)
     mats = MaterialPair(1.0, 1.0, eps, 1.0, k0)
     t0 = time.time()
     op = build_muller_operator(disc, mats)
@@ -199,10 +225,70 @@ def build_rand():
     print("rand done")
 
 
+def build_fields():
+    sys.path.insert(0, REF)
+    import emscat.geometry as rg
+    from emscat.operators import DensityBlock, MaterialPair, build_muller_operator
+    from emscat.reference import (_layer_fields, electric_dipole, evaluate_fields,
+                                  fibonacci_sphere, mie_solution, plane_wave)
+    k0 = 2 * np.pi
+    mats = MaterialPair(1.0, 1.0, 2.25, 1.0, k0)
+    pay = {}
+    # layer fields with smooth random tangential currents on sphere(1,10)
+    disc = rg.make_sphere_surface(1, 10)
+    rng = np.random.default_rng(11)
+    n = disc.normals
+    c = rng.normal(size=(4, 3)) + 1j * rng.normal(size=(4, 3))
+    m = np.cross(n, c[0] + np.outer(disc.points[:, 2], c[1]))
+    j = np.cross(n, c[2] + np.outer(disc.points[:, 0], c[3]))
+    dens = DensityBlock.from_currents(disc, j, m)
+    p_in = fibonacci_sphere(64, 0.6)
+    p_out = 1.8 * fibonacci_sphere(64, 1.0)
+    pay.update(s1_m=m, s1_j=j, s1_dens=dens.values, p_in=p_in, p_out=p_out,
+               lf_in=_layer_fields(disc, dens, mats.kappa_i, p_in),
+               lf_out=_layer_fields(disc, dens, mats.kappa_e, p_out))
+    e_in, h_in = evaluate_fields(disc, dens, mats, p_in, "interior")
+    inc = plane_wave(k0, omega=k0)
+    e_out, h_out = evaluate_fields(disc, dens, mats, p_out, "exterior",
+                                   incident=inc)
+    pay.update(e_in=e_in, h_in=h_in, e_out=e_out, h_out=h_out)
+    # Mie series
+    mie = mie_solution(1.0, mats)
+    pm_in = fibonacci_sphere(50, 0.7)
+    pm_out = fibonacci_sphere(50, 1.5)
+    ei, hi = mie.interior_fields(pm_in)
+    es, hs = mie.exterior_scattered(pm_out)
+    pay.update(mie_a=mie.a, mie_b=mie.b, mie_c=mie.c, mie_d=mie.d,
+               pm_in=pm_in, pm_out=pm_out, mie_e_in=ei, mie_h_in=hi,
+               mie_e_sc=es, mie_h_sc=hs)
+    dip = electric_dipole([0.1, -0.2, 0.3], [1.0, 0.5j, -0.25], eps=2.0,
+                          omega=k0)
+    ed, hd = dip.fields(pm_out)
+    pay.update(dip_e=ed, dip_h=hd)
+    # validate-sphere on the reference's cfg-1 GMRES solution
+    z = np.load(OUT / "c1_gmres.npz")
+    disc1 = rg.make_sphere_surface(2, 10)
+    op = build_muller_operator(disc1, mats)
+    mm, jj = op.decode(z["x"])
+    d1 = DensityBlock.from_currents(disc1, jj, mm)
+    pv = fibonacci_sphere(1000, 0.7)
+    e_num, h_num = evaluate_fields(disc1, d1, mats, pv, "interior")
+    # c1_gmres is driven by exp(+i k0 z) x_hat (BASELINE cfg 1): that is the
+    # series' own frame (MieSolution._eval), not the rotated -z default
+    e_ref, h_ref = mie._eval(pv, "interior")
+    pay.update(val_e=e_num, val_h=h_num,
+               val_err_e=np.linalg.norm(e_num - e_ref) / np.linalg.norm(e_ref),
+               val_err_h=np.linalg.norm(h_num - h_ref) / np.linalg.norm(h_ref))
+    np.savez_compressed(OUT / "fields.npz", **pay)
+    print("fields done", pay["val_err_e"], pay["val_err_h"])
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rand", "s1", "c1", "c1gmres"]
+    which = sys.argv[1:] or ["rand", "s1", "c1", "c1gmres", "fields"]
     for w_ in which:
-        if w_ == "c1gmres":
+        if w_ == "fields":
+            build_fields()
+        elif w_ == "c1gmres":
             build_gmres()
         elif w_ == "rand":
             build_rand()

@@ -44,6 +44,18 @@ def test_oracle_apply_vs_reference_golden():
     assert rel(out, z["apply_y"]) < 1e-10
 
 
+def test_oracle_apply_superellipsoid_vs_reference_golden():
+    """Non-sphere geometry (BASELINE cfg 3's body, PATCHGRID loaded by both
+    sides).  The reference's own linearity floor here is 1.5e-10
+    (golden floor_linearity), so the bar is 3e-10."""
+    z, inp = golden("se1"), inputs("se1")
+    op = oracle.OperatorData(inp["disc"], inp["mats"], inp["smap"],
+                             inp["moments"], inp["corr"].ell_idx,
+                             inp["corr"].src_idx, inp["tree"], inp["hier"])
+    assert float(z["floor_linearity"]) < 3e-10
+    assert rel(oracle.muller_apply(op, z["y"]), z["apply_y"]) < 3e-10
+
+
 def test_oracle_two_level_toy_matches_dense():
     rng = np.random.default_rng(4)
     src = rng.normal(size=(20, 3)) * 0.05 + [0.1, 0.1, 0.1]
