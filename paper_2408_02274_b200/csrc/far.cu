@@ -305,6 +305,15 @@ __device__ __forceinline__ void dmma4(double (&c0)[4], double (&c1)[4], double a
   dmma(c0[3], c1[3], av, b23.y);
 }
 
+// K4 option: software L1 prefetch of the B fragments IFGFB_ACC_PF k-steps
+// ahead (prefetch.global.L1 takes no registers; 0 = off).
+#ifndef IFGFB_ACC_PF
+#define IFGFB_ACC_PF 0
+#endif
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];\n" :: "l"(p));
+}
+
 template <bool EXACT, int QU = 3>
 __device__ __forceinline__ void basis_times_block(const BasisA& B,
                                                   const double* __restrict__ C,
@@ -314,8 +323,14 @@ __device__ __forceinline__ void basis_times_block(const BasisA& B,
 #pragma unroll QU
   for (int q = 0; q < 3; ++q) {
 #pragma unroll
-    for (int c = 0; c < PA; ++c)
-      dmma4(c0, c1, EXACT ? mul_rn(B.tst[q], B.tp[c]) : B.tst[q] * B.tp[c], F, 5 * q + c);
+    for (int c = 0; c < PA; ++c) {
+      const int ks = 5 * q + c;
+      if (!EXACT && IFGFB_ACC_PF > 0 && ks + IFGFB_ACC_PF < KSTEPS) {
+        prefetch_l1(F + (ks + IFGFB_ACC_PF) * 64);
+        prefetch_l1(F + (ks + IFGFB_ACC_PF) * 64 + 32);
+      }
+      dmma4(c0, c1, EXACT ? mul_rn(B.tst[q], B.tp[c]) : B.tst[q] * B.tp[c], F, ks);
+    }
   }
   const int tig = lane & 3;
 #pragma unroll
