@@ -587,6 +587,19 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
       const int g = tl.x & 0xff;
       const int crow_used = (!WIDE || g < MAX_GROUPS) ? S.crow[warp][g] : crow_g[g];
 #endif
+#if IFGFB_ACC_PF > 0 && defined(IFGFB_ACC_PFNEXT)
+      if (k + 1 < ntile) {   // warm L1 with the next tile's first k-steps
+        const int gn = S.tiles[pos0 + k + 1].x & 0xff;
+        const int crn = (!WIDE || gn < MAX_GROUPS) ? S.crow[warp][gn] : crow_g[gn];
+        const double2* Fn = reinterpret_cast<const double2*>(
+            a.coef_child + (size_t)crn * SEG_DOUBLES) + lane;
+#pragma unroll
+        for (int q = 0; q < IFGFB_ACC_PF; ++q) {
+          prefetch_l1(Fn + q * 64);
+          prefetch_l1(Fn + q * 64 + 32);
+        }
+      }
+#endif
       const double* ng = S.geom + (pos0 + slot) * 3;
       const BasisA B = make_basis<false>(ng[0], ng[1], ng[2], tig);
       double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};

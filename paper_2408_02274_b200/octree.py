@@ -908,6 +908,17 @@ def emission_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
     if disp_points_t is not None:
         sd, td, pd, rd = cone_coords(disp_points_t[tg] - ctr, np.zeros(3),
                                      lvl.side)
+        # Deliberate deviation from the reference (ifgf.py:647-651): the
+        # displaced point is evaluated with the undisplaced point's segment
+        # polynomial, but its phi is taken mod 2 pi, so a displacement
+        # across the phi = 0 seam lands ~2 n_a intervals away and the
+        # angular polynomial is extrapolated there (D_far = (S(x+hn) -
+        # S(x))/h then blows up by ~1e5 at those rows; GMRES stagnates from
+        # sphere(12,10) on).  Keep the displaced phi on the undisplaced
+        # point's branch.  Bitwise unchanged wherever the seam is not
+        # crossed (every golden configuration).
+        pd = np.where(pd - ph > np.pi, pd - 2.0 * np.pi,
+                      np.where(ph - pd > np.pi, pd + 2.0 * np.pi, pd))
         gd = np.stack(local_coords(cl, flat, sd, td, pd) + (rd,), axis=1)
     return EmissionPlan(d, row, tg, geom, gd, misses)
 

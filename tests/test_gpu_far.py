@@ -143,3 +143,94 @@ def test_displaced_outputs_fd_vs_analytic():
         ref = (q * wt[0, far]).sum()
         if abs(ref) > 1e-3:
             assert fd[0, 0, ell] == pytest.approx(ref, rel=2e-3)
+
+
+def _naive_far_at(tree, w, kappas, targets):
+    """Direct far sums (reference naive_far_sums, test_ifgf.py:22-38) at a
+    subset of targets (original indices): sources outside the target's
+    finest-level neighbour boxes."""
+    d = tree.depth
+    coords = tree.level(d).coords[tree.point_boxes(d)]
+    wt = np.atleast_2d(w)[:, tree.perm]
+    out = np.zeros((wt.shape[0], len(kappas), len(targets)), dtype=complex)
+    for j, ell in enumerate(targets):
+        t = tree.iperm[ell]
+        far = np.abs(coords - coords[t]).max(axis=1) >= 2
+        r = np.linalg.norm(tree.points[t] - tree.points[far], axis=1)
+        for k, kap in enumerate(kappas):
+            out[:, k, j] = (np.exp(1j * kap * r) / (4 * np.pi * r) * wt[:, far]).sum(1)
+    return out
+
+
+@pytest.mark.parametrize("geometry", ["sphere8", "superellipsoid_cfg3"])
+def test_full_size_accuracy_linearity_determinism(geometry):
+    """BASELINE sizes, size-independent properties: the far field against
+    direct sums at 100 sampled targets within the reference's accuracy bar
+    (test_ifgf.py:296-308, 1.5e-4), linearity to 1e-12 (test_ifgf.py:
+    311-330) and bitwise run-to-run determinism.  sphere8 = cfg 2 at
+    n = 8 (k0 = 8 pi, 153,600 unknowns, depth 7); superellipsoid_cfg3 =
+    cfg 3 (221,184 unknowns, depth 8)."""
+    if geometry == "sphere8":
+        disc = surface.make_sphere_surface(8, 10)
+        kap = (8 * np.pi, 12 * np.pi)
+    else:
+        disc = surface.make_superellipsoid_surface(8, 12, (2.0, 1.0, 0.5), 4.0)
+        kap = (4 * np.pi, 8 * np.pi)
+    tree = build_box_tree(disc.points, max(kap))
+    hier = build_cone_hierarchy(tree)
+    n = disc.n_points
+    rng = np.random.default_rng(7)
+    w = rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n))
+    w2 = rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n))
+    a, _ = ifgf_apply(tree, hier, w, kap)
+    a2, _ = ifgf_apply(tree, hier, w, kap)
+    assert np.array_equal(a, a2)
+    idx = rng.choice(n, 100, replace=False)
+    assert rel(a[:, :, idx], _naive_far_at(tree, w, kap, idx)) < 1.5e-4
+    b, _ = ifgf_apply(tree, hier, w2, kap)
+    c, _ = ifgf_apply(tree, hier, w + 0.5j * w2, kap)
+    assert np.abs(c - a - 0.5j * b).max() < 1e-12 * np.abs(c).max()
+
+
+def test_displaced_point_across_phi_seam():
+    """Displaced points (x + h n) that cross the phi = 0 seam of a source
+    box's cone stay on the undisplaced point's branch (octree.emission_plan;
+    the reference takes phi mod 2 pi there and extrapolates the angular
+    polynomial by ~2 n_a intervals, see DESIGN 2).  A large step makes many
+    crossings; the displaced far field must match direct sums at x + h n."""
+    disc = surface.make_sphere_surface(2, 10)
+    kap = (2 * np.pi, 3 * np.pi)
+    tree = build_box_tree(disc.points, max(kap))
+    hier = build_cone_hierarchy(tree)
+    step = 2e-3
+    rng = np.random.default_rng(4)
+    w = rng.normal(size=(1, disc.n_points)) + 1j * rng.normal(size=(1, disc.n_points))
+    out, od = ifgf_apply(tree, hier, w, kap, displaced_normals=disc.normals,
+                         displaced_step=step)
+    # targets whose displacement crosses a seam at some level
+    from paper_2408_02274_b200.octree import cone_coords
+    disp = tree.points + step * disc.normals[tree.perm]
+    cross = set()
+    for d in range(3, tree.depth + 1):
+        cl, lvl = hier.level(d), tree.level(d)
+        if cl.cpt_idx.size == 0:
+            continue
+        box = np.repeat(np.arange(lvl.n_boxes), np.diff(cl.cpt_off))
+        ctr = lvl.centers[box]
+        ph = cone_coords(tree.points[cl.cpt_idx] - ctr, np.zeros(3), lvl.side)[2]
+        pd = cone_coords(disp[cl.cpt_idx] - ctr, np.zeros(3), lvl.side)[2]
+        cross.update(int(tree.perm[t]) for t in cl.cpt_idx[np.abs(pd - ph) > np.pi])
+    idx = np.array(sorted(cross))[:40]
+    assert idx.size >= 5
+    # direct far sums at x + h n with x's own far-box set
+    dd = tree.depth
+    coords = tree.level(dd).coords[tree.point_boxes(dd)]
+    wt = w[:, tree.perm]
+    ref = np.zeros((1, 2, idx.size), dtype=complex)
+    for j, ell in enumerate(idx):
+        t = tree.iperm[ell]
+        far = np.abs(coords - coords[t]).max(axis=1) >= 2
+        r = np.linalg.norm(disp[t] - tree.points[far], axis=1)
+        for k, kp in enumerate(kap):
+            ref[:, k, j] = (np.exp(1j * kp * r) / (4 * np.pi * r) * wt[:, far]).sum(1)
+    assert rel(od[:, :, idx], ref) < 1e-3

@@ -58,6 +58,10 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-6)
     ap.add_argument("--max-iter", type=int, default=500)
     ap.add_argument("--device-moments", action="store_true")
+    ap.add_argument("--stream-parts", type=int, default=None,
+                    help="force single-GPU streaming over this many subtree groups")
+    ap.add_argument("--geom-on-device", default=None, choices=["none", "all", "auto"],
+                    help="propagation node geometry policy (engine._choose_otf)")
     args = ap.parse_args()
 
     import numpy as np
@@ -73,8 +77,11 @@ def main():
     disc, mats, _, name = bench.workload(args.n_refine, args.k0_pi, args.geometry)
     t0 = time.time()
     tree, hier, smap, mom, cp = bench.plan_inputs(disc, mats, args.device_moments)
+    if args.geom_on_device:
+        import os
+        os.environ["IFGFB_GEOM_ON_DEVICE"] = args.geom_on_device
     op = MullerOperator(disc, mats, smap, mom, (cp.ell_idx, cp.src_idx), tree=tree,
-                        hierarchy=hier)
+                        hierarchy=hier, stream_parts=args.stream_parts)
     t_plan = time.time() - t0
     inc, inc_name = incident_for(args.geometry, mats, disc)
     b = op.rhs(inc)
@@ -93,6 +100,8 @@ def main():
     line = {"workload": name, "unknowns": 4 * disc.n_points, "depth": tree.depth,
             "incident": inc_name, "tol": args.tol, "max_iter": args.max_iter,
             "plan_build_s": round(t_plan, 1), "matvec_s": t_mv,
+            "otf_levels": sorted(getattr(op.plan, "otf_levels", [])),
+            "residuals_head": [float(r) for r in rep.residuals[:12]],
             "gmres": {"iterations": rep.iterations, "converged": rep.converged,
                       "final_residual": float(rep.residuals[-1]) if rep.residuals else 0.0,
                       "solve_s": rep.wall_time,
