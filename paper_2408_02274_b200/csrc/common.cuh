@@ -219,6 +219,11 @@ struct Plan {
   double* coef[2] = {nullptr, nullptr};
   size_t coef_cap = 0;             // segments
   double* partial = nullptr;       // max pairs * 2 * NCOL complex
+  // emission overlap: a level's emission (K5 + reduce) runs on `aux`
+  // concurrently with the next propagation step on the apply stream
+  cudaStream_t aux = nullptr;
+  std::vector<cudaEvent_t> sync_events;
+  bool overlap_emit = false;
   double* out_tree = nullptr;      // N * NCOL complex
   double* out_disp_tree = nullptr;
   int64_t max_pairs = 0;

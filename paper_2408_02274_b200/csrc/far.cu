@@ -13,6 +13,8 @@
 // / parent level ping-pong).
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace ifgfb {
 
 __constant__ double c_ms[PS * PS];   // chebyshev transform_matrix(3)
@@ -305,10 +307,12 @@ __device__ __forceinline__ void dmma4(double (&c0)[4], double (&c1)[4], double a
   dmma(c0[3], c1[3], av, b23.y);
 }
 
-// K4 option: software L1 prefetch of the B fragments IFGFB_ACC_PF k-steps
-// ahead (prefetch.global.L1 takes no registers; 0 = off).
+// K4: software L1 prefetch of the B fragments IFGFB_ACC_PF k-steps ahead
+// (prefetch.global.L1 takes no registers; 0 = off).  Measured at (4,10):
+// 0 / 2 / 4 / 6 / 8 / 12 / 16 -> propagate 22.98 / 23.06 / 23.07 / 22.67 /
+// 22.58 / 22.52 / 23.40 ms (tools/ab_variants.sh, profiles/ab_r01_prefetch.txt).
 #ifndef IFGFB_ACC_PF
-#define IFGFB_ACC_PF 0
+#define IFGFB_ACC_PF 12
 #endif
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];\n" :: "l"(p));
@@ -742,10 +746,62 @@ static void apply_stream_part(Plan& p, int part) {
 
 int ensure_coef(Plan& p);
 
+// Emission overlap (Plan::overlap_emit, opt-in: env IFGFB_OVERLAP_EMIT=1).
+// Measured at (4,10): 26.27 -> 26.10 ms per matvec (0.7%); off by default
+// because per-kernel event times of the overlapped emission then include
+// the time its CTAs wait for SMs held by the propagation.
+// level d's emission reads only level d's coefficients, so it runs on the
+// plan's aux stream while the apply stream propagates d -> d-1.  The
+// propagation that overwrites level d's ping-pong buffer (d-1 -> d-2, or
+// the next streaming part's leaf) first waits for that emission.
+struct EmitSync {
+  Plan& p;
+  cudaStream_t st;
+  size_t next = 0;
+  bool on;
+  EmitSync(Plan& p_, cudaStream_t st_) : p(p_), st(st_), on(p_.overlap_emit && p_.aux) {}
+  cudaEvent_t ev() {
+    if (next == p.sync_events.size()) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      p.sync_events.push_back(e);
+    }
+    return p.sync_events[next++];
+  }
+  // aux waits for everything issued so far on st
+  void fork() {
+    if (!on) return;
+    cudaEvent_t e = ev();
+    cudaEventRecord(e, st);
+    cudaStreamWaitEvent(p.aux, e, 0);
+  }
+  // st waits for everything issued so far on aux
+  void join() {
+    if (!on) return;
+    cudaEvent_t e = ev();
+    cudaEventRecord(e, p.aux);
+    cudaStreamWaitEvent(st, e, 0);
+  }
+  cudaStream_t emit_stream() const { return on ? p.aux : st; }
+};
+
+static int ensure_aux(Plan& p) {
+  static const bool env_on = [] {
+    const char* v = std::getenv("IFGFB_OVERLAP_EMIT");
+    return v && v[0] == '1';
+  }();
+  p.overlap_emit = env_on;
+  if (p.overlap_emit && !p.aux)
+    IFGFB_CUDA(cudaStreamCreateWithFlags(&p.aux, cudaStreamNonBlocking));
+  return IFGFB_OK;
+}
+
 template <int NK>
 static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
                        double* out, double* out_disp, cudaStream_t st) {
   if (p.coef_cap == 0) IFGFB_RC(ensure_coef(p));
+  IFGFB_RC(ensure_aux(p));
+  EmitSync sync(p, st);
   constexpr int CH = NCOL / NK;
   const int n = p.n;
   const int threads = 256;
@@ -792,25 +848,38 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
           ++launches;
         }
       }
+      cudaEvent_t prev_done = nullptr;   // emission of level d + 1 finished
       for (int d = D; d >= 3; --d) {
         Level& L = p.levels[d];
+        // level d's coefficients (coef[cur]) are complete on st
+        sync.fork();
+        const cudaStream_t est = sync.emit_stream();
         if (L.tile_hi() > L.tile_lo()) {
           EmitArgs ea{L.etiles, L.tile_lo(), L.tile_hi(), L.pair_id, L.geom,
                       out_disp ? L.geom_disp : nullptr,
                       p.coef[cur] - (size_t)L.seg_lo() * SEG_DOUBLES,
                       {kr[0], kr[1]}, {ki[0], ki[1]},
                       reinterpret_cast<double2*>(p.partial)};
-          int tk = p.timer.begin(K_EMIT, st);
-          emit_kernel<NK><<<(L.tile_hi() - L.tile_lo() + 3) / 4, 128, 0, st>>>(ea);
-          p.timer.end(tk, st);
-          tk = p.timer.begin(K_REDUCE, st);
-          emit_reduce<<<(n * NCOL + threads - 1) / threads, threads, 0, st>>>(
+          int tk = p.timer.begin(K_EMIT, est);
+          emit_kernel<NK><<<(L.tile_hi() - L.tile_lo() + 3) / 4, 128, 0, est>>>(ea);
+          p.timer.end(tk, est);
+          tk = p.timer.begin(K_REDUCE, est);
+          emit_reduce<<<(n * NCOL + threads - 1) / threads, threads, 0, est>>>(
               n, L.pair_lo(), L.pair_hi(), L.tgt_off, L.tgt_pairs,
               reinterpret_cast<const double2*>(p.partial),
               reinterpret_cast<double2*>(p.out_tree),
               out_disp ? reinterpret_cast<double2*>(p.out_disp_tree) : nullptr);
-          p.timer.end(tk, st);
+          p.timer.end(tk, est);
           launches += 2;
+        }
+        // the propagation below overwrites coef[cur ^ 1], which holds level
+        // d + 1: wait for level d + 1's emission first
+        cudaEvent_t done_d = nullptr;
+        if (sync.on) {
+          done_d = sync.ev();
+          cudaEventRecord(done_d, p.aux);
+          if (prev_done) cudaStreamWaitEvent(st, prev_done, 0);
+          prev_done = done_d;
         }
         if (d > 3 && L.has_accum) {
           Level& U = p.levels[d - 1];
@@ -841,6 +910,8 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
           cur ^= 1;
         }
       }
+      // the next part's leaf overwrites coef[0]; unpermute reads out_tree
+      sync.join();
     }
   }
   const int ncols = nch * NK;

@@ -392,6 +392,8 @@ int ifgfb_plan_destroy(ifgfb_plan* h) {
   if (!h) return IFGFB_OK;
   for (void* ptr : h->p.allocations) cudaFree(ptr);
   if (h->p.host_stage) cudaFreeHost(h->p.host_stage);
+  for (cudaEvent_t e : h->p.sync_events) cudaEventDestroy(e);
+  if (h->p.aux) cudaStreamDestroy(h->p.aux);
   delete h;
   return IFGFB_OK;
 }

@@ -58,6 +58,9 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-6)
     ap.add_argument("--max-iter", type=int, default=500)
     ap.add_argument("--device-moments", action="store_true")
+    ap.add_argument("--eps-r", type=float, default=None, help="override the config's eps_r")
+    ap.add_argument("--incident", default="config", choices=["config", "plane-x", "plane-y", "plane-z"],
+                    help="override the config's incident field with a plane wave along an axis")
     ap.add_argument("--stream-parts", type=int, default=None,
                     help="force single-GPU streaming over this many subtree groups")
     ap.add_argument("--geom-on-device", default=None, choices=["none", "all", "auto"],
@@ -75,6 +78,10 @@ def main():
     build()
     torch.cuda.set_device(0)
     disc, mats, _, name = bench.workload(args.n_refine, args.k0_pi, args.geometry)
+    if args.eps_r is not None:
+        from paper_2408_02274_b200.operator import MaterialPair
+        mats = MaterialPair(1.0, 1.0, args.eps_r, 1.0, mats.omega)
+        name += f" (eps_r overridden: {args.eps_r:g})"
     t0 = time.time()
     tree, hier, smap, mom, cp = bench.plan_inputs(disc, mats, args.device_moments)
     if args.geom_on_device:
@@ -83,7 +90,16 @@ def main():
     op = MullerOperator(disc, mats, smap, mom, (cp.ell_idx, cp.src_idx), tree=tree,
                         hierarchy=hier, stream_parts=args.stream_parts)
     t_plan = time.time() - t0
-    inc, inc_name = incident_for(args.geometry, mats, disc)
+    if args.incident == "config":
+        inc, inc_name = incident_for(args.geometry, mats, disc)
+    else:
+        from paper_2408_02274_b200.fields import plane_wave
+        ax = "xyz".index(args.incident[-1])
+        dvec = np.eye(3)[ax]
+        pol = np.eye(3)[(ax + 1) % 3]
+        inc = plane_wave(float(np.real(mats.kappa_e)), direction=tuple(dvec),
+                         polarization=tuple(pol), omega=mats.omega)
+        inc_name = f"plane wave along {args.incident[-1]}"
     b = op.rhs(inc)
     # one matvec (warm) for the per-matvec time
     bd = torch.from_numpy(b).cuda()
