@@ -314,6 +314,9 @@ __device__ __forceinline__ void dmma4(double (&c0)[4], double (&c1)[4], double a
 #ifndef IFGFB_ACC_PF
 #define IFGFB_ACC_PF 12
 #endif
+#ifndef IFGFB_EMIT_PF   // same for the emission kernel (K5)
+#define IFGFB_EMIT_PF 0
+#endif
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];\n" :: "l"(p));
 }
@@ -329,9 +332,10 @@ __device__ __forceinline__ void basis_times_block(const BasisA& B,
 #pragma unroll
     for (int c = 0; c < PA; ++c) {
       const int ks = 5 * q + c;
-      if (!EXACT && IFGFB_ACC_PF > 0 && ks + IFGFB_ACC_PF < KSTEPS) {
-        prefetch_l1(F + (ks + IFGFB_ACC_PF) * 64);
-        prefetch_l1(F + (ks + IFGFB_ACC_PF) * 64 + 32);
+      constexpr int PF = EXACT ? IFGFB_EMIT_PF : IFGFB_ACC_PF;
+      if (PF > 0 && ks + PF < KSTEPS) {
+        prefetch_l1(F + (ks + PF) * 64);
+        prefetch_l1(F + (ks + PF) * 64 + 32);
       }
       dmma4(c0, c1, EXACT ? mul_rn(B.tst[q], B.tp[c]) : B.tst[q] * B.tp[c], F, ks);
     }

@@ -44,12 +44,16 @@ CONFIGS = {
     # superellipsoid |x/2|^4 + |y|^4 + |z/0.5|^4 = 1 (BASELINE cfg 3's body at
     # 2a = 2 wavelengths, eps_r 4): 1 x 1 subpatch per face, n_c = 8
     "se1": (1, 8, 1.0, 4.0),
+    # short cfg-4-like slab: exponent-8 superellipsoid, half-extents
+    # 2 x 0.25 x 0.11 wavelengths (wavelength 1), eps_r 12.11, (4, 2, 1) splits
+    "sl1": ((4, 2, 1), 10, 2.0, 12.11),
 }
 # non-sphere geometries: PATCHGRID files written by the framework's
 # generator (surface.make_superellipsoid_surface) and committed next to the
 # fixtures; both the reference and the framework load the same file with
 # their own load_surface (reference geometry.py:286-329)
-GEOMETRY = {"se1": dict(semi_axes=(2.0, 1.0, 0.5), exponent=4.0)}
+GEOMETRY = {"se1": dict(semi_axes=(2.0, 1.0, 0.5), exponent=4.0),
+            "sl1": dict(semi_axes=(2.0, 0.25, 0.11), exponent=8.0)}
 
 
 def geometry_file(name):
@@ -173,7 +177,7 @@ def build(name):
     payload = dict(y=y, apply_y=ay, weights=w, far=far, far_disp=far_d,
                    s_val=s_val, d_val=d_val, floor_linearity=floor_lin,
                    t_apply_ref_container=t_apply,
-                   config=np.array([nr, nc, k0pi, eps]))
+                   config=np.array([nr if np.isscalar(nr) else 0, nc, k0pi, eps]))
     if name == "s1":
         op.config = type(op.config)(fd_step=op.config.fd_step, mode="seq")
         ay_seq = op.apply(y)

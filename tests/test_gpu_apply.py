@@ -34,7 +34,7 @@ def device_op(name) -> MullerOperator:
     return _OPS[name]
 
 
-@pytest.mark.parametrize("name", ["s1", "c1", "se1"])
+@pytest.mark.parametrize("name", ["s1", "c1", "se1", "sl1"])
 def test_apply_vs_reference_golden(name):
     if not plan_matches_golden(name):
         pytest.skip("host numpy produced a different plan than the golden host")
@@ -42,6 +42,7 @@ def test_apply_vs_reference_golden(name):
     op = device_op(name)
     out = op.apply(z["y"])
     # se1 (superellipsoid): the reference's own linearity floor is 1.5e-10
+    # sl1 (short cfg-4 slab, eps_r 12.11): 3.6e-11
     assert rel(out, z["apply_y"]) < (1e-10 if name != "se1" else 3e-10)
 
 

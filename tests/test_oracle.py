@@ -56,6 +56,16 @@ def test_oracle_apply_superellipsoid_vs_reference_golden():
     assert rel(oracle.muller_apply(op, z["y"]), z["apply_y"]) < 3e-10
 
 
+def test_oracle_apply_slab_vs_reference_golden():
+    """Short cfg-4-like slab (exponent-8 superellipsoid 2 x 0.25 x 0.11
+    wavelengths, eps_r 12.11), PATCHGRID loaded by both sides."""
+    z, inp = golden("sl1"), inputs("sl1")
+    op = oracle.OperatorData(inp["disc"], inp["mats"], inp["smap"],
+                             inp["moments"], inp["corr"].ell_idx,
+                             inp["corr"].src_idx, inp["tree"], inp["hier"])
+    assert rel(oracle.muller_apply(op, z["y"]), z["apply_y"]) < 1e-10
+
+
 def test_oracle_two_level_toy_matches_dense():
     rng = np.random.default_rng(4)
     src = rng.normal(size=(20, 3)) * 0.05 + [0.1, 0.1, 0.1]

@@ -12,7 +12,7 @@ from paper_2408_02274_b200.octree import (ETA, build_box_tree,
                                           morton_decode, morton_encode)
 
 
-@pytest.mark.parametrize("name", ["s1", "c1", "se1"])
+@pytest.mark.parametrize("name", ["s1", "c1", "se1", "sl1"])
 def test_plan_digests_match_reference(name):
     mine = framework_digests(inputs(name))
     ref = golden_digests(name)
