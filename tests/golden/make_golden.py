@@ -229,6 +229,27 @@ def build_rand():
     print("rand done")
 
 
+def build_sl1_gmres():
+    """GMRES history on the short slab (sl1) for a plane wave along +y,
+    z-polarised: 15 iterations (tol 1e-12 is never reached)."""
+    sys.path.insert(0, REF)
+    import emscat.geometry as rg
+    from emscat.operators import MaterialPair, build_muller_operator
+    from emscat.reference import plane_wave
+    from emscat.solver import gmres
+    nr, nc, k0pi, eps = CONFIGS["sl1"]
+    disc = rg.load_surface(geometry_file("sl1"), nc)
+    k0 = k0pi * np.pi
+    mats = MaterialPair(1.0, 1.0, eps, 1.0, k0)
+    op = build_muller_operator(disc, mats)
+    b = op.rhs(plane_wave(k0, direction=(0.0, 1.0, 0.0),
+                          polarization=(0.0, 0.0, 1.0), omega=k0))
+    x, rep = gmres(op.apply, b, tol=1e-12, max_iter=15)
+    np.savez_compressed(OUT / "sl1_gmres.npz", b=b, x=x,
+                        residuals=np.array(rep.residuals))
+    print("sl1 gmres", rep.residuals)
+
+
 def build_fields():
     sys.path.insert(0, REF)
     import emscat.geometry as rg
@@ -292,6 +313,8 @@ if __name__ == "__main__":
     for w_ in which:
         if w_ == "fields":
             build_fields()
+        elif w_ == "sl1gmres":
+            build_sl1_gmres()
         elif w_ == "c1gmres":
             build_gmres()
         elif w_ == "rand":

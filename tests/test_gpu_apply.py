@@ -164,3 +164,22 @@ def test_geometry_on_device_matches_reference(name):
         (inp["corr"].ell_idx, inp["corr"].src_idx), tree=inp["tree"],
         hierarchy=inp["hier"], geometry_on_device="all")
     assert rel(op.apply(z["y"]), z["apply_y"]) < 1e-10
+
+
+def test_gmres_slab_matches_reference_history():
+    """Short cfg-4-like slab (sl1, eps_r 12.11): the device GMRES history
+    for a broadside plane wave follows the reference's (15 iterations; the
+    high-contrast thin body converges slowly in the reference too)."""
+    if not plan_matches_golden("sl1"):
+        pytest.skip("host numpy produced a different plan than the golden host")
+    z = golden("sl1_gmres")
+    op = device_op("sl1")
+    k0 = float(op.materials.omega)
+    b = op.rhs(plane_wave(k0, direction=(0.0, 1.0, 0.0),
+                          polarization=(0.0, 0.0, 1.0), omega=k0))
+    assert rel(b, z["b"]) < 1e-14
+    x, rep = gmres(op, b, tol=1e-12, max_iter=15)
+    r = np.array(rep.residuals)
+    assert r.size == z["residuals"].size
+    assert np.max(np.abs(r - z["residuals"])) < 1e-7
+    assert rel(x, z["x"]) < 1e-6
