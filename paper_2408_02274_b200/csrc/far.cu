@@ -181,8 +181,8 @@ constexpr int LEAF_RS = 20;   // padded row stride of the leaf's node values
 template <int NK>
 constexpr int leaf_threads() { return ((NN * NK + 31) / 32) * 32; }
 
-#ifndef IFGFB_LEAF_MINB
-#define IFGFB_LEAF_MINB 5
+#ifndef IFGFB_LEAF_MINB   // 6 CTAs/SM (64 registers, 40 B spill): 1.833 -> 1.739 ms at (4,10)
+#define IFGFB_LEAF_MINB 6
 #endif
 template <int NK>
 __global__ void __launch_bounds__(leaf_threads<NK>(), IFGFB_LEAF_MINB) leaf_kernel(LeafArgs a) {
@@ -314,8 +314,8 @@ __device__ __forceinline__ void dmma4(double (&c0)[4], double (&c1)[4], double a
 #ifndef IFGFB_ACC_PF
 #define IFGFB_ACC_PF 12
 #endif
-#ifndef IFGFB_EMIT_PF   // same for the emission kernel (K5)
-#define IFGFB_EMIT_PF 0
+#ifndef IFGFB_EMIT_PF   // same for the emission kernel (K5): 1.198 -> 1.046 ms at 8
+#define IFGFB_EMIT_PF 8
 #endif
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];\n" :: "l"(p));
