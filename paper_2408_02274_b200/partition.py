@@ -44,8 +44,16 @@ def _level3_ancestor(tree, d):
     return np.searchsorted(codes3, tree.level(d).codes >> np.uint64(3 * (d - 3)))
 
 
+# Leaf pairs cost ~10x their 128 algorithmic FLOP relative to propagation
+# instances in device time (B200, (4,10): 1.74 ms / 27.3 M pairs against
+# 22.5 ms / 1.21 M instances; the sincos and the per-segment K3 + store are
+# not in the FLOP count), so the balance weights a pair at 10 W_LEAF.
+W_LEAF_TIME = 10 * W_LEAF
+
+
 def subtree_work(tree, hier) -> np.ndarray:
-    """Modelled FLOP of the upward pass attributed to each level-3 box."""
+    """Modelled cost (FLOP-equivalents, time-calibrated leaf weight) of the
+    upward pass attributed to each level-3 box."""
     n3 = tree.level(3).n_boxes
     work = np.zeros(n3)
     D = tree.depth
@@ -54,7 +62,7 @@ def subtree_work(tree, hier) -> np.ndarray:
         anc = _level3_ancestor(tree, d)
         w = W_EMIT * np.diff(cl.cpt_off) + W_COEF * np.diff(cl.seg_off)
         if d == D:
-            w = w + W_LEAF * np.diff(cl.seg_off) * lvl.pt_count
+            w = w + W_LEAF_TIME * np.diff(cl.seg_off) * lvl.pt_count
         if d >= 4:
             pcl = hier.level(d - 1)
             w = w + W_PROP * np.diff(pcl.seg_off)[lvl.parent]
@@ -72,7 +80,11 @@ def level3_partition(tree, hier, n_ranks: int, n_patches: int,
     total = cum[-1]
     cuts = [0]
     for r in range(1, n_ranks):
-        cuts.append(int(np.searchsorted(cum, total * r / n_ranks)))
+        target = total * r / n_ranks
+        i = int(np.searchsorted(cum, target))      # first boundary >= target
+        if 0 < i <= work.size and target - cum[i - 1] < cum[i] - target:
+            i -= 1                                  # the nearer boundary
+        cuts.append(i)
     cuts.append(work.size)
     cuts = np.maximum.accumulate(np.minimum(cuts, work.size))
     n2 = n_c * n_c
