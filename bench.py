@@ -397,7 +397,9 @@ def run_b200(args):
                    "l2": "flushed (256 MB write) before every timed step",
                    "parallelism": (f"morton-level3-partition x{world} (NCCL all-reduce "
                                    "of far field + result)") if use_part else "single-gpu",
-                   "plan_build_s": round(t_plan, 1)},
+                   "plan_build_s": round(t_plan, 1),
+                   "geometry_on_device_levels": sorted(getattr(op.plan, "otf_levels", [])),
+                   "stream_parts": int(getattr(op.plan, "stream_parts", 1) or 1)},
         "roofline": {"kernel": "propagate (K4: child->parent re-interpolation on "
                                "FP64 DMMA + fused K3)",
                      "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,

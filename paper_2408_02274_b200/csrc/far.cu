@@ -320,6 +320,12 @@ __device__ __forceinline__ void dmma4(double (&c0)[4], double (&c1)[4], double a
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];\n" :: "l"(p));
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" :: "l"(p));
+}
+#ifndef IFGFB_ACC_L2PF   // K4: L2 prefetch of the next instance's child blocks
+#define IFGFB_ACC_L2PF 0
+#endif
 
 template <bool EXACT, int QU = 3>
 __device__ __forceinline__ void basis_times_block(const BasisA& B,
@@ -551,6 +557,12 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
     if (lane < ke - ks) cp_async16(&S.tiles[pos0 + lane], a.tiles + ks + lane);
     if (lane < min(ce - cs, MAX_GROUPS)) cp_async4(&S.crow[warp][lane], a.crow + cs + lane);
     cp_async_commit();
+    if (IFGFB_ACC_L2PF) {   // warp w warms L2 with groups w, w + 5, ...
+      for (int g = warp; g < ce - cs; g += WARP_PARTS) {
+        const double* blk = a.coef_child + (size_t)__ldg(a.crow + cs + g) * SEG_DOUBLES;
+        for (int off = lane * 16; off < SEG_DOUBLES; off += 32 * 16) prefetch_l2(blk + off);
+      }
+    }
   };
   if (ni > 0) stage_inst(0, stage[0]);
   for (int j = 0; j < ni; ++j) {

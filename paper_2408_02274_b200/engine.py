@@ -147,10 +147,19 @@ class FarFieldPlan:
         budget = 0.55 * torch.cuda.get_device_properties(
             torch.cuda.current_device()).total_memory
         tables = sum(b for b, _ in info.values())
+        # a level whose tables are below min_frac of the device memory cannot
+        # relieve it, while on-device geometry costs FP64 work (acos, atan2,
+        # sincos per node and instance) on the pipe the DMMAs use: keep its
+        # tables (fine levels of large configurations: few types, most
+        # instances).  IFGFB_OTF_MIN_FRAC=0 restores the plain rule.
+        min_frac = float(os.environ.get("IFGFB_OTF_MIN_FRAC", "0.01"))
+        total_mem = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory
         chosen = set()
         for d in sorted(levels, key=lambda d: -info[d][1]):
             if fixed + tables <= budget:
                 break
+            if info[d][0] < min_frac * total_mem:
+                continue
             chosen.add(d)
             tables -= info[d][0]
         return chosen
