@@ -17,6 +17,19 @@ from _support import golden, inputs, rel
 from paper_2408_02274_b200.partition import level3_partition, subtree_work
 
 
+@pytest.mark.parametrize("n_ranks", [2, 4, 8])
+def test_partition_nearest_cuts_balanced_and_nonempty(n_ranks):
+    """Cuts go to the nearer level-3 boundary: every rank owns subtrees and
+    no rank is further from the mean than one level-3 subtree's work."""
+    inp = inputs("c1")
+    tree, hier, disc = inp["tree"], inp["hier"], inp["disc"]
+    work = subtree_work(tree, hier)
+    parts = level3_partition(tree, hier, n_ranks, disc.n_patches, disc.n_c)
+    assert all(p.box3[1] > p.box3[0] for p in parts)
+    mean = work.sum() / n_ranks
+    assert max(abs(p.work - mean) for p in parts) <= work.max() + 1e-6 * mean
+
+
 @pytest.mark.parametrize("n_ranks", [1, 2, 3, 8])
 def test_partition_covers_everything_once(n_ranks):
     inp = inputs("c1")
