@@ -277,6 +277,9 @@ def run_b200(args):
     torch.cuda.set_device(local)
     use_part = world > 1 or args.force_partition
     if use_part:
+        # keep rank 0's stdout to the one JSON line (NCCL prints its version
+        # banner at NCCL_DEBUG=VERSION/INFO; an explicit setting is kept)
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if rank == 0:
         build()
