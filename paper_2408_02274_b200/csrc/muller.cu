@@ -182,7 +182,10 @@ __device__ __forceinline__ void warp_reduce_owned(const double2 (&s)[8][2],
 // (+ entries) and local corrections (- entries), then the reference's
 // combination with the far field (operators.py:341-350), including
 // D_far = (S_disp - S) / h.  Three phases keep 28 complex accumulators live.
-__global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
+#ifndef IFGFB_NEAR_MINB
+#define IFGFB_NEAR_MINB 1
+#endif
+__global__ void __launch_bounds__(128, IFGFB_NEAR_MINB) near_kernel(NearArgs a) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int n = a.s.n, n2 = a.s.n_c * a.s.n_c;

@@ -6,7 +6,10 @@ import sys
 rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(raw.splitlines()))
-h, units, v = r[0], r[1], r[2]
+h, units = r[0], r[1]
+# optional: the launch whose kernel name contains argv[3] (default: first)
+pick = sys.argv[3] if len(sys.argv) > 3 else None
+v = next((x for x in r[2:] if pick is None or pick in x[h.index("Kernel Name")]), r[2])
 want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "launch__registers_per_thread", "launch__occupancy_limit_registers",
         "launch__occupancy_limit_shared_mem", "sm__warps_active.avg.pct_of_peak_sustained_active",
