@@ -7,21 +7,26 @@ value   = device throughput with y resident in HBM (CUDA events, L2 flushed
 e2e     = same metric through the public host API (MullerOperator.apply on a
           numpy vector: pinned staging, H2D, apply, D2H inside the timed call)
 
-Workload (BASELINE.json configs[1], cfg-2 family): unit dielectric sphere,
-eps_r = 2.25, 6 x n^2 patches on 10x10 Chebyshev grids, k0 = pi * n (fixed
-points per wavelength, reference cli.py:300-307), y ~ N(0,1) + i N(0,1)
-(seed 0), reference default IFGF parameters.  Default n = 4 (38,400
-unknowns).
+Default workload: BASELINE.json configs[4] (cfg 5, the north-star config):
+unit dielectric sphere, eps_r = 2.25, k0 = 32 pi, 6 x 45^2 patches on 10x10
+Chebyshev grids = 1,215,000 points = 4,860,000 unknowns; y ~ N(0,1) +
+i N(0,1) (seed 0); the reference's default IFGF parameters.  Other configs:
+--n-refine / --k0-pi (cfg 1 / 2 family), --geometry superellipsoid|slab
+(cfg 3 / 4).
 
 --impl reference: the reference algorithm's CPU implementation (the numpy
-oracle restatement, `oracle/`, since the reference is Python and cannot be
-compiled) on this host's cores, on a bounded sample of the same workload.
+oracle restatement, `oracle/`: the reference is Python and cannot be
+compiled) on this host's cores.  The cfg-5 plan alone takes ~10 min of host
+numpy and a matvec hours, so the arm times one FULL matvec of the runnable
+sphere(4,10) (k0 = 4 pi) and bounded samples of it per step, and reports the
+workload's value as its algorithmic work / the port's achieved GFLOP/s
+(labelled "extrapolated").
 
-Multi-GPU (torchrun, N > 1): ONE matvec partitioned over the ranks
-(paper_2408_02274_b200/partition.py): Morton ranges of level-3 subtrees for
-the upward pass, patch ranges for near field and assembly, NCCL all-reduce
-of the far-field partials and of the result rows (strong scaling); the
-timed region is barrier-bracketed and the max over ranks is reported.
+Multi-GPU (torchrun, N > 1): one process per GPU; rank r builds and runs
+only its window of level-3 subtrees (far-field sources) and its target rows
+(near field), exchanging one NCCL reduce-scatter of the far-field partials
+and one all-gather of the result rows per matvec (partition.py).  The timed
+region is barrier-bracketed and the max over ranks is reported.
 """
 
 from __future__ import annotations
@@ -43,6 +48,8 @@ W_PROP = 75 * 75 * 16 * 4          # FLOP per (parent segment, child) instance
 W_COEF = 16 * (3 * 3 * 25 + 5 * 5 * 15 + 5 * 5 * 15) * 4   # K3 per segment
 W_EMIT = 2 * 75 * 16 * 4           # per (box, target) pair, x and x + h n
 W_LEAF = 128                       # per (node, source) pair (2 kernels x 8 ch)
+METRIC = "IFGF N-Muller matvec unknowns*matvec/s"
+COUNTS_FILE = ROOT / "profiles" / "work_counts.json"
 
 
 def parse():
@@ -51,20 +58,31 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--n-refine", type=int, default=4)
+    ap.add_argument("--n-refine", type=int, default=45)
     ap.add_argument("--k0-pi", type=float, default=None,
-                    help="k0 / pi (default n_refine: ~10 points per wavelength; cfg 5 is 45 / 32)")
+                    help="k0 / pi (sphere default: 32 at n_refine 45 (cfg 5), else n_refine)")
     ap.add_argument("--geometry", choices=["sphere", "superellipsoid", "slab"],
                     default="sphere", help="BASELINE cfg 1/2/5, cfg 3, cfg 4 bodies")
+    ap.add_argument("--moments", choices=["auto", "host", "device"], default="auto",
+                    help="singular moments: host restatement (reference-exact) or the "
+                         "plan-time GPU kernel; auto = device above 100k points")
+    ap.add_argument("--device-moments", action="store_true", help="= --moments device")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--device-moments", action="store_true",
-                    help="singular moments from the plan-time GPU kernel (large surfaces)")
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--max-rss-gb", type=float, default=0.0,
                     help="abort (kill this process) if host RSS exceeds this")
     ap.add_argument("--force-partition", action="store_true",
-                    help="use the partitioned (multi-GPU) operator even at N=1")
-    return ap.parse_args()
+                    help="run the multi-GPU (rank) operator and NCCL exchange even at N=1")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="one GPU: build and time only rank --emulate-rank's share of an "
+                         "R-way partition (per-rank work / memory; no exchange)")
+    ap.add_argument("--emulate-rank", type=int, default=0)
+    args = ap.parse_args()
+    if args.device_moments:
+        args.moments = "device"
+    if args.k0_pi is None and args.geometry == "sphere":
+        args.k0_pi = 32.0 if args.n_refine == 45 else float(args.n_refine)
+    return args
 
 
 def dist_env():
@@ -73,10 +91,10 @@ def dist_env():
 
 
 def workload(n_refine, k0_pi=None, geometry="sphere"):
-    """BASELINE configs: 'sphere' = cfg 1/2/5 family (sphere(n, 10), k0 = pi n
-    by default, eps_r 2.25); 'superellipsoid' = cfg 3 (|x/2|^4 + |y|^4 +
-    |z/0.5|^4 = 1, n x n subpatches per face on 12 x 12 grids, eps_r 4,
-    2a = 8 wavelengths -> k0 = 4 pi); 'slab' = cfg 4 (exponent-8
+    """BASELINE configs: 'sphere' = cfg 1/2/5 family (sphere(n, 10), eps_r
+    2.25; cfg 5 is n = 45 at k0 = 32 pi); 'superellipsoid' = cfg 3 (|x/2|^4 +
+    |y|^4 + |z/0.5|^4 = 1, n x n subpatches per face on 12 x 12 grids, eps_r
+    4, 2a = 8 wavelengths -> k0 = 4 pi); 'slab' = cfg 4 (exponent-8
     superellipsoid with half-extents 20 x 0.25 x 0.11 wavelengths, eps_r
     12.11, (16n, 2n, n) aspect-graded splits on 10 x 10 grids, wavelength 1
     -> k0 = 2 pi)."""
@@ -88,6 +106,8 @@ def workload(n_refine, k0_pi=None, geometry="sphere"):
         k0_pi = n_refine if k0_pi is None else k0_pi
         eps = 2.25
         name = f"sphere(n_refine={n_refine}, n_c=10) k0={k0_pi:g}pi eps_r=2.25"
+        if n_refine == 45 and k0_pi == 32:
+            name = "cfg5 " + name
     elif geometry == "superellipsoid":
         disc = surface.make_superellipsoid_surface(n_refine, 12, (2.0, 1.0, 0.5), 4.0)
         k0_pi = 4.0 if k0_pi is None else k0_pi
@@ -112,12 +132,20 @@ def workload(n_refine, k0_pi=None, geometry="sphere"):
     return disc, mats, y, name
 
 
+def use_device_moments(args, disc) -> bool:
+    return args.moments == "device" or (args.moments == "auto" and disc.n_points > 100_000)
+
+
+def _stage_logger():
+    t0 = time.time()
+    return lambda what: print(f"[plan] {what} {time.time() - t0:.1f}s", file=sys.stderr,
+                              flush=True)
+
+
 def plan_inputs(disc, mats, device_moments=False):
     from paper_2408_02274_b200 import nearfield, octree
     kmax = max(abs(mats.kappa_e), abs(mats.kappa_i))
-    t0 = time.time()
-    stage = lambda what: print(f"[plan] {what} {time.time() - t0:.1f}s", file=sys.stderr,
-                               flush=True)
+    stage = _stage_logger()
     tree = octree.build_box_tree(disc.points, kmax)
     stage("tree")
     hier = octree.build_cone_hierarchy(tree)
@@ -131,11 +159,13 @@ def plan_inputs(disc, mats, device_moments=False):
         mom = nearfield.compute_moments(disc, smap, cfg, mats.kappas)
     stage("moments")
     cp = nearfield.correction_pairs(disc, tree, smap)
+    stage("corrections")
     return tree, hier, smap, mom, cp
 
 
 def work_counts(tree, hier):
-    """Algorithmic FLOP per matvec from the plan."""
+    """Algorithmic FLOP per matvec from the plan (or a
+    window's plan: that rank's share)."""
     from paper_2408_02274_b200 import octree
     D = tree.depth
     prop = {}
@@ -148,6 +178,20 @@ def work_counts(tree, hier):
     return {"prop_by_level": prop, "prop": sum(prop.values()), "leaf": leaf,
             "leaf_coef": W_COEF * cl.n_segments, "emit": emit,
             "total": sum(prop.values()) + leaf + W_COEF * cl.n_segments + emit}
+
+
+def record_counts(name, counts, unknowns):
+    """Keep the workload's algorithmic work where the reference arm (which
+    cannot build the cfg-5 plan in minutes) finds it."""
+    try:
+        data = json.loads(COUNTS_FILE.read_text()) if COUNTS_FILE.exists() else {}
+        entry = {"total_flop": counts["total"], "prop_flop": counts["prop"],
+                 "unknowns": unknowns}
+        if data.get(name) != entry:
+            data[name] = entry
+            COUNTS_FILE.write_text(json.dumps(data, indent=1, sort_keys=True) + "\n")
+    except OSError:
+        pass
 
 
 class ClockSampler:
@@ -207,62 +251,128 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def cpu_baseline(disc, mats, y, inputs, budget_s, counts):
-    """The oracle (numpy restatement of the reference) on a bounded sample of
-    the same matvec: the far field of one Morton-contiguous block of level-3
-    subtrees holding 1/k of the modelled far-field work (the multi-GPU
-    partition of k parts, part 0), and every k-th near-field target group /
-    correction entry; the sample time is scaled by k."""
+def _threads():
+    return os.environ.get("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
+
+
+def oracle_sample(disc, mats, y, inputs, counts, budget_s, rate_guess=1.5e9):
+    """Time the oracle (numpy restatement of the reference) on a bounded
+    sample of one matvec: the far field of every `stride`-th box of level-3
+    subtree block 0 (1/k of the subtrees), every k*stride-th near-field
+    box / moment / correction entry.  Returns (sample wall s, sampled
+    fraction of the matvec, description)."""
     import oracle
     from paper_2408_02274_b200.partition import level3_partition
     tree, hier, smap, mom, cp = inputs
     op = oracle.OperatorData(disc, mats, smap, mom, cp.ell_idx, cp.src_idx, tree, hier)
-    # the numpy port runs ~1.5 GFLOP/s of the algorithmic count on 16 cores
-    k = max(1, int(round(counts["total"] / 1.5e9 / budget_s)))
-    k = min(k, tree.level(3).n_boxes)
-    part = level3_partition(tree, hier, k, disc.n_patches, disc.n_c)[0]
+    frac = min(1.0, budget_s * rate_guess / counts["total"])
+    n3 = tree.level(3).n_boxes
+    k = max(1, min(n3, int(round(1.0 / frac))))
+    stride = max(1, int(round(1.0 / (frac * k))))
+    parts = level3_partition(tree, hier, k, disc.n_patches, disc.n_c)
+    part = parts[0]
     ranges = {d: part.levels[d]["box"] for d in part.levels}
     t0 = time.perf_counter()
-    oracle.muller_apply(op, y, stride=k, box_ranges=ranges)
+    oracle.muller_apply(op, y, stride=k * stride, box_ranges=ranges, far_stride=stride)
     wall = time.perf_counter() - t0
-    est = wall * k
-    cores = os.cpu_count()
+    sampled = part.work / max(1e-300, sum(p.work for p in parts)) / stride
+    desc = (f"oracle/ (numpy restatement of the reference): far field of every "
+            f"{stride}-th box of level-3 subtrees {part.box3} ({sampled:.2e} of the "
+            f"modelled far-field work), every {k * stride}-th near-field box / moment / "
+            f"correction entry; sample wall {wall:.1f}s")
+    return wall, sampled, desc
+
+
+def cpu_baseline(disc, mats, y, inputs, budget_s, counts):
+    wall, frac, desc = oracle_sample(disc, mats, y, inputs, counts, budget_s)
+    est = wall / frac
     return {"value": 4 * disc.n_points / est, "unit": "unknowns*matvec/s",
-            "cores": cores, "kind": "port",
-            "sample": (f"oracle/ (numpy restatement of the reference): far field of "
-                       f"level-3 subtrees {part.box3} (1/{k} of the modelled work), "
-                       f"every {k}-th near-field box / patch group / correction entry; "
-                       f"sample wall {wall:.1f}s x{k} = estimated full matvec {est:.1f}s; "
-                       f"numpy/OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', cores)}")}
+            "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{desc} / {frac:.2e} = estimated full matvec {est:.1f}s; "
+                      f"numpy/OpenBLAS threads={_threads()}"}
 
 
 def run_reference(args):
+    """The reference arm (see module docstring): one full port matvec of
+    sphere(4,10) as calibration, then warmup + steps bounded samples of it;
+    value = the workload's algorithmic work at the port's achieved rate."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import numpy as np  # noqa: F401
-    disc, mats, y, name = workload(args.n_refine, args.k0_pi, args.geometry)
-    inputs = plan_inputs(disc, mats)
-    counts = work_counts(inputs[0], inputs[1])
-    per_step = min(15.0, 150.0 / max(1, args.steps + args.warmup))
-    vals = []
+    _, _, _, name = workload(args.n_refine, args.k0_pi, args.geometry)
+    counts_all = json.loads(COUNTS_FILE.read_text()) if COUNTS_FILE.exists() else {}
+    target = counts_all.get(name)
+    cal_disc, cal_mats, cal_y, cal_name = workload(4, 4.0, "sphere")
+    stage = _stage_logger()
+    inputs = plan_inputs(cal_disc, cal_mats)
+    cal_counts = work_counts(inputs[0], inputs[1])
+    stage("calibration plan")
+    if target is None:            # a workload the arm can plan itself
+        disc, mats, y, name = workload(args.n_refine, args.k0_pi, args.geometry)
+        if disc.n_points > 100_000:
+            print(json.dumps({"impl": "reference", "unavailable":
+                              f"no recorded work count for {name} (run the b200 arm once)"}))
+            return
+        tin = plan_inputs(disc, mats)
+        target = {"total_flop": work_counts(tin[0], tin[1])["total"],
+                  "unknowns": 4 * disc.n_points}
+    import oracle
+    op = oracle.OperatorData(cal_disc, cal_mats, inputs[2], inputs[3], inputs[4].ell_idx,
+                             inputs[4].src_idx, inputs[0], inputs[1])
+    t0 = time.perf_counter()
+    oracle.muller_apply(op, cal_y)
+    t_full = time.perf_counter() - t0
+    rate_full = cal_counts["total"] / t_full
+    stage(f"full port matvec {t_full:.1f}s")
+    per_step = min(10.0, 120.0 / max(1, args.steps + args.warmup))
+    rates, walls, desc = [], [], ""
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(disc, mats, y, inputs, per_step, counts)
+        wall, frac, desc = oracle_sample(cal_disc, cal_mats, cal_y, inputs, cal_counts,
+                                         per_step, rate_full)
         if i >= args.warmup:
-            vals.append(cb)
-    v = statistics.mean(c["value"] for c in vals)
-    t_step = 4 * disc.n_points / v
-    line = {"impl": "reference", "metric": "IFGF N-Muller matvec unknowns*matvec/s",
-            "value": v, "unit": "unknowns*matvec/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            rates.append(frac * cal_counts["total"] / wall)
+            walls.append(wall)
+    rate = statistics.mean(rates)
+    t_target = target["total_flop"] / rate
+    v = target["unknowns"] / t_target
+    line = {"impl": "reference", "metric": METRIC, "value": v,
+            "unit": "unknowns*matvec/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": statistics.mean(walls) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "c128/f64", "data": "synthetic (seeded N(0,1) densities)",
-            "config": {"workload": name, "unknowns": 4 * disc.n_points,
-                       "parallelism": "cpu"},
-            "cpu_baseline": {**vals[-1], "value": v},
+            "extrapolated": True,
+            "config": {"workload": name, "unknowns": target["unknowns"],
+                       "parallelism": "cpu",
+                       "algorithmic_gflop_per_matvec": target["total_flop"] / 1e9,
+                       "step": f"one bounded sample of a {cal_name} port matvec "
+                               f"(ms_per_step = its wall time)"},
+            "calibration": {"workload": cal_name, "full_matvec_s": t_full,
+                            "gflop": cal_counts["total"] / 1e9,
+                            "achieved_gflops": rate_full / 1e9,
+                            "sampled_gflops": rate / 1e9},
+            "cpu_baseline": {"value": v, "unit": "unknowns*matvec/s",
+                             "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{desc}; value = {target['total_flop'] / 1e9:.0f} "
+                                       f"GFLOP / {rate / 1e9:.2f} GFLOP/s (sampled rate; "
+                                       f"full {cal_name} matvec {t_full:.1f}s = "
+                                       f"{rate_full / 1e9:.2f} GFLOP/s); numpy/OpenBLAS "
+                                       f"threads={_threads()}"},
             "e2e": {"value": v, "unit": "unknowns*matvec/s",
                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _traffic(name):
+    """Per-launch DRAM bytes of K4 from an ncu --set full capture of this
+    workload (profiles/traffic_*.json), if one was committed."""
+    for f in sorted((ROOT / "profiles").glob("traffic_*.json")):
+        try:
+            d = json.loads(f.read_text())
+        except (OSError, ValueError):
+            continue
+        if d.get("workload") == name:
+            return d.get("propagate_bytes_per_launch"), f.name
+    return None, None
 
 
 def run_b200(args):
@@ -275,8 +385,9 @@ def run_b200(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    use_part = world > 1 or args.force_partition
-    if use_part:
+    use_rank = world > 1 or args.force_partition
+    emulate = args.emulate_ranks > 0
+    if use_rank:
         # keep rank 0's stdout to the one JSON line (NCCL prints its version
         # banner at NCCL_DEBUG=VERSION/INFO; an explicit setting is kept)
         os.environ.setdefault("NCCL_DEBUG", "WARN")
@@ -286,33 +397,47 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
     disc, mats, y, name = workload(args.n_refine, args.k0_pi, args.geometry)
+    dev_mom = use_device_moments(args, disc)
     t0 = time.time()
-    inputs = plan_inputs(disc, mats, args.device_moments)
-    tree, hier, smap, mom, cp = inputs
-    op = MullerOperator(disc, mats, smap, mom, (cp.ell_idx, cp.src_idx),
-                        tree=tree, hierarchy=hier)
-    counts = work_counts(tree, hier)
-    runner = op
-    if use_part:
-        # partitioned matvec: Morton level-3 subtrees per rank, NCCL sums
-        from paper_2408_02274_b200.octree import accumulation_plan
+    inputs = None
+    if use_rank or emulate:
+        from paper_2408_02274_b200 import octree
         from paper_2408_02274_b200.partition import (DistributedMullerOperator,
                                                      level3_partition)
-        parts = level3_partition(tree, hier, world, disc.n_patches, disc.n_c)
-        runner = DistributedMullerOperator(op, parts[rank])
-        mine = 0
-        for d in range(4, tree.depth + 1):
-            ap = accumulation_plan(tree, hier, d, geometry=False)
-            lo, hi = parts[rank].levels[d - 1]["seg"]
-            mine += W_PROP * int(ap.inst_off[hi] - ap.inst_off[lo]) + W_COEF * (hi - lo)
-        counts = dict(counts, prop=mine)
+        kmax = max(abs(mats.kappa_e), abs(mats.kappa_i))
+        tree = octree.build_box_tree(disc.points, kmax)
+        n_r, r = (args.emulate_ranks, args.emulate_rank) if emulate else (world, rank)
+        part = level3_partition(tree, None, n_r, disc.n_patches, disc.n_c)[r]
+        runner = DistributedMullerOperator(disc, mats, part, tree=tree,
+                                           exchange=False if emulate else None,
+                                           device_moments=dev_mom)
+        op = runner.op
+        counts = work_counts(runner.view, runner.hier)
+    else:
+        inputs = plan_inputs(disc, mats, dev_mom)
+        tree, hier, smap, mom, cp = inputs
+        op = MullerOperator(disc, mats, smap, mom, (cp.ell_idx, cp.src_idx),
+                            tree=tree, hierarchy=hier)
+        runner = op
+        counts = work_counts(tree, hier)
+        record_counts(name, counts, 4 * disc.n_points)
     t_plan = time.time() - t0
     dev = torch.device("cuda", local)
     yd = torch.from_numpy(y).to(dev)
     out = torch.empty_like(yd)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        if emulate:       # this rank's far + near work; no exchange
+            runner.far_phase(yd)
+            c = runner.xfar_mine.numel()
+            runner.xfar_mine.copy_(runner.xfar[r * c:(r + 1) * c])
+            runner.near_phase(yd)
+        else:
+            runner.apply_device(yd, out)
+
     for _ in range(max(args.warmup, 3)):
-        runner.apply_device(yd, out)
+        step()
     torch.cuda.synchronize()
     launches_per_step = runner.last_launches()
     # ---- timed device loop (events per step, L2 flushed between steps)
@@ -326,7 +451,7 @@ def run_b200(args):
         for i in range(args.steps):
             flush.zero_()
             evs[i][0].record()
-            runner.apply_device(yd, out)
+            step()
             evs[i][1].record()
         torch.cuda.synchronize()
     if world > 1:
@@ -335,13 +460,23 @@ def run_b200(args):
     ms = sum(ms_steps) / len(ms_steps)
     ktimes = kernel_times(op.plan)
     set_kernel_timing(op.plan, False)
+    rank_info = {"ms": ms, "plan_s": t_plan, "device_gib": op.plan.device_bytes() / 2**30,
+                 "prop_gflop": counts["prop"] / 1e9, "total_gflop": counts["total"] / 1e9}
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms, t_plan], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms, t_plan = float(t[0].item()), float(t[1].item())
+        gathered = [None] * world
+        dist.all_gather_object(gathered, rank_info)
+        rank_info = gathered
+        tot = torch.tensor([counts["total"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(tot)
+        total_flop = float(tot.item())
+    else:
+        total_flop = counts["total"]
     # ---- end to end through the host API
     y_host = np.ascontiguousarray(y)
-    if not use_part:
+    if not (use_rank or emulate):
         host_apply = op.apply                 # library host path (pinned staging)
     else:
         y_pin = torch.from_numpy(y_host).pin_memory()
@@ -350,7 +485,7 @@ def run_b200(args):
         def host_apply(v):
             y_pin.copy_(torch.from_numpy(v))
             yd.copy_(y_pin, non_blocking=True)
-            runner.apply_device(yd, out)
+            step()
             o_pin.copy_(out, non_blocking=True)
             torch.cuda.current_stream().synchronize()
             return o_pin.numpy().copy()
@@ -370,45 +505,48 @@ def run_b200(args):
         e2e_s = float(t.item())
     clocks = clk.summary()
     if rank != 0:
-        if use_part:
+        if use_rank:
             dist.barrier()
             dist.destroy_process_group()
         return
     unknowns = 4 * disc.n_points
     value = unknowns / (ms * 1e-3)        # one matvec over all ranks
     prop_ms, prop_n = ktimes["propagate"]
-    prop_flop = counts["prop"] * args.steps
-    achieved = prop_flop / (prop_ms * 1e-3) / 1e12 if prop_ms > 0 else None
-    traffic = None
-    tf = ROOT / "profiles" / f"traffic_n{args.n_refine}.json"
-    if args.geometry != "sphere":
-        tf = ROOT / "profiles" / f"traffic_{args.geometry}_n{args.n_refine}.json"
-    if tf.exists() and args.k0_pi is None:
-        traffic = json.loads(tf.read_text()).get("propagate_bytes_per_launch")
+    achieved = counts["prop"] * args.steps / (prop_ms * 1e-3) / 1e12 if prop_ms > 0 else None
+    traffic, tsrc = _traffic(name)
     kern = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
             for k, v in ktimes.items() if v[1]}
+    par = "single-gpu"
+    if use_rank:
+        par = (f"{world} ranks: level-3 subtree windows (sources) + target rows, "
+               "NCCL reduce-scatter of far partials + all-gather of result rows")
+    if emulate:
+        par = (f"emulated rank {args.emulate_rank} of {args.emulate_ranks} on one GPU "
+               "(its share of the work only; no exchange)")
     line = {
-        "metric": "IFGF N-Muller matvec unknowns*matvec/s", "value": value,
+        "metric": METRIC, "value": value,
         "unit": "unknowns*matvec/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c128/f64",
         "data": "synthetic (seeded N(0,1) densities; analytic sphere mesh)",
         "config": {"workload": name, "unknowns": unknowns, "points": disc.n_points,
-                   "depth": tree.depth, "segments": int(sum(hier.level(d).n_segments
-                                                            for d in hier.cone_levels)),
-                   "algorithmic_gflop_per_matvec": counts["total"] / 1e9,
+                   "depth": tree.depth,
+                   "algorithmic_gflop_per_matvec": total_flop / 1e9,
                    "l2": "flushed (256 MB write) before every timed step",
-                   "parallelism": (f"morton-level3-partition x{world} (NCCL all-reduce "
-                                   "of far field + result)") if use_part else "single-gpu",
+                   "parallelism": par,
+                   "moments": ("device kernel (beta_d at its ~1e-7 conditioning; "
+                               "tests/test_gpu_moments.py)" if dev_mom else
+                               "host restatement (reference-exact)"),
                    "plan_build_s": round(t_plan, 1),
+                   "device_plan_gib": round(op.plan.device_bytes() / 2**30, 2),
                    "geometry_on_device_levels": sorted(getattr(op.plan, "otf_levels", [])),
                    "stream_parts": int(getattr(op.plan, "stream_parts", 1) or 1)},
         "roofline": {"kernel": "propagate (K4: child->parent re-interpolation on "
-                               "FP64 DMMA + fused K3)",
+                               "FP64 DMMA + fused K3)" + (" of rank 0" if world > 1 else ""),
                      "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": (achieved / FP64_PEAK_TFLOPS
                                                  if achieved else None),
-                     "traffic": traffic,
+                     "traffic": traffic, "traffic_source": tsrc,
                      "flop_per_launch": counts["prop"] / max(1, prop_n // args.steps),
                      "ms_per_launch": prop_ms / max(1, prop_n),
                      "peak_source": "FP64 mma.sync m8n8k4 measured on B200 "
@@ -417,16 +555,19 @@ def run_b200(args):
                      "share_of_step": prop_ms / args.steps / ms},
         "kernels": kern,
         "e2e": {"value": unknowns / e2e_s, "unit": "unknowns*matvec/s",
-                "h2d_bytes_per_step": unknowns * 16, "d2h_bytes_per_step": unknowns * 16},
+                "h2d_bytes_per_step": unknowns * 16 * world,
+                "d2h_bytes_per_step": unknowns * 16 * world},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
     }
-    if world == 1 and not args.no_cpu_baseline and not args.device_moments:
+    if world > 1 or emulate:
+        line["ranks"] = rank_info if isinstance(rank_info, list) else [rank_info]
+    if world == 1 and not emulate and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(disc, mats, y, inputs, 15.0, counts)
-    if world == 1 and not args.no_gmres:
+    if world == 1 and not emulate and not args.no_gmres:
         line["gmres"] = gmres_cfg1()
     print(json.dumps(line), flush=True)
-    if use_part:
+    if use_rank:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define IFGFB_ABI_VERSION 5
+#define IFGFB_ABI_VERSION 6
 
 enum {
   IFGFB_OK = 0,
@@ -289,6 +289,15 @@ int ifgfb_arnoldi_mgs(double* basis, int64_t ld, int k, int64_t n, double* w,
 /* x = sum_{j<k} y[j] V[j]   (reference solver.py:92), y device k complex */
 int ifgfb_basis_combine(const double* basis, int64_t ld, int k, int64_t n,
                         const double* y, double* x, void* stream);
+/* The same two operations on a basis given as a host table of row pointers
+ * (rows[i] = V[i]; device memory or pinned host memory, which sm_100
+ * kernels address directly under UVA), so the Krylov basis can grow in
+ * chunks and spill to host memory instead of being preallocated
+ * (max_iter+1) x n on the device.  v_next receives w / h[k+1]. */
+int ifgfb_arnoldi_mgs_rows(const double* const* rows, int k, int64_t n, double* w,
+                           double* h, double* v_next, void* stream);
+int ifgfb_basis_combine_rows(const double* const* rows, int k, int64_t n,
+                             const double* y, double* x, void* stream);
 
 /* Per-kernel-class CUDA-event timing (recorded on the launching stream).
  * Classes: 0 leaf (K2+K3), 1 propagation (K4+K3), 2 emission (K5),
@@ -302,46 +311,69 @@ int ifgfb_plan_kernel_times(ifgfb_plan* plan, double* ms, int64_t* counts);
 /* Number of kernels launched by the last apply on this plan. */
 int64_t ifgfb_plan_last_launches(const ifgfb_plan* plan);
 
-/* ---- multi-GPU partition.  One plan per rank/GPU.  The
- * upward pass (leaf spectra, propagation, emission) is restricted to the
- * rank's Morton range of level-3 subtrees: per level, its segment rows and
- * its box-major emission pair range.  Near field and assembly are
- * restricted to a patch-aligned original-order target range.  With a
- * partition set, ifgfb_muller_far_phase leaves PARTIAL far-field sums in the
- * plan's far buffers (sum them over ranks, e.g. NCCL all-reduce, before the
- * near phase); ifgfb_muller_near_phase writes only the owned rows of the 4N
- * output.  Without a partition both phases cover everything and
- * far_phase + near_phase == ifgfb_muller_apply. */
+/* ---- streaming and multi-GPU ranks.
+ *
+ * Windows: a plan may be built for a Morton range of level-3 subtrees only
+ * (the host builds the window's cones, propagation and emission plans; the
+ * device plan is a complete plan over that forest: levels <= 2 carry no
+ * cones, reference ifgf.py:433, so no parent lies outside the window).  Its
+ * far field is then the PARTIAL sum of the window's sources at all N
+ * targets.
+ *
+ * Single-GPU streaming: run the upward pass as n_parts sequential passes,
+ * one per group of Morton-contiguous level-3 subtrees of the plan,
+ * accumulating the far field; the coefficient buffers shrink to the largest
+ * part, so levels larger than half the HBM fit (cfg 5 on one B200). */
 typedef struct {
   int32_t level;
-  int64_t seg_lo, seg_hi;     /* owned segment rows of this level */
-  int64_t pair_lo, pair_hi;   /* owned (box, cousin point) pairs of this level */
+  int64_t seg_lo, seg_hi;     /* segment rows of this level in the part */
+  int64_t pair_lo, pair_hi;   /* (box, cousin point) pairs of this level */
 } ifgfb_level_part;
 
 typedef struct {
   int32_t n_levels;                 /* entries for levels 3..depth */
   const ifgfb_level_part* levels;
-  int64_t target_lo, target_hi;     /* original order, multiples of n_c^2 */
+  int64_t target_lo, target_hi;     /* unused (kept for layout) */
 } ifgfb_partition_desc;
 
-int ifgfb_plan_set_partition(ifgfb_plan* plan, const ifgfb_partition_desc* part);
-/* Single-GPU streaming: run the upward pass as n_parts sequential passes,
- * one per group of Morton-contiguous level-3 subtrees (same descriptor as a
- * rank's partition; target ranges ignored), accumulating the far field.
- * The coefficient buffers shrink to the largest part, so levels larger than
- * half the HBM fit (e.g. cfg 2 at n_refine = 24 on one B200).  Exclusive
- * with ifgfb_plan_set_partition. */
 int ifgfb_plan_set_streaming(ifgfb_plan* plan, const ifgfb_partition_desc* parts,
                              int n_parts);
-/* density packing (all points) + far field of the owned subtrees */
+
+/* Rank mode (one process per GPU).  The plan is rank `rank`'s window (far
+ * field sources) and its near-field plan covers the owned targets
+ * [target_lo, target_hi) = [rank*chunk, min((rank+1)*chunk, N)) (original
+ * order, patch aligned); exchange buffers are point-major and padded to
+ * n_ranks*chunk rows so each rank's rows are one contiguous, equal-size
+ * chunk (NCCL reduce-scatter / all-gather):
+ *   ifgfb_muller_far_phase  -> xfar (n_ranks*chunk rows x 32 complex: the 8
+ *                              channels x 2 kernels far field, then the same
+ *                              at x + h n) = this rank's PARTIAL sums;
+ *   caller: reduce-scatter(sum) xfar -> xfar_mine (chunk rows);
+ *   ifgfb_muller_near_phase -> xout_mine (chunk rows x 4 complex: the owned
+ *                              result rows of y = [m1, m2, j1, j2]);
+ *   caller: all-gather xout_mine -> xout (n_ranks*chunk rows x 4);
+ *   ifgfb_rank_unpack       -> out (4N, the apply's y layout).
+ * Replaces the reference's single-process MullerOperator.apply
+ * (operators.py:399-403); the whole-plan entry points (ifgfb_muller_apply,
+ * _host, ifgfb_potentials, ifgfb_far_apply) refuse a rank plan. */
+typedef struct {
+  int64_t target_lo, target_hi;
+  int64_t chunk;
+  int32_t rank, n_ranks;
+} ifgfb_rank_desc;
+
+int ifgfb_plan_set_rank(ifgfb_plan* plan, const ifgfb_rank_desc* rank);
+int ifgfb_plan_rank_buffers(ifgfb_plan* plan, double** xfar, double** xfar_mine,
+                            double** xout_mine, double** xout, int64_t* chunk);
+int ifgfb_rank_unpack(ifgfb_plan* plan, double* out, void* stream);
+/* density packing (all points) + far field of the plan's sources (whole plan:
+ * into the internal far buffers; rank mode: into xfar) */
 int ifgfb_muller_far_phase(ifgfb_plan* plan, const double* y, void* stream);
-/* near field + assembly of the owned targets; rows outside are untouched */
+/* near field + assembly of the owned targets (whole plan: all, into out;
+ * rank mode: into xout_mine, out may be NULL).  Without a rank,
+ * far_phase + near_phase == ifgfb_muller_apply. */
 int ifgfb_muller_near_phase(ifgfb_plan* plan, const double* y, double* out,
                             void* stream);
-/* device pointers of the far-field buffers (each 16*N complex, layout
- * (8 ch, 2 kernels, N) original order) for the cross-rank reduction */
-int ifgfb_plan_far_buffers(ifgfb_plan* plan, double** far, double** far_disp,
-                           int64_t* n_complex);
 
 #ifdef __cplusplus
 }

@@ -12,7 +12,7 @@ baseline.  The product (``paper_2408_02274_b200``) never imports it.
 
 Pinning: the oracle is checked against golden vectors produced by the
 unmodified reference (``tests/golden/make_golden.py``; tests in
-``tests/test_oracle_golden.py``).  Plan inputs (tree, cone hierarchy,
+``tests/test_oracle.py``).  Plan inputs (tree, cone hierarchy,
 singular map, moments, correction lists) come from the framework's plan
 builder, whose arrays are checked bit-exact against the reference plan
 digests (``tests/test_plan.py``).

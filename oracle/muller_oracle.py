@@ -396,8 +396,13 @@ def _corrections(op, phi, kap, stride=1):
     return cs, cd
 
 
-def potentials(op: OperatorData, phi, stride: int = 1, box_ranges=None):
-    """(S (8,2,N), D (6,2,N)) (operators.py:321-350)."""
+def potentials(op: OperatorData, phi, stride: int = 1, box_ranges=None,
+               far_stride: int | None = None):
+    """(S (8,2,N), D (6,2,N)) (operators.py:321-350).  Bounded samples:
+    stride > 1 takes every stride-th near-field box / moment / correction,
+    box_ranges restricts the far field to a box window, far_stride samples
+    every far_stride-th box inside it (default: 1 with a window, else
+    stride)."""
     disc = op.disc
     kap = op.materials.kappas
     nc = disc.n_c
@@ -410,9 +415,20 @@ def potentials(op: OperatorData, phi, stride: int = 1, box_ranges=None):
     for p, grp in list(op.moments.groups.items())[::stride]:
         s_near[:, :, grp.targets] += np.einsum("kbmn,cmn->ckb", grp.beta_s, coeffs[:, p])
         d_near[:, :, grp.targets] += np.einsum("kbmn,cmn->ckb", grp.beta_d, coeffs[:, p])
+    csr = getattr(op.moments, "csr_blocks", None)
+    if csr is not None:   # moments in the singularity map's CSR order
+        smap = op.smap
+        tg = np.repeat(np.arange(smap.n_targets), np.diff(smap.offsets)) + getattr(
+            smap, "target_lo", 0)
+        for q in range(0, tg.size, stride):
+            blk = csr[q].reshape(4, nc, nc)
+            cf = coeffs[:, int(smap.patch_ids[q])]
+            s_near[:, :, tg[q]] += np.einsum("kmn,cmn->ck", blk[0:2], cf)
+            d_near[:, :, tg[q]] += np.einsum("kmn,cmn->ck", blk[2:4], cf)
+    if far_stride is None:
+        far_stride = 1 if box_ranges is not None else stride
     s_if, s_disp = far_field(op.tree, op.hier, phi * disc.weights, kap,
-                             disc.normals, op.fd_step,
-                             box_stride=1 if box_ranges is not None else stride,
+                             disc.normals, op.fd_step, box_stride=far_stride,
                              box_ranges=box_ranges)
     s_nb, d_nb = _neighbor_sums(op, phi, kap, stride)
     s_far = s_if + s_nb
@@ -424,7 +440,8 @@ def potentials(op: OperatorData, phi, stride: int = 1, box_ranges=None):
     return s_near + s_far, d_near[:6] + d_far
 
 
-def muller_apply(op: OperatorData, y, stride: int = 1, box_ranges=None):
+def muller_apply(op: OperatorData, y, stride: int = 1, box_ranges=None,
+                 far_stride: int | None = None):
     """y (4N) -> A y (operators.py:399-403 with apply_block :354-397).
 
     stride > 1 runs a bounded CPU-baseline sample (every stride-th box /
@@ -438,7 +455,7 @@ def muller_apply(op: OperatorData, y, stride: int = 1, box_ranges=None):
     phi = np.empty((8, n), dtype=complex)
     phi[0:3], phi[3:6] = j.T, m.T
     phi[6], phi[7] = _divergence(disc, j), _divergence(disc, m)
-    S, D = potentials(op, phi, stride, box_ranges)
+    S, D = potentials(op, phi, stride, box_ranges, far_stride)
     G = _grads(disc, S)
     nrm = disc.normals
     kap = mats.kappas

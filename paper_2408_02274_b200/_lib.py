@@ -94,6 +94,11 @@ class PartitionDesc(C.Structure):
                 ("target_lo", C.c_int64), ("target_hi", C.c_int64)]
 
 
+class RankDesc(C.Structure):
+    _fields_ = [("target_lo", C.c_int64), ("target_hi", C.c_int64),
+                ("chunk", C.c_int64), ("rank", C.c_int32), ("n_ranks", C.c_int32)]
+
+
 class MomentDesc(C.Structure):
     _fields_ = [("n_pairs", C.c_int64), ("target_xyz", _dp), ("target_nrm", _dp),
                 ("patch", C.POINTER(C.c_int32)), ("uv", _dp),
@@ -137,16 +142,19 @@ EXPORTS = {
                            C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_basis_combine": ([C.c_void_p, C.c_int64, C.c_int, C.c_int64,
                              C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
-    "ifgfb_plan_set_partition": ([C.c_void_p, C.POINTER(PartitionDesc)],
-                                 C.c_int),
+    "ifgfb_arnoldi_mgs_rows": ([C.c_void_p, C.c_int, C.c_int64, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "ifgfb_basis_combine_rows": ([C.c_void_p, C.c_int, C.c_int64, C.c_void_p,
+                                  C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_plan_set_streaming": ([C.c_void_p, C.POINTER(PartitionDesc),
                                   C.c_int], C.c_int),
     "ifgfb_muller_far_phase": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_muller_near_phase": ([C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p], C.c_int),
-    "ifgfb_plan_far_buffers": ([C.c_void_p, C.POINTER(C.c_void_p),
-                                C.POINTER(C.c_void_p), C.POINTER(C.c_int64)],
-                               C.c_int),
+    "ifgfb_plan_set_rank": ([C.c_void_p, C.POINTER(RankDesc)], C.c_int),
+    "ifgfb_plan_rank_buffers": ([C.c_void_p] + [C.POINTER(C.c_void_p)] * 4
+                                + [C.POINTER(C.c_int64)], C.c_int),
+    "ifgfb_rank_unpack": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_row_tiles_plan": ([C.c_int64, _ip, _ip, C.c_int64, _u8p, _u8p, _u8p,
                               _ip, C.c_int32, C.c_int32], C.c_int),
     "ifgfb_row_tiles_fill": ([C.c_int64, _ip, _ip, C.c_int64, _u8p, _u8p, _u8p,
@@ -157,6 +165,7 @@ EXPORTS = {
                          C.c_void_p], C.c_int),
 }
 
+ABI_VERSION = 6
 _lib = None
 
 
@@ -174,7 +183,7 @@ def load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.ifgfb_abi_version() != 5:
+    if lib.ifgfb_abi_version() != ABI_VERSION:
         raise RuntimeError("libifgfb200 ABI version mismatch")
     _lib = lib
     return lib

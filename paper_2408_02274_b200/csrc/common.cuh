@@ -255,7 +255,20 @@ struct Plan {
   double* dev_out = nullptr;    // 4N complex
   int64_t launches = 0;
   KTimer timer;
-  bool partitioned = false;
+  // rank mode (multi-GPU, ifgfb_plan_set_rank): the plan holds one rank's
+  // window of level-3 subtrees; the far phase leaves the PARTIAL far field of
+  // its sources in xfar (point-major, padded: n_ranks*chunk rows of 32
+  // complex = 16 far + 16 displaced), the caller reduce-scatters it into
+  // xfar_mine (chunk rows), the near phase writes the owned result rows
+  // into xout_mine (chunk rows of 4 complex), the caller all-gathers them
+  // into xout and ifgfb_rank_unpack writes the 4N y-layout vector.
+  bool rank_mode = false;
+  int rank = 0, n_ranks = 1;
+  int64_t chunk = 0;
+  double* xfar = nullptr;
+  double* xfar_mine = nullptr;
+  double* xout_mine = nullptr;
+  double* xout = nullptr;
   // streaming: per part, per level (index d) the ranges of one group of
   // level-3 subtrees; empty = single pass
   std::vector<std::vector<StreamRange>> stream_parts;
@@ -298,8 +311,10 @@ inline int dev_alloc(Plan& p, T** dst, size_t n) {
     if (rc_ != IFGFB_OK) return rc_; \
   } while (0)
 
+// pm_stride == 0: out / out_disp are (nch*nk, N) channel-major (original
+// order); pm_stride > 0: point-major, out[ell * pm_stride + m]
 int far_apply(Plan& p, const double* w, int nch, const double* kappas, int nk,
-              double* out, double* out_disp, cudaStream_t st);
+              double* out, double* out_disp, cudaStream_t st, int pm_stride = 0);
 int potentials(Plan& p, const double* phi, double* s_val, double* d_val,
                cudaStream_t st);
 int muller_apply(Plan& p, const double* y, double* out, cudaStream_t st);

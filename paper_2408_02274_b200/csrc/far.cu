@@ -735,14 +735,16 @@ __global__ void emit_reduce(int n, int pair_lo, int pair_hi,
   if (out_disp) out_disp[idx] = sd;
 }
 
-// out[(c*nk + k)][ell] = out_tree[iperm[ell]][c*NK + k]  (original order)
+// out[(c*nk + k)][ell] = out_tree[iperm[ell]][c*NK + k]  (original order);
+// pm_stride > 0: point-major out[ell * pm_stride + m] (rank exchange rows)
 __global__ void unpermute(int n, int ncols, const int* __restrict__ perm,
                           const double2* __restrict__ src,
-                          double2* __restrict__ dst) {
+                          double2* __restrict__ dst, int pm_stride) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * ncols) return;
   const int t = idx / ncols, m = idx % ncols;
-  dst[(size_t)m * n + perm[t]] = src[(size_t)t * NCOL + m];
+  const size_t o = pm_stride ? (size_t)perm[t] * pm_stride + m : (size_t)m * n + perm[t];
+  dst[o] = src[(size_t)t * NCOL + m];
 }
 
 // ------------------------------------------------------------ driver -----
@@ -814,7 +816,7 @@ static int ensure_aux(Plan& p) {
 
 template <int NK>
 static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
-                       double* out, double* out_disp, cudaStream_t st) {
+                       double* out, double* out_disp, cudaStream_t st, int pm_stride) {
   if (p.coef_cap == 0) IFGFB_RC(ensure_coef(p));
   IFGFB_RC(ensure_aux(p));
   EmitSync sync(p, st);
@@ -933,12 +935,12 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
   const int ncols = nch * NK;
   unpermute<<<(n * ncols + threads - 1) / threads, threads, 0, st>>>(
       n, ncols, p.perm, reinterpret_cast<const double2*>(p.out_tree),
-      reinterpret_cast<double2*>(out));
+      reinterpret_cast<double2*>(out), pm_stride);
   ++launches;
   if (out_disp) {
     unpermute<<<(n * ncols + threads - 1) / threads, threads, 0, st>>>(
         n, ncols, p.perm, reinterpret_cast<const double2*>(p.out_disp_tree),
-        reinterpret_cast<double2*>(out_disp));
+        reinterpret_cast<double2*>(out_disp), pm_stride);
     ++launches;
   }
   IFGFB_CUDA(cudaGetLastError());
@@ -949,14 +951,14 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
 int far_setup_kernels() { return init_constants(); }
 
 int far_apply(Plan& p, const double* w, int nch, const double* kappas, int nk,
-              double* out, double* out_disp, cudaStream_t st) {
+              double* out, double* out_disp, cudaStream_t st, int pm_stride) {
   if (nk == 1) {
     if (nch < 1 || nch > NCOL) { set_error("far_apply: 1 <= nch <= 16 for nk=1"); return IFGFB_ERR_ARG; }
-    return far_apply_t<1>(p, w, nch, kappas, out, out_disp, st);
+    return far_apply_t<1>(p, w, nch, kappas, out, out_disp, st, pm_stride);
   }
   if (nk == 2) {
     if (nch < 1 || nch > NCOL / 2) { set_error("far_apply: 1 <= nch <= 8 for nk=2"); return IFGFB_ERR_ARG; }
-    return far_apply_t<2>(p, w, nch, kappas, out, out_disp, st);
+    return far_apply_t<2>(p, w, nch, kappas, out, out_disp, st, pm_stride);
   }
   set_error("far_apply: nk must be 1 or 2");
   return IFGFB_ERR_ARG;

@@ -144,6 +144,7 @@ struct NearArgs {
   double fd_step;
   double2* s_val; double2* d_val;
   int t_lo, t_hi;        // owned targets (original order)
+  int far_pm;            // rank mode: far = xfar_mine, row (ell - t_lo) x 32
 };
 
 
@@ -267,10 +268,11 @@ __global__ void __launch_bounds__(128, IFGFB_NEAR_MINB) near_kernel(NearArgs a) 
   if (lane < 16) {
     const int c = lane >> 1;
     const size_t o = (size_t)lane * n + ell;   // (c*2+k)*N + ell
-    const double2 s_if = a.far[o];
+    const size_t of = a.far_pm ? (size_t)(ell - a.t_lo) * 32 + lane : o;
+    const double2 s_if = a.far[of];
     a.s_val[o] = cadd(near_s, csub(cadd(s_if, nb_s), cr_s));
     if (c < 6) {
-      const double2 sd = a.far_disp[o];
+      const double2 sd = a.far_pm ? a.far[of + 16] : a.far_disp[o];
       // numpy's complex / real: multiply by the reciprocal (Smith, rat = 0)
       const double scl = 1.0 / a.fd_step;
       const double2 d_if = make_double2(mul_rn(sd.x - s_if.x, scl),
@@ -288,6 +290,8 @@ struct AsmArgs {
   double omega;
   double2* out;
   int p0;                // first patch handled (partition)
+  int out_pm;            // rank mode: out = xout_mine, row (ell - t_lo) x 4
+  int t_lo;
 };
 
 __device__ __forceinline__ void cross3(const double* n, const double2* v, double2* o) {
@@ -406,7 +410,19 @@ __global__ void assemble_kernel(AsmArgs a) {
     o[3] = cadd(o[3], cscale(t2[c], rj[c]));
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) a.out[(size_t)q * n + ell] = o[q];
+  for (int q = 0; q < 4; ++q) {
+    const size_t oi = a.out_pm ? (size_t)(ell - a.t_lo) * 4 + q : (size_t)q * n + ell;
+    a.out[oi] = o[q];
+  }
+}
+
+// rank mode: y-layout out[q*N + ell] = gathered point-major rows xout[ell*4 + q]
+__global__ void rank_unpack_kernel(int n, const double2* __restrict__ xout,
+                                   double2* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= 4 * n) return;
+  const int ell = idx >> 2, q = idx & 3;
+  out[(size_t)q * n + ell] = xout[idx];
 }
 
 // ------------------------------------------------------------ drivers ----
@@ -426,7 +442,12 @@ static int near_launch(Plan& p, cudaStream_t st) {
               reinterpret_cast<const double2*>(p.far_disp),
               {p.kappa[0], p.kappa[2]}, {p.kappa[1], p.kappa[3]}, p.fd_step,
               reinterpret_cast<double2*>(p.s_val), reinterpret_cast<double2*>(p.d_val),
-              p.t_lo(), p.t_hi()};
+              p.t_lo(), p.t_hi(), 0};
+  if (p.rank_mode) {
+    na.far = reinterpret_cast<const double2*>(p.xfar_mine);
+    na.far_disp = nullptr;
+    na.far_pm = 1;
+  }
   const int warps_per_block = 4;
   const int nt = p.t_hi() - p.t_lo();
   if (nt <= 0) return IFGFB_OK;
@@ -438,8 +459,11 @@ static int near_launch(Plan& p, cudaStream_t st) {
   return IFGFB_OK;
 }
 
-// far field on phi * weights (operators.py:336-340), partial when partitioned
+// far field on phi * weights (operators.py:336-340); rank mode: the partial
+// sums of the window's sources into the point-major exchange rows
 static int far_launch(Plan& p, cudaStream_t st) {
+  if (p.rank_mode)
+    return far_apply(p, p.phiw, 8, p.kappa, 2, p.xfar, p.xfar + 2 * 16, st, 32);
   return far_apply(p, p.phiw, 8, p.kappa, 2, p.far_out, p.far_disp, st);
 }
 
@@ -476,7 +500,11 @@ static int assemble_launch(Plan& p, const double* y, double* out, cudaStream_t s
              make_double2(p.eps_e[0], p.eps_e[1]), make_double2(p.mu_e[0], p.mu_e[1]),
              make_double2(p.eps_i[0], p.eps_i[1]), make_double2(p.mu_i[0], p.mu_i[1]),
              {make_double2(p.kappa[0], p.kappa[1]), make_double2(p.kappa[2], p.kappa[3])},
-             p.omega, reinterpret_cast<double2*>(out), p0};
+             p.omega, reinterpret_cast<double2*>(out), p0, 0, p.t_lo()};
+  if (p.rank_mode) {
+    aa.out = reinterpret_cast<double2*>(p.xout_mine);
+    aa.out_pm = 1;
+  }
   const int tk = p.timer.begin(K_ASSEMBLE, st);
   assemble_kernel<<<p1 - p0, threads, sizeof(double2) * 16 * n2, st>>>(aa);
   p.timer.end(tk, st);
@@ -519,6 +547,13 @@ int ifgfb_plan_set_surface(ifgfb_plan* h, const ifgfb_surface_desc* d) {
   p.n_patches = d->n_patches;
   p.n_c = d->n_c;
   const size_t n = p.n, n2 = (size_t)d->n_c * d->n_c;
+  // pack / assemble stage 20 resp. 16 complex n_c x n_c tiles in dynamic
+  // shared memory: 54 KB at n_c = 13, 80 KB at n_c = 16 (above the 48 KB
+  // default from n_c = 13)
+  IFGFB_CUDA(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double2) * 20 * n2)));
+  IFGFB_CUDA(cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double2) * 16 * n2)));
   RC(dev_upload(p, &p.pts, d->points, 3 * n));
   RC(dev_upload(p, &p.nrm, d->normals, 3 * n));
   RC(dev_upload(p, &p.wq, d->weights, n));
@@ -584,14 +619,27 @@ int ifgfb_plan_set_near(ifgfb_plan* h, const ifgfb_near_desc* d) {
   return IFGFB_OK;
 }
 
-int ifgfb_potentials(ifgfb_plan* h, const double* phi, double* s_val,
-                     double* d_val, void* stream) {
-  CHECK_ARG(h && phi && s_val && d_val, "null argument");
-  Plan& p = h->p;
+// a partitioned plan computes rank-local partial sums: only the phase entry
+// points (ifgfb_muller_far_phase / _near_phase, driven by the collective
+// layer) may run it
+static int whole_plan_state(const Plan& p) {
   if (!p.finalized || !p.has_near) {
     set_error("plan has no surface/near-field data");
     return IFGFB_ERR_STATE;
   }
+  if (p.rank_mode) {
+    set_error("plan is one rank's share (partitioned across ranks): use the far/near "
+              "phase entry points with the rank exchange (DistributedMullerOperator)");
+    return IFGFB_ERR_STATE;
+  }
+  return IFGFB_OK;
+}
+
+int ifgfb_potentials(ifgfb_plan* h, const double* phi, double* s_val,
+                     double* d_val, void* stream) {
+  CHECK_ARG(h && phi && s_val && d_val, "null argument");
+  Plan& p = h->p;
+  RC(whole_plan_state(p));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   p.launches = 0;
   RC(pack_launch(p, nullptr, phi, st));
@@ -606,10 +654,7 @@ int ifgfb_potentials(ifgfb_plan* h, const double* phi, double* s_val,
 int ifgfb_muller_apply(ifgfb_plan* h, const double* y, double* out, void* stream) {
   CHECK_ARG(h && y && out, "null argument");
   Plan& p = h->p;
-  if (!p.finalized || !p.has_near) {
-    set_error("plan has no surface/near-field data");
-    return IFGFB_ERR_STATE;
-  }
+  RC(whole_plan_state(p));
   return muller_apply(p, y, out, static_cast<cudaStream_t>(stream));
 }
 
@@ -624,7 +669,7 @@ int ifgfb_muller_far_phase(ifgfb_plan* h, const double* y, void* stream) {
 }
 
 int ifgfb_muller_near_phase(ifgfb_plan* h, const double* y, double* out, void* stream) {
-  CHECK_ARG(h && y && out, "null argument");
+  CHECK_ARG(h && y && (out || h->p.rank_mode), "null argument");
   Plan& p = h->p;
   if (!p.finalized || !p.has_near) {
     set_error("plan has no surface/near-field data");
@@ -633,17 +678,67 @@ int ifgfb_muller_near_phase(ifgfb_plan* h, const double* y, double* out, void* s
   return muller_near_phase(p, y, out, static_cast<cudaStream_t>(stream));
 }
 
-int ifgfb_plan_far_buffers(ifgfb_plan* h, double** far, double** far_disp,
-                           int64_t* n_complex) {
-  CHECK_ARG(h && far && far_disp && n_complex, "null argument");
+int ifgfb_plan_set_rank(ifgfb_plan* h, const ifgfb_rank_desc* d) {
+  CHECK_ARG(h && d, "null argument");
   Plan& p = h->p;
-  if (!p.has_surface) {
-    set_error("plan has no surface data");
+  CHECK_ARG(p.finalized && p.has_near, "finalize the plan (with surface and near field) first");
+  CHECK_ARG(!p.rank_mode, "rank already set");
+  CHECK_ARG(d->n_ranks >= 1 && 0 <= d->rank && d->rank < d->n_ranks, "bad rank");
+  const int n2 = p.n_c * p.n_c;
+  CHECK_ARG(0 <= d->target_lo && d->target_lo <= d->target_hi && d->target_hi <= p.n,
+            "target range out of bounds");
+  CHECK_ARG(d->target_lo % n2 == 0 && d->target_hi % n2 == 0,
+            "target range must be patch aligned");
+  CHECK_ARG(d->target_lo == (int64_t)d->rank * d->chunk &&
+                d->target_hi - d->target_lo <= d->chunk,
+            "targets must be rank * chunk .. (rank + 1) * chunk (clipped to N)");
+  CHECK_ARG((int64_t)d->n_ranks * d->chunk >= p.n, "n_ranks * chunk must cover N");
+  const size_t rows = (size_t)d->n_ranks * d->chunk;
+  RC(dev_alloc(p, &p.xfar, rows * 32 * 2));
+  RC(dev_alloc(p, &p.xfar_mine, (size_t)d->chunk * 32 * 2));
+  RC(dev_alloc(p, &p.xout_mine, (size_t)d->chunk * 4 * 2));
+  RC(dev_alloc(p, &p.xout, rows * 4 * 2));
+  // padding rows (>= N) are never written: zero once
+  IFGFB_CUDA(cudaMemset(p.xfar, 0, rows * 32 * 2 * sizeof(double)));
+  IFGFB_CUDA(cudaMemset(p.xout_mine, 0, (size_t)d->chunk * 4 * 2 * sizeof(double)));
+  p.rank = d->rank;
+  p.n_ranks = d->n_ranks;
+  p.chunk = d->chunk;
+  p.part_t_lo = (int)d->target_lo;
+  p.part_t_hi = (int)d->target_hi;
+  p.rank_mode = true;
+  return IFGFB_OK;
+}
+
+int ifgfb_plan_rank_buffers(ifgfb_plan* h, double** xfar, double** xfar_mine,
+                            double** xout_mine, double** xout, int64_t* chunk) {
+  CHECK_ARG(h && xfar && xfar_mine && xout_mine && xout && chunk, "null argument");
+  Plan& p = h->p;
+  if (!p.rank_mode) {
+    set_error("plan has no rank (ifgfb_plan_set_rank)");
     return IFGFB_ERR_STATE;
   }
-  *far = p.far_out;
-  *far_disp = p.far_disp;
-  *n_complex = 16 * (int64_t)p.n;
+  *xfar = p.xfar;
+  *xfar_mine = p.xfar_mine;
+  *xout_mine = p.xout_mine;
+  *xout = p.xout;
+  *chunk = p.chunk;
+  return IFGFB_OK;
+}
+
+int ifgfb_rank_unpack(ifgfb_plan* h, double* out, void* stream) {
+  CHECK_ARG(h && out, "null argument");
+  Plan& p = h->p;
+  if (!p.rank_mode) {
+    set_error("plan has no rank (ifgfb_plan_set_rank)");
+    return IFGFB_ERR_STATE;
+  }
+  const int threads = 256;
+  rank_unpack_kernel<<<(4 * p.n + threads - 1) / threads, threads, 0,
+                       static_cast<cudaStream_t>(stream)>>>(
+      p.n, reinterpret_cast<const double2*>(p.xout), reinterpret_cast<double2*>(out));
+  p.launches += 1;
+  IFGFB_CUDA(cudaGetLastError());
   return IFGFB_OK;
 }
 
@@ -651,10 +746,7 @@ int ifgfb_muller_apply_host(ifgfb_plan* h, const double* y_host, double* out_hos
                             void* stream) {
   CHECK_ARG(h && y_host && out_host, "null argument");
   Plan& p = h->p;
-  if (!p.finalized || !p.has_near) {
-    set_error("plan has no surface/near-field data");
-    return IFGFB_ERR_STATE;
-  }
+  RC(whole_plan_state(p));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t bytes = sizeof(double) * 8 * (size_t)p.n;
   memcpy(p.host_stage, y_host, bytes);

@@ -320,7 +320,6 @@ int ifgfb_plan_set_streaming(ifgfb_plan* h, const ifgfb_partition_desc* parts,
   CHECK_ARG(h && parts && n_parts >= 1, "bad argument");
   Plan& p = h->p;
   CHECK_ARG(p.finalized, "finalize the plan before setting streaming");
-  CHECK_ARG(!p.partitioned, "streaming and a multi-GPU partition are exclusive");
   std::vector<std::vector<StreamRange>> sp(n_parts, std::vector<StreamRange>(p.depth + 1));
   size_t need = 1;
   for (int q = 0; q < n_parts; ++q) {
@@ -349,42 +348,6 @@ int ifgfb_plan_set_streaming(ifgfb_plan* h, const ifgfb_partition_desc* parts,
   p.stream_parts.swap(sp);
   (void)need;
   RC(ensure_coef(p));
-  return IFGFB_OK;
-}
-
-int ifgfb_plan_set_partition(ifgfb_plan* h, const ifgfb_partition_desc* d) {
-  CHECK_ARG(h && d, "null argument");
-  Plan& p = h->p;
-  CHECK_ARG(p.finalized, "finalize the plan before setting a partition");
-  CHECK_ARG(p.stream_parts.empty(), "streaming and a multi-GPU partition are exclusive");
-  CHECK_ARG(d->n_levels == std::max(0, p.depth - 2), "need one entry per level 3..depth");
-  for (int i = 0; i < d->n_levels; ++i) {
-    const ifgfb_level_part& lp = d->levels[i];
-    CHECK_ARG(lp.level >= 3 && lp.level <= p.depth, "partition level out of range");
-    Level& L = p.levels[lp.level];
-    CHECK_ARG(0 <= lp.seg_lo && lp.seg_lo <= lp.seg_hi && lp.seg_hi <= L.n_seg,
-              "segment range out of bounds");
-    CHECK_ARG(0 <= lp.pair_lo && lp.pair_lo <= lp.pair_hi && lp.pair_hi <= L.n_pairs,
-              "pair range out of bounds");
-    L.part_seg_lo = (int)lp.seg_lo;
-    L.part_seg_hi = (int)lp.seg_hi;
-    L.part_pair_lo = (int)lp.pair_lo;
-    L.part_pair_hi = (int)lp.pair_hi;
-    // tiles are sorted by segment row: owned rows -> contiguous tile range
-    L.part_tile_lo = (int)(std::lower_bound(L.etile_rows.begin(), L.etile_rows.end(),
-                                            (int)lp.seg_lo) - L.etile_rows.begin());
-    L.part_tile_hi = (int)(std::lower_bound(L.etile_rows.begin(), L.etile_rows.end(),
-                                            (int)lp.seg_hi) - L.etile_rows.begin());
-  }
-  const int n2 = p.n_c * p.n_c;
-  CHECK_ARG(0 <= d->target_lo && d->target_lo <= d->target_hi && d->target_hi <= p.n,
-            "target range out of bounds");
-  CHECK_ARG(n2 == 0 || (d->target_lo % n2 == 0 && d->target_hi % n2 == 0),
-            "target range must be patch aligned");
-  p.part_t_lo = (int)d->target_lo;
-  p.part_t_hi = (int)d->target_hi;
-  p.partitioned = true;
-  RC(ensure_coef(p));   // coefficient buffers: owned rows only
   return IFGFB_OK;
 }
 
@@ -430,6 +393,11 @@ int ifgfb_far_apply(ifgfb_plan* h, const double* w, int nch,
   Plan& p = h->p;
   if (!p.finalized) {
     set_error("plan not finalized");
+    return IFGFB_ERR_STATE;
+  }
+  if (p.rank_mode) {
+    set_error("plan is one rank's share: ifgfb_far_apply would return a rank-local "
+              "partial sum");
     return IFGFB_ERR_STATE;
   }
   double kap[4] = {kappas[0], kappas[1], nk > 1 ? kappas[2] : 0.0,

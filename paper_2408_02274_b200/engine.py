@@ -23,6 +23,28 @@ def device_stream():
     return torch.cuda.current_stream().cuda_stream
 
 
+class _StageLog:
+    """Plan-time stage timings to stderr when IFGFB_PLAN_LOG=1 (cumulative
+    seconds since creation, plus the stage's own share)."""
+
+    def __init__(self, name):
+        import os
+        import time
+        self.on = os.environ.get("IFGFB_PLAN_LOG", "0") not in ("", "0")
+        self.name = name
+        self.t0 = self.t = time.time()
+
+    def __call__(self, what):
+        if not self.on:
+            return
+        import sys
+        import time
+        now = time.time()
+        print(f"[{self.name}] {what} +{now - self.t:.1f}s ({now - self.t0:.1f}s)",
+              file=sys.stderr, flush=True)
+        self.t = now
+
+
 def _c(a, dtype):
     return np.ascontiguousarray(a, dtype=dtype)
 
@@ -33,7 +55,7 @@ class FarFieldPlan:
     def __init__(self, tree, hier, displaced_normals=None,
                  displaced_step: float = 1e-6, surface=None, near=None,
                  kappas=None, trim_host: bool = True,
-                 geometry_on_device: str | None = None):
+                 geometry_on_device: str | None = None, seam: str = "unwrap"):
         lib = _lib.load()
         if not torch.cuda.is_available():
             raise RuntimeError("CUDA device required (no CPU fallback)")
@@ -45,6 +67,7 @@ class FarFieldPlan:
         self.disp = displaced_normals is not None
         self.step = float(displaced_step)
         self.kappas = None if kappas is None else tuple(kappas)
+        self.seam = seam
         disp_t = None
         if self.disp:
             nrm = np.asarray(displaced_normals, dtype=float)
@@ -58,18 +81,22 @@ class FarFieldPlan:
         _lib.check(lib.ifgfb_plan_create(td, h), "ifgfb_plan_create")
         self._h = h
         self.stats = {"levels": {}}
+        self._log = log = _StageLog("farplan")
         try:
             # uploads are synchronous: host staging arrays are dropped per call
             for d in range(3, self.depth + 1):
                 self._add_level(lib, d)
                 self._keep = []
+            log("levels")
             self.otf_levels = self._choose_otf(geometry_on_device)
+            log(f"accumulation plans / otf {sorted(self.otf_levels)}")
             for d in range(4, self.depth + 1):
                 self._add_accum(lib, d, d in self.otf_levels)
                 self._keep = []
             for d in range(3, self.depth + 1):
                 self._add_emission(lib, d, disp_t)
                 self._keep = []
+                log(f"emission {d}")
             if surface is not None:
                 _lib.check(lib.ifgfb_plan_set_surface(self._h, surface),
                            "ifgfb_plan_set_surface")
@@ -166,9 +193,11 @@ class FarFieldPlan:
 
     def _add_accum(self, lib, d, otf=False):
         ap = accumulation_plan(self.tree, self.hier, d)
+        self._log(f"accum plan {d}")
         # crow rows are reproduced exactly as the reference's searchsorted
         # picks them (ifgf.py:743-746), including any inexact hit.
         row_order, row_cuts, tile_off, tiles = row_tiles(ap)
+        self._log(f"row tiles {d}")
         node_geom, node_r = (None, None) if otf else node_tables(ap)
         u8 = __import__("ctypes").POINTER(__import__("ctypes").c_uint8)
         a = dict(ng=None if otf else _c(node_geom, np.float64),
@@ -190,13 +219,14 @@ class FarFieldPlan:
             a["oc"].ctypes.data_as(u8))
         _lib.check(lib.ifgfb_plan_add_accum(self._h, desc),
                    f"ifgfb_plan_add_accum({d})")
+        self._log(f"accum upload {d}")
         st = self.stats["levels"].setdefault(d, {})
         st.update(types=int(ap.n_types), instances=int(ap.n_instances),
                   crow_misses=int(ap.crow_misses), tiles=int(tiles.shape[0]),
                   geometry_on_device=bool(otf))
 
     def _add_emission(self, lib, d, disp_t):
-        ep = emission_plan(self.tree, self.hier, d, disp_t)
+        ep = emission_plan(self.tree, self.hier, d, disp_t, self.seam)
         a = dict(row=_c(ep.row, np.int64), tg=_c(ep.target, np.int64),
                  g=_c(ep.geom, np.float64),
                  gd=None if ep.geom_disp is None else _c(ep.geom_disp,

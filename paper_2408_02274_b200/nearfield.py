@@ -51,7 +51,9 @@ class SingularQuadratureConfig:
 
 @dataclass
 class SingularityMap:
-    """CSR per target: singular/near patch ids, closest (u, v), distance."""
+    """CSR per target: singular/near patch ids, closest (u, v), distance.
+    A rank's map (classify_targets(..., target_range=(lo, hi))) covers the
+    on-surface targets lo..hi-1 only: local target j is point lo + j."""
 
     n_targets: int
     n_patches: int
@@ -60,6 +62,7 @@ class SingularityMap:
     patch_ids: np.ndarray
     closest_uv: np.ndarray
     dists: np.ndarray
+    target_lo: int = 0
 
     def singular_patches(self, ell: int) -> np.ndarray:
         return self.patch_ids[self.offsets[ell]:self.offsets[ell + 1]]
@@ -73,24 +76,37 @@ class SingularityMap:
 
 def classify_targets(disc: SurfaceDiscretization,
                      config: SingularQuadratureConfig | None = None,
-                     targets=None) -> SingularityMap:
-    """(target, patch) is singular when dist <= delta_factor * spacing_p."""
+                     targets=None, target_range=None) -> SingularityMap:
+    """(target, patch) is singular when dist <= delta_factor * spacing_p.
+
+    target_range=(lo, hi): the map of the surface points lo..hi-1 only (a
+    rank's targets).  Each patch still runs its closest-point search on its
+    FULL candidate batch (the golden-section loop runs until the whole batch
+    converges, so a point's (u, v) depends on its batch), hence the rank's
+    rows equal the full map's rows bit for bit; patches with no candidate in
+    the range are skipped."""
     config = config or SingularQuadratureConfig()
     on_surface = targets is None
+    t0, t1 = 0, None
     pts = disc.points if on_surface else np.atleast_2d(
         np.asarray(targets, dtype=float))
-    n_t = pts.shape[0]
+    if on_surface and target_range is not None:
+        t0, t1 = (int(v) for v in target_range)
+        if not 0 <= t0 <= t1 <= disc.n_points:
+            raise ValueError("target range out of bounds")
+    t1 = pts.shape[0] if t1 is None else t1
+    n_t = t1 - t0
     delta = config.delta_factor * disc.max_spacing
     grid = cheb.nodes(disc.n_c)
     global _CLASSIFY_CTX
-    _CLASSIFY_CTX = (disc, pts, delta, grid, on_surface)
+    _CLASSIFY_CTX = (disc, pts, delta, grid, on_surface, t0, t1, _point_index(pts))
     found = [[] for _ in range(n_t)]
     # per-patch work is independent; entries are sorted per target below, so
     # the merge order does not matter (the golden-section loops are
     # Python-bound: processes when fork is available, else in-process)
     for hits in _map_patches(_classify_patch, disc.n_patches):
         for ell, ent in hits:
-            found[ell].append(ent)
+            found[ell - t0].append(ent)
     _CLASSIFY_CTX = None
     offsets = np.zeros(n_t + 1, dtype=np.int64)
     ids, uvs, ds = [], [], []
@@ -104,10 +120,20 @@ def classify_targets(disc: SurfaceDiscretization,
     return SingularityMap(n_t, disc.n_patches, delta, offsets,
                           np.asarray(ids, dtype=np.int32),
                           np.asarray(uvs, dtype=float).reshape(-1, 2),
-                          np.asarray(ds, dtype=float))
+                          np.asarray(ds, dtype=float), t0)
 
 
 _CLASSIFY_CTX = None
+
+
+def _point_index(pts):
+    """k-d tree over the targets for the per-patch candidate search (the
+    exact candidate test below is the reference's expression)."""
+    try:
+        from scipy.spatial import cKDTree
+    except ImportError:       # pragma: no cover - scipy is a dependency
+        return None
+    return cKDTree(pts)
 
 
 def _map_patches(fn, n_patches):
@@ -134,20 +160,30 @@ def _map_patches(fn, n_patches):
 
 
 def _classify_patch(p):
-    """Singular/near pairs of patch p (runs in a worker process)."""
-    disc, pts, delta, grid, on_surface = _CLASSIFY_CTX
+    """Singular/near pairs of patch p (runs in a worker process); targets
+    outside [t0, t1) are searched (same batch as the full map) but not
+    reported."""
+    disc, pts, delta, grid, on_surface, t0, t1, kd = _CLASSIFY_CTX
     patch = disc.patches[p]
     hits = []
-    lower = np.linalg.norm(pts - patch.center, axis=1) - patch.bound_radius
-    cand = np.nonzero(lower <= delta[p])[0]
-    if cand.size == 0:
+    if kd is not None:
+        reach = (patch.bound_radius + delta[p]) * (1.0 + 1e-9) + 1e-300
+        cand = np.sort(np.asarray(kd.query_ball_point(patch.center, reach), dtype=np.int64))
+        lower = np.linalg.norm(pts[cand] - patch.center, axis=1) - patch.bound_radius
+        cand = cand[lower <= delta[p]]
+    else:
+        lower = np.linalg.norm(pts - patch.center, axis=1) - patch.bound_radius
+        cand = np.nonzero(lower <= delta[p])[0]
+    if cand.size == 0 or not np.any((cand >= t0) & (cand < t1)):
         return hits
+    mine = lambda ell: t0 <= ell < t1
     own = np.zeros(cand.size, dtype=bool)
     if on_surface:
         own = disc.patch_of[cand] == p
         for ell in cand[own]:
-            _, i, j = disc.decode_index(int(ell))
-            hits.append((int(ell), (p, grid[i], grid[j], 0.0)))
+            if mine(ell):
+                _, i, j = disc.decode_index(int(ell))
+                hits.append((int(ell), (p, grid[i], grid[j], 0.0)))
     rest = cand[~own]
     if rest.size == 0:
         return hits
@@ -156,11 +192,11 @@ def _classify_patch(p):
         pts[rest][:, None, :] - seed.reshape(-1, 3)[None, :, :], axis=-1),
         axis=1)
     rest = rest[dmin - disc.max_spacing[p] <= delta[p]]
-    if rest.size == 0:
+    if rest.size == 0 or not np.any((rest >= t0) & (rest < t1)):
         return hits
     u, v, dist = closest_point_batch(patch, pts[rest], seed)
     for ell, uu, vv, dd in zip(rest, u, v, dist):
-        if dd <= delta[p]:
+        if dd <= delta[p] and mine(ell):
             hits.append((int(ell), (p, uu, vv, dd)))
     return hits
 
@@ -378,11 +414,22 @@ class CorrectionPairs:
 
 def correction_pairs(disc: SurfaceDiscretization, tree,
                      smap: SingularityMap) -> CorrectionPairs:
+    """Entries per patch in ascending patch order (reference
+    quadrature.py:490-525); targets are global point ids (a rank's map
+    yields its targets' entries in the same order)."""
     coords = tree.point_level_coords(tree.depth)
     n2 = disc.n_c**2
     ells, srcs = [], []
-    for p in sorted({int(q) for q in smap.patch_ids}):
-        tg, _, _ = smap.pairs_for_patch(p)
+    # per-patch target lists in one pass (pairs_for_patch scans the whole
+    # map per patch)
+    order = np.argsort(smap.patch_ids, kind="stable")
+    bounds = np.searchsorted(smap.patch_ids[order],
+                             np.arange(disc.n_patches + 1))
+    tg_all = (np.repeat(np.arange(smap.n_targets, dtype=np.int64),
+                        np.diff(smap.offsets)) + smap.target_lo)
+    for p in np.nonzero(np.diff(bounds))[0]:
+        p = int(p)
+        tg = tg_all[order[bounds[p]:bounds[p + 1]]]
         s0 = p * n2
         sep = np.abs(coords[s0:s0 + n2][None, :, :] -
                      coords[tg][:, None, :]).max(-1)

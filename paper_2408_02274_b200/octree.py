@@ -34,7 +34,8 @@ from . import cheb
 __all__ = ["ETA", "IfgfConfig", "BoxTree", "LevelBoxes", "ConeLevel",
            "ConeHierarchy", "morton_encode", "morton_decode",
            "build_box_tree", "build_cone_hierarchy", "cone_coords",
-           "accumulation_plan", "emission_plan", "tree_stats"]
+           "accumulation_plan", "emission_plan", "tree_stats", "TreeWindow",
+           "tree_window", "window_view", "level3_ancestors"]
 
 ETA = np.sqrt(3.0) / 3.0
 
@@ -140,6 +141,8 @@ class LevelBoxes:
     nbr_off: np.ndarray
     cousin_idx: np.ndarray
     cousin_off: np.ndarray
+    box_lo: int = 0               # window views: global id of local box 0
+    full: "LevelBoxes | None" = None   # window views: the whole level
 
     @property
     def n_boxes(self) -> int:
@@ -257,6 +260,79 @@ def build_box_tree(points, kappa_max: float, padding: float = 0.01) -> BoxTree:
         lvl.cousin_idx = kids[order]
         lvl.cousin_off = _offsets_from_owner(box, lvl.n_boxes)
     return tree
+
+
+# ---------------------------------------------------------------------------
+# windows: Morton ranges of level-3 subtrees (multi-GPU ranks, streaming)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class TreeWindow:
+    """Level-3 boxes [box3[0], box3[1]) and their subtrees: per level d >= 3
+    the contiguous global box range ``ranges[d]`` (Morton order keeps every
+    subtree contiguous)."""
+
+    box3: tuple
+    ranges: dict
+
+
+def level3_ancestors(tree: BoxTree, d: int) -> np.ndarray:
+    """Level-3 ancestor (index into level 3) of every box at level d."""
+    return np.searchsorted(tree.level(3).codes,
+                           tree.level(d).codes >> np.uint64(3 * (d - 3)))
+
+
+def tree_window(tree: BoxTree, box3_lo: int, box3_hi: int) -> TreeWindow:
+    if tree.depth < 3:
+        raise ValueError("no cone levels: nothing to window")
+    n3 = tree.level(3).n_boxes
+    if not 0 <= box3_lo <= box3_hi <= n3:
+        raise ValueError("level-3 box range out of bounds")
+    ranges = {}
+    for d in range(3, tree.depth + 1):
+        anc = level3_ancestors(tree, d)
+        ranges[d] = (int(np.searchsorted(anc, box3_lo, side="left")),
+                     int(np.searchsorted(anc, box3_hi, side="left")))
+    return TreeWindow((int(box3_lo), int(box3_hi)), ranges)
+
+
+def _slice_csr(idx, off, lo, hi):
+    return idx[off[lo]:off[hi]], off[lo:hi + 1] - off[lo]
+
+
+def window_view(tree: BoxTree, win: TreeWindow) -> BoxTree:
+    """The tree restricted to a window's subtrees: levels >= 3 sliced to
+    their box ranges with LOCAL box ids (parent / child links re-based,
+    ``box_lo`` and ``full`` kept); neighbour / cousin lists keep GLOBAL box
+    ids; points, permutation and codes are shared.  Every plan builder
+    (cones, propagation, emission, device upload) runs on a view unchanged
+    and yields exactly the window's slice of the full plan."""
+    view = BoxTree(tree.origin, tree.root_side, tree.depth, tree.kappa_max,
+                   tree.perm, tree.iperm, tree.points, tree.point_codes)
+    for d in range(1, tree.depth + 1):
+        lvl = tree.level(d)
+        if d < 3:
+            view.levels.append(lvl)
+            continue
+        lo, hi = win.ranges[d]
+        sl = slice(lo, hi)
+        parent = lvl.parent[sl]
+        if d > 3:
+            parent = parent - win.ranges[d - 1][0]
+        if d < tree.depth:
+            clo = win.ranges[d + 1][0]
+            cs, ce = lvl.child_start[sl] - clo, lvl.child_end[sl] - clo
+        else:
+            cs, ce = lvl.child_start[sl], lvl.child_end[sl]
+        nbr_idx, nbr_off = _slice_csr(lvl.nbr_idx, lvl.nbr_off, lo, hi)
+        cz_idx, cz_off = _slice_csr(lvl.cousin_idx, lvl.cousin_off, lo, hi)
+        view.levels.append(LevelBoxes(
+            level=d, side=lvl.side, codes=lvl.codes[sl], coords=lvl.coords[sl],
+            centers=lvl.centers[sl], pt_start=lvl.pt_start[sl],
+            pt_count=lvl.pt_count[sl], parent=parent, child_start=cs,
+            child_end=ce, nbr_idx=nbr_idx, nbr_off=nbr_off,
+            cousin_idx=cz_idx, cousin_off=cz_off, box_lo=lo, full=lvl))
+    return view
 
 
 # ---------------------------------------------------------------------------
@@ -415,12 +491,14 @@ def cone_counts(tree: BoxTree, config: IfgfConfig) -> dict:
 
 
 def _cousin_points(tree: BoxTree, d: int):
-    """CSR of the cousin points (tree order) of every box at level d."""
+    """CSR of the cousin points (tree order) of every box at level d
+    (cousin ids are global box ids, also in a window view)."""
     lvl = tree.level(d)
+    glob = lvl.full if lvl.full is not None else lvl
     cz, owner = _expand_ranges(lvl.cousin_off[:-1], lvl.cousin_off[1:])
     cz = lvl.cousin_idx[cz]
-    pts, p_own = _expand_ranges(lvl.pt_start[cz],
-                                lvl.pt_start[cz] + lvl.pt_count[cz])
+    pts, p_own = _expand_ranges(glob.pt_start[cz],
+                                glob.pt_start[cz] + glob.pt_count[cz])
     box = owner[p_own]
     return pts, _offsets_from_owner(box, lvl.n_boxes), box
 
@@ -885,8 +963,19 @@ class EmissionPlan:
         return self.row.size
 
 
+SEAM_MODES = ("unwrap", "reference")
+
+
 def emission_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
-                  disp_points_t: np.ndarray | None = None) -> EmissionPlan:
+                  disp_points_t: np.ndarray | None = None,
+                  seam: str = "unwrap") -> EmissionPlan:
+    """seam: how the displaced point's phi is taken.  "unwrap" (default)
+    keeps it on the undisplaced point's branch; "reference" takes it mod
+    2 pi exactly as reference ifgf.py:647-651 (parity runs at seam-crossing
+    configurations).  Rows whose displacement does not cross phi = 0 are
+    bitwise identical under both."""
+    if seam not in SEAM_MODES:
+        raise ValueError(f"seam must be one of {SEAM_MODES}")
     cl, lvl = hier.level(d), tree.level(d)
     tg = cl.cpt_idx
     box = np.repeat(np.arange(lvl.n_boxes, dtype=np.int64),
@@ -917,8 +1006,9 @@ def emission_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
         # sphere(12,10) on).  Keep the displaced phi on the undisplaced
         # point's branch.  Bitwise unchanged wherever the seam is not
         # crossed (every golden configuration).
-        pd = np.where(pd - ph > np.pi, pd - 2.0 * np.pi,
-                      np.where(ph - pd > np.pi, pd + 2.0 * np.pi, pd))
+        if seam == "unwrap":
+            pd = np.where(pd - ph > np.pi, pd - 2.0 * np.pi,
+                          np.where(ph - pd > np.pi, pd + 2.0 * np.pi, pd))
         gd = np.stack(local_coords(cl, flat, sd, td, pd) + (rd,), axis=1)
     return EmissionPlan(d, row, tg, geom, gd, misses)
 

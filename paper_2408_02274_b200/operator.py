@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _lib, cheb
-from .engine import FarFieldPlan, device_stream
+from .engine import FarFieldPlan, _StageLog, device_stream
 from .nearfield import (SingularQuadratureConfig, classify_targets,
                         compute_moments, compute_moments_device,
                         correction_pairs)
@@ -148,20 +148,24 @@ def _complex2(z) -> np.ndarray:
 
 
 def _near_desc(disc, tree, smap, moments, corr_ell, corr_src, keep):
-    """Per-target singular moment pairs and the signed direct list."""
+    """Per-target singular moment pairs and the signed direct list.  A
+    rank's map (smap.target_lo, smap.n_targets) yields entries for its
+    targets only; the per-target offsets stay full length (N + 1) with
+    empty ranges elsewhere, so the device indexes targets globally."""
     n, n_c = disc.n_points, disc.n_c
     n2 = n_c * n_c
+    t0 = int(getattr(smap, "target_lo", 0))
+    t1 = t0 + int(smap.n_targets)
     # ---- moments, per (target, patch) sorted by target then patch
     tg, pt, blocks = [], [], []
     csr = getattr(moments, "csr_blocks", None)
     if csr is not None:   # device moments, already in the map's CSR order
-        mom_off = _c(smap.offsets, np.int64)
         pt = _c(smap.patch_ids, np.int64)
         blocks = np.ascontiguousarray(csr)
-        tg = np.repeat(np.arange(n, dtype=np.int64), np.diff(mom_off))
+        tg = np.repeat(np.arange(t0, t1, dtype=np.int64), np.diff(smap.offsets))
     for p in sorted(moments.groups) if csr is None else ():
         grp = moments.groups[p]
-        tg.append(np.asarray(grp.targets, dtype=np.int64))
+        tg.append(np.asarray(grp.targets, dtype=np.int64) + t0)
         pt.append(np.full(grp.targets.size, p, dtype=np.int64))
         blk = np.stack([grp.beta_s[0], grp.beta_s[1], grp.beta_d[0],
                         grp.beta_d[1]], axis=1).reshape(-1, 4, n2)
@@ -173,19 +177,19 @@ def _near_desc(disc, tree, smap, moments, corr_ell, corr_src, keep):
                   else np.empty((0, 4, n2), complex))
         order = np.lexsort((pt, tg))
         tg, pt, blocks = tg[order], pt[order], np.ascontiguousarray(blocks[order])
-        mom_off = np.zeros(n + 1, dtype=np.int64)
-        np.cumsum(np.bincount(tg, minlength=n), out=mom_off[1:])
+    mom_off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(tg, minlength=n), out=mom_off[1:])
     # ---- + neighbour-box sources not on the target's singular patches
     d = tree.depth
     lvl = tree.level(d)
-    box_t = tree.point_boxes(d)                    # per tree slot
-    box_of = box_t[tree.iperm]                     # per original target
+    tgt = np.arange(t0, t1, dtype=np.int64)
+    box_of = np.searchsorted(lvl.codes, tree.point_codes[tree.iperm[tgt]])
     nb_lo = lvl.nbr_off[box_of]
     nb_hi = lvl.nbr_off[box_of + 1]
     cnt = nb_hi - nb_lo
-    own = np.repeat(np.arange(n), cnt)
+    own = np.repeat(tgt, cnt)
     starts = np.cumsum(cnt) - cnt
-    nb = lvl.nbr_idx[np.arange(own.size) - starts[own] + nb_lo[own]]
+    nb = lvl.nbr_idx[np.arange(own.size) - np.repeat(starts - nb_lo, cnt)]
     pc = lvl.pt_count[nb]
     own2 = np.repeat(own, pc)
     st2 = np.cumsum(pc) - pc
@@ -193,13 +197,15 @@ def _near_desc(disc, tree, smap, moments, corr_ell, corr_src, keep):
         lvl.pt_start[nb], pc)
     src = tree.perm[src_t]
     P = disc.n_patches
-    sing_key = (np.repeat(np.arange(n), np.diff(smap.offsets)) * P +
+    sing_key = (np.repeat(tgt, np.diff(smap.offsets)) * P +
                 smap.patch_ids.astype(np.int64))
     pair_key = own2 * P + disc.patch_of[src].astype(np.int64)
     keep_mask = ~np.isin(pair_key, sing_key)
     pos_t, pos_s = own2[keep_mask], src[keep_mask]
     # ---- - corrections
     neg_t = np.asarray(corr_ell, dtype=np.int64)
+    if neg_t.size and (neg_t.min() < t0 or neg_t.max() >= t1):
+        raise ValueError("correction targets outside the map's target range")
     neg_s = -np.asarray(corr_src, dtype=np.int64) - 1
     all_t = np.concatenate([pos_t, neg_t])
     all_s = np.concatenate([pos_s, neg_s])
@@ -213,7 +219,8 @@ def _near_desc(disc, tree, smap, moments, corr_ell, corr_src, keep):
                          _lib.dptr(blocks), dir_src.size, _lib.iptr(dir_off),
                          _lib.iptr(dir_src))
     return desc, {"moment_pairs": int(tg.size), "neighbor_entries":
-                  int(pos_t.size), "correction_entries": int(neg_t.size)}
+                  int(pos_t.size), "correction_entries": int(neg_t.size),
+                  "targets": (t0, t1)}
 
 
 def _surface_desc(disc, materials, fd_step, keep):
@@ -245,7 +252,12 @@ class MullerOperator:
     def __init__(self, disc, materials, smap, moments, corrections,
                  config: OperatorConfig = OperatorConfig(), tree=None,
                  hierarchy=None, stream_parts=None,
-                 geometry_on_device: str | None = None):
+                 geometry_on_device: str | None = None, seam: str = "unwrap",
+                 near_tree=None):
+        """seam: "unwrap" (default) or "reference" phi branch of the
+        displaced emission points (octree.emission_plan, DESIGN 2).
+        near_tree: the whole tree for the near-field neighbour lists when
+        ``tree`` is a window view (multi-GPU ranks); default ``tree``."""
         self.disc = disc
         self.materials = materials
         self.smap = smap
@@ -257,20 +269,23 @@ class MullerOperator:
         self.accelerated = True
         self.corrections_enabled = True
         keep = []
+        log = _StageLog("operator")
         corr_ell, corr_src = corrections
         surf = _surface_desc(disc, materials, config.fd_step, keep)
-        near, self.near_stats = _near_desc(disc, tree, smap, moments,
-                                           corr_ell, corr_src, keep)
+        near, self.near_stats = _near_desc(disc, tree if near_tree is None else near_tree,
+                                           smap, moments, corr_ell, corr_src, keep)
+        log("near-field description")
         self.plan = FarFieldPlan(tree, hierarchy, disc.normals,
                                  config.fd_step, surface=surf, near=near,
                                  kappas=materials.kappas,
-                                 geometry_on_device=geometry_on_device)
+                                 geometry_on_device=geometry_on_device, seam=seam)
         # memory: stream the upward pass over groups of level-3 subtrees when
         # two full coefficient levels do not fit (None = automatic)
         if stream_parts is None:
             self.plan.auto_stream()
         elif stream_parts > 1:
             self.plan.set_streaming(stream_parts)
+        log("device plan")
         del keep
         self._dev = torch.device("cuda")
 

@@ -103,3 +103,26 @@ def plan_matches_golden(name: str) -> bool:
     mine = framework_digests(inputs(name))
     ref = golden_digests(name)
     return all(str(mine[k]) == str(ref[k]) for k in ref)
+
+
+def golden_rows(name: str):
+    """Point subset at which a large fixture stores its per-point outputs
+    (c2n4 / c2n8: every 3rd / 8th point), else all points."""
+    z = golden(name)
+    return z["rows"] if "rows" in z else slice(None)
+
+
+def golden_weights(name: str):
+    """ifgf_apply input of a fixture: stored, or phi * weights rebuilt from y
+    (reference operators.py:336; c2n4 / c2n8 do not store it)."""
+    z = golden(name)
+    if "weights" in z:
+        return z["weights"]
+    from paper_2408_02274_b200.operator import DensityBlock
+    disc = inputs(name)["disc"]
+    n = disc.n_points
+    y = z["y"]
+    t1, t2 = disc.tangent1, disc.tangent2
+    m = y[0:n, None] * t1 + y[n:2 * n, None] * t2
+    j = y[2 * n:3 * n, None] * t1 + y[3 * n:, None] * t2
+    return DensityBlock.from_currents(disc, j, m).values * disc.weights

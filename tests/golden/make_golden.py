@@ -5,7 +5,7 @@ the committed .npz outputs travel to the GPU hosts.
 Usage:  python tests/golden/make_golden.py [s1] [c1] [c1gmres] [rand]
 
 Fixtures (complex arrays stored as complex128):
-  <name>.npz
+  <name>.npz (s1, c1, se1, sl1, c2n4, c2n8)
     plan_digest_*   sha256 of every plan integer array (tree, cones,
                     accumulation types, emission rows, singular map,
                     correction lists) -- see plan_digests()
@@ -13,7 +13,9 @@ Fixtures (complex arrays stored as complex128):
     apply_y         MullerOperator.apply(y)            (operators.py:399)
     weights         phi * disc.weights fed to ifgf_apply (operators.py:336)
     far / far_disp  ifgf_apply(..., mode='vec', normals, 1e-6)  (ifgf.py:885)
-    far_seq_disp    same in 'seq' mode (reference's own noise floor)
+    rows            c2n4 / c2n8 only: the strided point subset at which
+                    far, far_disp, s_val, d_val are stored (weights omitted;
+                    they follow from y)
     s_val / d_val   potentials(dens)                   (operators.py:321)
     floor_*         reference self-consistency floors (linearity, vec/seq)
   c1_gmres.npz      GMRES tol 1e-6, plane wave exp(i k0 z) x-pol (cfg 1)
@@ -47,7 +49,15 @@ CONFIGS = {
     # short cfg-4-like slab: exponent-8 superellipsoid, half-extents
     # 2 x 0.25 x 0.11 wavelengths (wavelength 1), eps_r 12.11, (4, 2, 1) splits
     "sl1": ((4, 2, 1), 10, 2.0, 12.11),
+    # BASELINE cfg 2 sizes the reference can run here (k0 = pi * n_refine,
+    # reference cli.py:300-307): the benchmarked family at 38,400 and
+    # 153,600 unknowns
+    "c2n4": (4, 10, 4.0, 2.25),
+    "c2n8": (8, 10, 8.0, 2.25),
 }
+# large fixtures keep the per-point outputs (far, far_disp, potentials) on a
+# strided subset of points only (the `rows` array); y and apply_y are full
+ROW_STRIDE = {"c2n4": 3, "c2n8": 8}
 # non-sphere geometries: PATCHGRID files written by the framework's
 # generator (surface.make_superellipsoid_surface) and committed next to the
 # fixtures; both the reference and the framework load the same file with
@@ -174,10 +184,17 @@ def build(name):
                                                           op.hierarchy),
                        op.smap, cs.ell_idx, cs.src_idx,
                        _ref_emit_rows(ri, op.tree, op.hierarchy))
-    payload = dict(y=y, apply_y=ay, weights=w, far=far, far_disp=far_d,
-                   s_val=s_val, d_val=d_val, floor_linearity=floor_lin,
+    stride = ROW_STRIDE.get(name, 1)
+    rows = np.arange(0, n, stride)
+    sub = (lambda a: a) if stride == 1 else (lambda a: np.ascontiguousarray(a[..., rows]))
+    payload = dict(y=y, apply_y=ay, far=sub(far), far_disp=sub(far_d),
+                   s_val=sub(s_val), d_val=sub(d_val), floor_linearity=floor_lin,
                    t_apply_ref_container=t_apply,
                    config=np.array([nr if np.isscalar(nr) else 0, nc, k0pi, eps]))
+    if stride == 1:
+        payload["weights"] = w
+    else:
+        payload["rows"] = rows
     if name == "s1":
         op.config = type(op.config)(fd_step=op.config.fd_step, mode="seq")
         ay_seq = op.apply(y)

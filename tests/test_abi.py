@@ -38,7 +38,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_abi_version(lib):
-    assert lib.ifgfb_abi_version() == 5
+    assert lib.ifgfb_abi_version() == _lib.ABI_VERSION == 6
 
 
 STRUCTS = {
@@ -50,6 +50,7 @@ STRUCTS = {
     "ifgfb_near_desc": _lib.NearDesc,
     "ifgfb_level_part": _lib.LevelPart,
     "ifgfb_partition_desc": _lib.PartitionDesc,
+    "ifgfb_rank_desc": _lib.RankDesc,
 }
 
 

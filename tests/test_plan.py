@@ -12,8 +12,11 @@ from paper_2408_02274_b200.octree import (ETA, build_box_tree,
                                           morton_decode, morton_encode)
 
 
-@pytest.mark.parametrize("name", ["s1", "c1", "se1", "sl1"])
+@pytest.mark.parametrize("name", ["s1", "c1", "se1", "sl1", "c2n4", "c2n8"])
 def test_plan_digests_match_reference(name):
+    from _support import GOLDEN
+    if not (GOLDEN / f"{name}.npz").exists():
+        pytest.skip(f"{name} fixture not generated")
     mine = framework_digests(inputs(name))
     ref = golden_digests(name)
     bad = [k for k in ref if str(mine[k]) != str(ref[k])]
@@ -201,3 +204,45 @@ def test_row_tiles_rejects_bad_radius():
     ap = octree.accumulation_plan(inp["tree"], inp["hier"], 4)
     with pytest.raises(ValueError):
         octree.row_tiles(ap, cut_radius=5)
+
+
+def test_seam_modes_bitwise_outside_crossings():
+    """The phi-seam fix of displaced emission points (octree.emission_plan,
+    DESIGN 2) changes only the rows whose displacement crosses phi = 0 of
+    the source box's cone.  seam="reference" equals a plain restatement of
+    reference ifgf.py:647-651 (phi mod 2 pi, the oracle's expression) bit
+    for bit; seam="unwrap" equals it bit for bit on every row that does not
+    cross, and differs by exactly one 2 pi branch in xp on the rows that do.
+    A large step (2e-3) forces crossings on cfg 1's sphere."""
+    import oracle.muller_oracle as mo
+    disc = surface.make_sphere_surface(2, 10)
+    tree = build_box_tree(disc.points, 3 * np.pi)
+    hier = build_cone_hierarchy(tree)
+    disp = tree.points + 2e-3 * disc.normals[tree.perm]
+    n_cross = 0
+    for d in range(3, tree.depth + 1):
+        cl, lvl = hier.level(d), tree.level(d)
+        if cl.cpt_idx.size == 0:
+            continue
+        ref = octree.emission_plan(tree, hier, d, disp, seam="reference")
+        fix = octree.emission_plan(tree, hier, d, disp)
+        box = np.repeat(np.arange(lvl.n_boxes), np.diff(cl.cpt_off))
+        ctr = lvl.centers[box]
+        s, th, ph, r = mo._cone(tree.points[cl.cpt_idx] - ctr, lvl.side)
+        f = mo._flat(cl, s, th, ph)
+        sd, td, pd, rd = mo._cone(disp[cl.cpt_idx] - ctr, lvl.side)
+        want = np.stack(mo._local(cl, f, sd, td, pd) + (rd,), axis=1)
+        assert np.array_equal(ref.geom_disp, want)
+        assert np.array_equal(ref.geom, fix.geom) and np.array_equal(ref.row, fix.row)
+        cross = np.abs(pd - ph) > np.pi
+        assert np.array_equal(fix.geom_disp[~cross], ref.geom_disp[~cross])
+        if cross.any():
+            jump = 2.0 * (2.0 * np.pi / cl.delta_a)
+            dxp = np.abs(fix.geom_disp[cross, 2] - ref.geom_disp[cross, 2])
+            assert np.allclose(dxp, jump, rtol=1e-12)
+            assert np.array_equal(fix.geom_disp[cross][:, [0, 1, 3]],
+                                  ref.geom_disp[cross][:, [0, 1, 3]])
+        n_cross += int(cross.sum())
+    assert n_cross >= 5
+    with pytest.raises(ValueError):
+        octree.emission_plan(tree, hier, 3, disp, seam="bogus")

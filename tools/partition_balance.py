@@ -1,11 +1,13 @@
 #!/usr/bin/env python
-"""Load balance of the multi-GPU partition (DESIGN 7), measured on ONE GPU:
-for P logical ranks, each rank's plan (its Morton range of level-3 subtrees
-and its patch range) is built and its far phase and near phase are timed
-with CUDA events, one rank after another (no collective, nothing waits on
-another rank).  Reports per-rank times, max/mean imbalance and the bytes
-each NCCL all-reduce moves per matvec.  This is a projection input, not a
-multi-GPU measurement: the pool grants one GPU per call.
+"""Per-rank work and memory of the multi-GPU matvec (DESIGN 7), measured on
+ONE GPU: for P logical ranks, each rank's own plan (its window of level-3
+subtrees and its target rows, built from the tree-only partition exactly as
+a rank process builds it) is created, its far phase and near phase are
+timed with CUDA events, and it is freed before the next rank (one rank at a
+time: no collective, nothing waits on another rank).  Reports per-rank
+times, plan build times, device bytes, max/mean imbalance and the bytes each
+collective moves per matvec.  A projection input, not a multi-GPU
+measurement: the pool grants one GPU per call.
 
   python tools/partition_balance.py --n-refine 8 --ranks 1 2 4 8
 """
@@ -16,15 +18,11 @@ import argparse
 import gc
 import json
 import sys
+import time
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-
-
-class _NoComm:
-    def all_reduce(self, t, group=None):
-        pass
 
 
 def main():
@@ -33,65 +31,67 @@ def main():
     ap.add_argument("--k0-pi", type=float, default=None)
     ap.add_argument("--ranks", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--moments", choices=["host", "device"], default="device")
     args = ap.parse_args()
 
-    import numpy as np
     import torch
     import bench
-    from paper_2408_02274_b200 import _lib
+    from paper_2408_02274_b200 import octree
     from paper_2408_02274_b200.build import build
-    from paper_2408_02274_b200.engine import device_stream
-    from paper_2408_02274_b200.operator import MullerOperator
     from paper_2408_02274_b200.partition import DistributedMullerOperator, level3_partition
 
     build()
     torch.cuda.set_device(0)
     disc, mats, y_np, name = bench.workload(args.n_refine, args.k0_pi)
-    tree, hier, smap, mom, cp = bench.plan_inputs(disc, mats)
-    lib, st = _lib.load(), device_stream()
+    kmax = max(abs(mats.kappa_e), abs(mats.kappa_i))
+    tree = octree.build_box_tree(disc.points, kmax)
     y = torch.from_numpy(y_np).cuda()
-    n = disc.n_points
     rows = []
     for P in args.ranks:
-        parts = level3_partition(tree, hier, P, disc.n_patches, disc.n_c)
-        far_ms, near_ms = [], []
+        parts = level3_partition(tree, None, P, disc.n_patches, disc.n_c)
+        res = []
         for part in parts:
-            op = MullerOperator(disc, mats, smap, mom, (cp.ell_idx, cp.src_idx),
-                                tree=tree, hierarchy=hier, stream_parts=1)
-            dop = DistributedMullerOperator(op, part)
-            dop.dist = _NoComm()
-            out = torch.zeros_like(y)
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            best_f, best_n = 1e30, 1e30
-            for r in range(args.reps + 1):
+            t0 = time.time()
+            op = DistributedMullerOperator(disc, mats, part, tree=tree, exchange=False,
+                                           device_moments=args.moments == "device")
+            t_plan = time.time() - t0
+            far, near = [], []
+            for _ in range(args.reps + 1):
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                e[0].record()
+                op.far_phase(y)
+                e[1].record()
+                c = op.xfar_mine.numel()
+                op.xfar_mine.copy_(op.xfar[part.rank * c:(part.rank + 1) * c])
+                op.near_phase(y)
+                e[2].record()
                 torch.cuda.synchronize()
-                ev[0].record(torch.cuda.current_stream())
-                _lib.check(lib.ifgfb_muller_far_phase(op.plan.handle, y.data_ptr(), st), "far")
-                ev[1].record(torch.cuda.current_stream())
-                _lib.check(lib.ifgfb_muller_near_phase(op.plan.handle, y.data_ptr(),
-                                                       out.data_ptr(), st), "near")
-                ev[2].record(torch.cuda.current_stream())
-                torch.cuda.synchronize()
-                if r:
-                    best_f = min(best_f, ev[0].elapsed_time(ev[1]))
-                    best_n = min(best_n, ev[1].elapsed_time(ev[2]))
-            far_ms.append(best_f)
-            near_ms.append(best_n)
-            del dop, op
+                far.append(e[0].elapsed_time(e[1]))
+                near.append(e[1].elapsed_time(e[2]))
+            res.append({"rank": part.rank, "box3": part.box3, "targets": part.targets,
+                        "far_ms": min(far[1:]), "near_ms": min(near[1:]),
+                        "plan_s": round(t_plan, 1),
+                        "device_gib": round(op.device_bytes() / 2**30, 3),
+                        "modelled_work": part.work})
+            del op
             gc.collect()
             torch.cuda.empty_cache()
-        tot = [f + m for f, m in zip(far_ms, near_ms)]
-        rows.append({"ranks": P, "far_ms": [round(v, 3) for v in far_ms],
-                     "near_ms": [round(v, 3) for v in near_ms],
-                     "max_rank_ms": round(max(tot), 3), "mean_rank_ms": round(float(np.mean(tot)), 3),
-                     "imbalance_max_over_mean": round(max(tot) / float(np.mean(tot)), 3),
-                     "allreduce_bytes": {"far_partials": 2 * 16 * n * 16, "result_rows": 4 * n * 16}})
-        print(json.dumps(rows[-1]), flush=True)
-    base = rows[0]["max_rank_ms"] if rows and rows[0]["ranks"] == 1 else None
-    print(json.dumps({"workload": name, "unknowns": 4 * n,
-                      "projected_speedup_compute_only": {
-                          r["ranks"]: (round(base / r["max_rank_ms"], 2) if base else None)
-                          for r in rows}}), flush=True)
+        tot = [r["far_ms"] + r["near_ms"] for r in res]
+        chunk = parts[0].chunk
+        row = {"workload": name, "ranks": P, "per_rank": res,
+               "max_ms": max(tot), "mean_ms": sum(tot) / P,
+               "imbalance": max(tot) / (sum(tot) / P),
+               "reduce_scatter_mb": P * chunk * 32 * 16 / 1e6,
+               "all_gather_mb": P * chunk * 4 * 16 / 1e6}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    if rows and rows[0]["ranks"] == 1:
+        t1 = rows[0]["max_ms"]
+        for r in rows:
+            print(f"P={r['ranks']}: slowest rank {r['max_ms']:.2f} ms, imbalance "
+                  f"{r['imbalance']:.3f}, projected compute speedup {t1 / r['max_ms']:.2f}x, "
+                  f"max device {max(x['device_gib'] for x in r['per_rank']):.2f} GiB",
+                  flush=True)
 
 
 if __name__ == "__main__":
