@@ -132,6 +132,13 @@ typedef struct {
                                 coarse levels of large configurations) */
   const uint8_t* type_octant;/* n_types: child octant of each type (used
                                 when geometry_on_device) */
+  const uint8_t* group_id;   /* n_types*75: sigma group (index into the
+                                instance's crow list) of each parent node,
+                                or NULL.  Given group_id, tile_off / tiles
+                                may be NULL (n_tiles 0): the ring-staged
+                                kernel forms each warp's row tiles on the fly
+                                (same tiles as ifgfb_row_tiles_fill) and the
+                                plan holds no tile records */
 } ifgfb_accum_desc;
 
 /* ---- surface + operator data (reference SurfaceDiscretization,
@@ -374,6 +381,55 @@ int ifgfb_muller_far_phase(ifgfb_plan* plan, const double* y, void* stream);
  * far_phase + near_phase == ifgfb_muller_apply. */
 int ifgfb_muller_near_phase(ifgfb_plan* plan, const double* y, double* out,
                             void* stream);
+
+/* ---- plan-time cone hierarchy on the device (native plan builder,
+ * SURVEY 8(f) rank 1; replaces the relevance pass of
+ * build_cone_hierarchy, reference ifgf.py:417-482).  Per cone level:
+ *   begin -> mark_points (cousin points) -> mark_parents (nodes of the
+ *   parent level's relevant segments) -> ambiguous (evaluations whose
+ *   arccos / arctan2 sit within a few ulp of a segment edge: the caller
+ *   decides them with the reference's own expressions and returns them
+ *   through cones_set) -> finish (per-box counts -> seg_off) -> ids
+ *   (ascending segment ids per box) -> free.
+ * Every other floating-point step replays numpy's operation order with
+ * correctly rounded ops, so the result equals the host builder bit for
+ * bit.  Synchronous; host arrays in, host arrays out. */
+typedef struct ifgfb_cone_build ifgfb_cone_build;
+
+typedef struct {
+  int32_t n_s, n_a;            /* cone counts of the level */
+  double delta_s, delta_a;     /* ETA / n_s, pi / n_a */
+  double s_num;                /* np.sqrt(3.0) / 2.0 * side */
+  int64_t n_boxes;
+  int64_t amb_capacity;        /* edge cases buffered (>= 65536 used) */
+} ifgfb_cone_level_desc;
+
+typedef struct {
+  int64_t n_boxes;             /* boxes of the level (== the build's) */
+  const int64_t* inst_off;     /* n_boxes + 1: (box, parent row) instances */
+  const int64_t* row0;         /* n_boxes: first segment row of the parent box */
+  const int32_t* parent_box;   /* n_boxes */
+  int64_t n_parent_rows;
+  const int32_t* parent_seg_ids;   /* parent level segment ids */
+  int64_t n_parent_boxes;
+  const double* parent_centers;    /* n_parent_boxes x 3 */
+  const double* centers;           /* n_boxes x 3 */
+  int32_t pn_s, pn_a;              /* parent cone counts */
+  double ph;                       /* parent level h */
+  const double* parent_tabs;       /* s_nodes | sin_t | cos_t | sin_p | cos_p */
+} ifgfb_cone_parent_desc;
+
+int ifgfb_cones_begin(const ifgfb_cone_level_desc* level, ifgfb_cone_build** out);
+int ifgfb_cones_mark_points(ifgfb_cone_build* b, int64_t n_pairs, const int32_t* pair_box,
+                            const int32_t* pair_point, int64_t n_points,
+                            const double* points, const double* centers);
+int ifgfb_cones_mark_parents(ifgfb_cone_build* b, const ifgfb_cone_parent_desc* parents);
+int ifgfb_cones_ambiguous(ifgfb_cone_build* b, int64_t* n, int64_t* box, double* dx);
+int ifgfb_cones_set(ifgfb_cone_build* b, int64_t n, const int64_t* box, const int64_t* key);
+int ifgfb_cones_finish(ifgfb_cone_build* b, int64_t* seg_off, int64_t** reserved,
+                       int64_t* n_segments);
+int ifgfb_cones_ids(ifgfb_cone_build* b, const int64_t* seg_off, int64_t* seg_ids);
+int ifgfb_cones_free(ifgfb_cone_build* b);
 
 #ifdef __cplusplus
 }

@@ -63,7 +63,8 @@ class AccumDesc(C.Structure):
                 ("tile_off", _ip), ("n_tiles", C.c_int64),
                 ("tiles", C.POINTER(C.c_uint8)),
                 ("geometry_on_device", C.c_int32),
-                ("type_octant", C.POINTER(C.c_uint8))]
+                ("type_octant", C.POINTER(C.c_uint8)),
+                ("group_id", C.POINTER(C.c_uint8))]
 
 
 class SurfaceDesc(C.Structure):
@@ -97,6 +98,20 @@ class PartitionDesc(C.Structure):
 class RankDesc(C.Structure):
     _fields_ = [("target_lo", C.c_int64), ("target_hi", C.c_int64),
                 ("chunk", C.c_int64), ("rank", C.c_int32), ("n_ranks", C.c_int32)]
+
+
+class ConeLevelDesc(C.Structure):
+    _fields_ = [("n_s", C.c_int32), ("n_a", C.c_int32), ("delta_s", C.c_double),
+                ("delta_a", C.c_double), ("s_num", C.c_double), ("n_boxes", C.c_int64),
+                ("amb_capacity", C.c_int64)]
+
+
+class ConeParentDesc(C.Structure):
+    _fields_ = [("n_boxes", C.c_int64), ("inst_off", _ip), ("row0", _ip),
+                ("parent_box", C.POINTER(C.c_int32)), ("n_parent_rows", C.c_int64),
+                ("parent_seg_ids", C.POINTER(C.c_int32)), ("n_parent_boxes", C.c_int64),
+                ("parent_centers", _dp), ("centers", _dp), ("pn_s", C.c_int32),
+                ("pn_a", C.c_int32), ("ph", C.c_double), ("parent_tabs", _dp)]
 
 
 class MomentDesc(C.Structure):
@@ -151,6 +166,15 @@ EXPORTS = {
     "ifgfb_muller_far_phase": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_muller_near_phase": ([C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p], C.c_int),
+    "ifgfb_cones_begin": ([C.POINTER(ConeLevelDesc), C.POINTER(C.c_void_p)], C.c_int),
+    "ifgfb_cones_mark_points": ([C.c_void_p, C.c_int64, C.POINTER(C.c_int32),
+                                 C.POINTER(C.c_int32), C.c_int64, _dp, _dp], C.c_int),
+    "ifgfb_cones_mark_parents": ([C.c_void_p, C.POINTER(ConeParentDesc)], C.c_int),
+    "ifgfb_cones_ambiguous": ([C.c_void_p, C.POINTER(C.c_int64), _ip, _dp], C.c_int),
+    "ifgfb_cones_set": ([C.c_void_p, C.c_int64, _ip, _ip], C.c_int),
+    "ifgfb_cones_finish": ([C.c_void_p, _ip, C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
+    "ifgfb_cones_ids": ([C.c_void_p, _ip, _ip], C.c_int),
+    "ifgfb_cones_free": ([C.c_void_p], C.c_int),
     "ifgfb_plan_set_rank": ([C.c_void_p, C.POINTER(RankDesc)], C.c_int),
     "ifgfb_plan_rank_buffers": ([C.c_void_p] + [C.POINTER(C.c_void_p)] * 4
                                 + [C.POINTER(C.c_int64)], C.c_int),

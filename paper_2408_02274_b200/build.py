@@ -10,7 +10,8 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-SOURCES = ["plan.cu", "far.cu", "muller.cu", "gmres.cu", "moments.cu", "fields.cu", "tiles.cpp"]
+SOURCES = ["plan.cu", "far.cu", "muller.cu", "gmres.cu", "moments.cu", "fields.cu",
+           "planbuild.cu", "tiles.cpp"]
 TARGET = PKG / "libifgfb200.so"
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3",
               "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",

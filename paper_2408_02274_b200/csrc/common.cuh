@@ -181,7 +181,8 @@ struct Level {
   int max_groups = 0;                  // most child segments of one instance
   bool otf = false;                    // node geometry computed on the device
   unsigned char* type_octant = nullptr;  // per type (otf levels)
-  uint4* tiles = nullptr;      // 16-byte tile records
+  uint4* tiles = nullptr;      // 16-byte tile records (null: tile-free)
+  unsigned char* gid = nullptr;  // per type x NN: sigma group of each node
   double* node_geom = nullptr; // n_types*NN*3 (parent node order)
   double* node_r = nullptr;    // n_types*NN*2 (r_parent, r_child)
   double* ratio = nullptr;     // workspace n_types*NN*2 complex

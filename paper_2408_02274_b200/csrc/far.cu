@@ -13,6 +13,7 @@
 // / parent level ping-pong).
 #include "common.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace ifgfb {
@@ -60,7 +61,16 @@ __device__ __forceinline__ int node_row(const unsigned char* inv, int a, int b, 
 // In-place node values -> coefficients for one segment held in shared memory
 // (rows per node_row<OWNER>, NCOL complex columns, row stride RS complex):
 // three axis transforms (reference ifgf.py:502-522).
-template <bool OWNER, int RS = NCOL>
+// CTA-wide barrier of the threads running the transform: all threads
+// (__syncthreads) or, in the K4 ring kernel, the 160 consumer threads only
+// (named barrier 1; the producer warp never joins)
+template <bool NAMED>
+__device__ __forceinline__ void k3_sync() {
+  if (NAMED) asm volatile("bar.sync 1, %0;\n" :: "n"(32 * WARP_PARTS) : "memory");
+  else __syncthreads();
+}
+
+template <bool OWNER, int RS = NCOL, bool NAMED = false>
 __device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, int nthr) {
   for (int task = tid; task < PA * PA * NCOL; task += nthr) {
     const int bc = task / NCOL, m = task % NCOL;
@@ -79,7 +89,7 @@ __device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, in
       V[node_row<OWNER>(inv, a, b, c) * RS + m] = s;
     }
   }
-  __syncthreads();
+  k3_sync<NAMED>();
   for (int task = tid; task < PS * PA * NCOL; task += nthr) {
     const int ac = task / NCOL, m = task % NCOL;
     const int a = ac / PA, c = ac % PA;
@@ -97,7 +107,7 @@ __device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, in
       V[node_row<OWNER>(inv, a, b, c) * RS + m] = s;
     }
   }
-  __syncthreads();
+  k3_sync<NAMED>();
   for (int task = tid; task < PS * PA * NCOL; task += nthr) {
     const int ab = task / NCOL, m = task % NCOL;
     const int a = ab / PA, b = ab % PA;
@@ -115,7 +125,7 @@ __device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, in
       V[node_row<OWNER>(inv, a, b, c) * RS + m] = s;
     }
   }
-  __syncthreads();
+  k3_sync<NAMED>();
 }
 
 // Write one segment's coefficients V[i][m] (rows per node_row<OWNER>, row
@@ -452,6 +462,7 @@ struct AccArgs {
   int row_end;           // one past the last parent row handled
   int rows_per_cta;      // consecutive parent rows per CTA
   OtfGeom o;             // OTF instantiation only
+  const unsigned char* gid;   // tile-free ring kernel: sigma group per (type, node)
 };
 
 // cp.async (LDGSTS) helpers: global -> shared without a register round trip
@@ -651,6 +662,315 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
   }
 }
 
+// ------------------------------------------------- K4, ring-staged ----
+// The same owner-computes propagation with the child coefficient blocks
+// staged in shared memory: a producer warp streams every (instance, sigma
+// group) block of the CTA's rows, in the order the owner warps consume them,
+// into a ring of NSLOT 19 KB slots with one cp.async.bulk (TMA, UBLKCP) per
+// block and an mbarrier per slot (full: transaction bytes landed; empty: all
+// five owner warps done with it).  Each block crosses L2 -> SMEM once per
+// CTA; the owner warps read their B fragments with LDS.128 instead of each
+// pulling the block through L1 (round-1 ncu: L1 hit 30%, long-scoreboard the
+// second stall).  CTAs are persistent (rows blockIdx.x, +gridDim.x, ...), so
+// the producer fills the next row's first blocks during the K3 epilogue.
+constexpr int SEG_BYTES = SEG_DOUBLES * 8;   // 19,456 B, a multiple of 16
+
+struct __align__(16) InstStage {
+  uint4 tiles[NN];          // warp w: tiles[cuts[w] ..]
+  double2 ratio[NN * 2];    // [position][kappa]
+  double geom[NN * 3];      // [position][xs, xt, xp]
+};
+
+template <int NSLOT>
+struct __align__(128) RingSmem {
+  double ring[NSLOT][SEG_DOUBLES];
+  double2 acc[NN * NCOL];
+  InstStage stage[2];
+  unsigned long long full[NSLOT], empty[NSLOT];
+  unsigned char ord[NN], inv[NN], sgrp[NN];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" :: "r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+               :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA), completing transaction bytes on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ double2 lds128(const double2* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+
+// acc (+)= basis x block for a block resident in shared memory
+__device__ __forceinline__ void basis_times_smem(const BasisA& B, const double* C, int lane,
+                                                 double (&c0)[4], double (&c1)[4]) {
+  const double2* F = reinterpret_cast<const double2*>(C) + lane;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+#pragma unroll
+    for (int c = 0; c < PA; ++c) {
+      const int ks = 5 * q + c;
+      const double2 b01 = lds128(F + ks * 64), b23 = lds128(F + ks * 64 + 32);
+      const double av = B.tst[q] * B.tp[c];
+      dmma(c0[0], c1[0], av, b01.x);
+      dmma(c0[1], c1[1], av, b01.y);
+      dmma(c0[2], c1[2], av, b23.x);
+      dmma(c0[3], c1[3], av, b23.y);
+    }
+  }
+  const int tig = lane & 3;
+#pragma unroll
+  for (int st = 0; st < 4; ++st) {
+    const double us = __shfl_sync(0xffffffffu, B.u, (lane & ~3) | (st < 3 ? st : 0));
+    const double x = tig < 3 ? B.u : us, y = tig < 3 ? B.tp[st] : B.tp[PA - 1];
+    const double av = (tig < 3 || st < 3) ? x * y : 0.0;
+    const int ks = KMAIN + st;
+    const double2 b01 = lds128(F + ks * 64), b23 = lds128(F + ks * 64 + 32);
+    dmma(c0[0], c1[0], av, b01.x);
+    dmma(c0[1], c1[1], av, b01.y);
+    dmma(c0[2], c1[2], av, b23.x);
+    dmma(c0[3], c1[3], av, b23.y);
+  }
+}
+
+#ifndef IFGFB_RING_SLOTS
+#define IFGFB_RING_SLOTS 2
+#endif
+#ifndef IFGFB_RING_MINB
+#define IFGFB_RING_MINB 3
+#endif
+constexpr int RING_THREADS = 32 * (WARP_PARTS + 1);
+
+// TILEFREE: no tile records; each warp forms its row tiles per sigma group
+// from the group ids of its slots (ballot, runs of <= 8 in slot order: the
+// tiles ifgfb_row_tiles_fill would have written).
+template <int NK, bool OTF, int NSLOT, bool TILEFREE>
+__global__ void __launch_bounds__(RING_THREADS, IFGFB_RING_MINB) accum_ring_kernel(AccArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  RingSmem<NSLOT>& S = *reinterpret_cast<RingSmem<NSLOT>*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NSLOT; ++i) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], WARP_PARTS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == WARP_PARTS) {
+    // ---------------- producer: one lane streams the blocks in consumption order
+    if (lane == 0) {
+      uint32_t seq = 0;
+      for (int p = a.row0 + blockIdx.x; p < a.row_end; p += gridDim.x) {
+        const int i0 = a.inst_off[p], i1 = a.inst_off[p + 1];
+        for (int i = i0; i < i1; ++i) {
+          const int c0 = a.inst_crow_off[i], c1 = a.inst_crow_off[i + 1];
+          for (int c = c0; c < c1; ++c, ++seq) {
+            const int slot = seq % NSLOT;
+            const uint32_t use = seq / NSLOT;
+            if (use > 0) mbar_wait(&S.empty[slot], (use - 1) & 1);
+            mbar_expect_tx(&S.full[slot], SEG_BYTES);
+            bulk_g2s(S.ring[slot], a.coef_child + (size_t)__ldg(a.crow + c) * SEG_DOUBLES,
+                     SEG_BYTES, &S.full[slot]);
+          }
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- owner warps
+  const int grp = lane >> 2, tig = lane & 3;
+  uint32_t seq = 0;
+  for (int p = a.row0 + blockIdx.x; p < a.row_end; p += gridDim.x) {
+    const int pos0 = a.row_cuts[(size_t)p * (WARP_PARTS + 1) + warp];
+    const int nset = a.row_cuts[(size_t)p * (WARP_PARTS + 1) + warp + 1] - pos0;
+    double2* mine = S.acc + pos0 * NCOL;
+    const unsigned char* word = S.ord + pos0;
+    if (lane < nset) S.ord[pos0 + lane] = a.row_order[(size_t)p * NN + pos0 + lane];
+    for (int i = lane; i < nset * NCOL; i += 32) mine[i] = make_double2(0.0, 0.0);
+    const int i0 = a.inst_off[p], ni = a.inst_off[p + 1] - i0;
+    int my_t = 0, my_ks = 0, my_ke = 0, my_co = 0;
+    if (lane < ni) {
+      my_t = a.inst_type[i0 + lane];
+      if (!TILEFREE) {
+        my_ks = a.tile_off[(i0 + lane) * WARP_PARTS + warp];
+        my_ke = a.tile_off[(i0 + lane) * WARP_PARTS + warp + 1];
+      }
+    }
+    if (lane <= ni) my_co = a.inst_crow_off[i0 + lane];
+    __syncwarp();
+    // TILEFREE: sigma group of the lane's slot, loaded one instance ahead
+    auto slot_group = [&](int j) -> int {
+      if (!TILEFREE || j >= ni || lane >= nset) return 0xFF;
+      const int t = __shfl_sync(0xffffffffu, my_t, j);
+      return __ldg(a.gid + (size_t)t * NN + word[lane]);
+    };
+    auto stage_inst = [&](int j, InstStage& T) {
+      const int t = __shfl_sync(0xffffffffu, my_t, j);
+      const int ks = __shfl_sync(0xffffffffu, my_ks, j);
+      const int ke = __shfl_sync(0xffffffffu, my_ke, j);
+      const size_t tb = (size_t)t * NN;
+      if (!OTF) {
+        for (int e = lane; e < nset * 3; e += 32)
+          cp_async8(&T.geom[3 * pos0 + e], a.node_geom + (tb + word[e / 3]) * 3 + e % 3);
+        for (int e = lane; e < nset * NK; e += 32)
+          cp_async16(&T.ratio[NK * pos0 + e], a.ratio + (tb + word[e / NK]) * NK + e % NK);
+      }
+      if (!TILEFREE && lane < ke - ks) cp_async16(&T.tiles[pos0 + lane], a.tiles + ks + lane);
+      cp_async_commit();
+    };
+    __syncwarp();
+    int g_next = slot_group(0);
+    if (ni > 0) stage_inst(0, S.stage[0]);
+    for (int j = 0; j < ni; ++j) {
+      InstStage& T = S.stage[j & 1];
+      const int g_cur = g_next;
+      if (j + 1 < ni) {
+        stage_inst(j + 1, S.stage[(j + 1) & 1]);
+        g_next = slot_group(j + 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      const int ntile = __shfl_sync(0xffffffffu, my_ke - my_ks, j);
+      const int cs = __shfl_sync(0xffffffffu, my_co, j);
+      const int ng = __shfl_sync(0xffffffffu, my_co, j + 1) - cs;
+      if (OTF && TILEFREE) {
+        const int pseg = a.o.parent_seg_id[p];
+        const int oct = a.o.type_octant[__shfl_sync(0xffffffffu, my_t, j)];
+        if (lane < nset) {
+          const int cr = a.crow[cs + g_cur];
+          otf_node<NK>(a.o, pseg, oct, word[lane], a.o.child_seg_id[cr],
+                       &T.geom[(pos0 + lane) * 3], &T.ratio[(pos0 + lane) * NK]);
+        }
+        __syncwarp();
+      } else if (OTF) {   // slot -> sigma group from the tile records, then geometry
+        for (int e = lane; e < ntile * 8; e += 32) {
+          const uint4 tl = T.tiles[pos0 + (e >> 3)];
+          const int r = e & 7;
+          if (r < (int)((tl.x >> 8) & 0xff)) {
+            const int byte = 2 + r;
+            const unsigned w = byte < 4 ? tl.x : byte < 8 ? tl.y : tl.z;
+            S.sgrp[pos0 + ((w >> (8 * (byte & 3))) & 0xff)] = (unsigned char)(tl.x & 0xff);
+          }
+        }
+        __syncwarp();
+        const int pseg = a.o.parent_seg_id[p];
+        const int oct = a.o.type_octant[__shfl_sync(0xffffffffu, my_t, j)];
+        for (int e = lane; e < nset; e += 32) {
+          const int cr = a.crow[cs + S.sgrp[pos0 + e]];
+          otf_node<NK>(a.o, pseg, oct, word[e], a.o.child_seg_id[cr], &T.geom[(pos0 + e) * 3],
+                       &T.ratio[(pos0 + e) * NK]);
+        }
+        __syncwarp();
+      }
+      int k = 0;
+      for (int g = 0; g < ng; ++g, ++seq) {
+        const int slot = seq % NSLOT;
+        mbar_wait(&S.full[slot], (seq / NSLOT) & 1);
+        const double* blk = S.ring[slot];
+        unsigned mask = TILEFREE ? __ballot_sync(0xffffffffu, g_cur == g) : 0u;
+        for (;;) {
+          bool valid;
+          int slot_n;
+          if (TILEFREE) {
+            if (!mask) break;
+            // tile row grp = the grp-th owned slot of group g (slot order)
+            unsigned m = mask;
+            for (int i = 0; i < grp; ++i) m &= m - 1;
+            valid = m != 0u;
+            slot_n = valid ? __ffs(m) - 1 : __ffs(mask) - 1;
+            if (__popc(mask) > 8) {
+              for (int i = 0; i < 8; ++i) mask &= mask - 1;
+            } else {
+              mask = 0u;
+            }
+          } else {
+            if (k >= ntile) break;
+            const uint4 tl = T.tiles[pos0 + k];
+            if ((int)(tl.x & 0xff) != g) break;
+            slot_n = tile_slot(tl, grp, valid);
+            ++k;
+          }
+          const double* ng3 = T.geom + (pos0 + slot_n) * 3;
+          const BasisA B = make_basis<false>(ng3[0], ng3[1], ng3[2], tig);
+          double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+          basis_times_smem(B, blk, lane, c0, c1);
+          if (valid) {
+            const double2 r0 = T.ratio[(pos0 + slot_n) * NK];
+            const double2 r1 = NK > 1 ? T.ratio[(pos0 + slot_n) * NK + NK - 1] : r0;
+            double2* dst = mine + slot_n * NCOL;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              const int m = 4 * nt + tig;
+              const double2 v = cmul(make_double2(c0[nt], c1[nt]),
+                                     (NK > 1 && (tig & 1)) ? r1 : r0);
+              dst[m].x += v.x;
+              dst[m].y += v.y;
+            }
+          }
+          __syncwarp();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[slot]);
+      }
+    }
+    k3_sync<true>();
+    if (threadIdx.x < NN) S.inv[S.ord[threadIdx.x]] = (unsigned char)threadIdx.x;
+    k3_sync<true>();
+    to_coeffs_smem<true, NCOL, true>(S.acc, S.inv, threadIdx.x, 32 * WARP_PARTS);
+    store_segment<true>(a.coef_parent + (size_t)p * SEG_DOUBLES, S.acc, S.inv, threadIdx.x,
+                        32 * WARP_PARTS);
+    k3_sync<true>();
+  }
+}
+
+template <int NK, bool OTF, bool TILEFREE>
+static int launch_ring(const AccArgs& aa, int nrows, cudaStream_t st) {
+  constexpr int NS = IFGFB_RING_SLOTS;
+  auto kern = accum_ring_kernel<NK, OTF, NS, TILEFREE>;
+  const int smem = (int)sizeof(RingSmem<NS>);
+  static bool attr = false;
+  static int per_sm = 0, n_sm = 0;
+  if (!attr) {
+    IFGFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    IFGFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RING_THREADS, smem));
+    int dev = 0;
+    IFGFB_CUDA(cudaGetDevice(&dev));
+    IFGFB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    attr = true;
+  }
+  const int grid = std::max(1, std::min(nrows, std::max(1, per_sm) * n_sm));
+  kern<<<grid, RING_THREADS, smem, st>>>(aa);
+  return IFGFB_OK;
+}
+
 // ---------------------------------------------------------------- K5 ----
 struct EmitArgs {
   const int4* tiles; int tile0, tile_end;
@@ -803,6 +1123,16 @@ struct EmitSync {
   cudaStream_t emit_stream() const { return on ? p.aux : st; }
 };
 
+// K4 implementation: the ring-staged kernel (default) or the round-1
+// L1-streaming kernel (IFGFB_K4=l1), for A/B measurements
+static bool use_ring() {
+  static const bool ring = [] {
+    const char* v = std::getenv("IFGFB_K4");
+    return !(v && v[0] == 'l');
+  }();
+  return ring;
+}
+
 static int ensure_aux(Plan& p) {
   static const bool env_on = [] {
     const char* v = std::getenv("IFGFB_OVERLAP_EMIT");
@@ -913,9 +1243,17 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
             const int tk = p.timer.begin(K_ACCUM, st);
             const int grid = (nrows + IFGFB_ACC_ROWS - 1) / IFGFB_ACC_ROWS;
             const bool wide = L.max_groups > MAX_GROUPS;
-            if (L.otf) {
+            if (L.otf)
               aa.o = OtfGeom{L.type_octant, U.seg_id, U.tabs, U.n_s, U.n_a, U.h, L.seg_id,
                              L.n_a, L.delta_s, L.delta_a, L.side, {kr[0], kr[1]}, {ki[0], ki[1]}};
+            aa.gid = L.gid;
+            if (!L.tiles) {   // tile-free plan: the ring kernel forms the tiles
+              if (L.otf) IFGFB_RC((launch_ring<NK, true, true>(aa, nrows, st)));
+              else IFGFB_RC((launch_ring<NK, false, true>(aa, nrows, st)));
+            } else if (use_ring()) {
+              if (L.otf) IFGFB_RC((launch_ring<NK, true, false>(aa, nrows, st)));
+              else IFGFB_RC((launch_ring<NK, false, false>(aa, nrows, st)));
+            } else if (L.otf) {
               if (wide) accum_kernel<NK, true, true><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
               else accum_kernel<NK, false, true><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
             } else {

@@ -164,15 +164,17 @@ int ifgfb_plan_set_emission(ifgfb_plan* h, const ifgfb_emit_desc* e) {
   CHECK_ARG(np_ >= 0 && np_ < INT32_MAX, "pair count out of range");
   L.n_pairs = np_;
   L.has_disp = e->geom_disp != nullptr;
-  // sort pairs by segment row (stable) -> per-row tiles of <= 4 pairs
+  // sort pairs by segment row (stable counting sort, O(pairs + rows)) ->
+  // per-row tiles of <= 4 pairs
   std::vector<int> order(np_);
-  std::iota(order.begin(), order.end(), 0);
+  std::vector<int64_t> rstart((size_t)L.n_seg + 1, 0);
   for (int64_t i = 0; i < np_; ++i) {
     CHECK_ARG(e->row[i] >= 0 && e->row[i] < L.n_seg, "emission row out of range");
     CHECK_ARG(e->target[i] >= 0 && e->target[i] < p.n, "emission target out of range");
+    rstart[e->row[i] + 1]++;
   }
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int a, int b) { return e->row[a] < e->row[b]; });
+  for (int64_t r = 0; r < L.n_seg; ++r) rstart[r + 1] += rstart[r];
+  for (int64_t i = 0; i < np_; ++i) order[rstart[e->row[i]]++] = (int)i;
   std::vector<double4> g(np_), gd(L.has_disp ? np_ : 0);
   std::vector<int4> tiles;
   for (int64_t s = 0; s < np_; ++s) {
@@ -225,16 +227,21 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
   L.n_types = nt;
   std::vector<int> tmp;
   const int64_t ni = a->n_instances;
-  if (!to_i32(a->tile_off, ni * WARP_PARTS + 1, tmp, "tile_off")) return IFGFB_ERR_ARG;
-  CHECK_ARG(a->tile_off[ni * WARP_PARTS] == a->n_tiles, "tile_off end != n_tiles");
-  RC(dev_upload(p, &L.tile_off, tmp.data(), tmp.size()));
-  for (int64_t i = 0; i < a->n_tiles; ++i) {
-    const uint8_t* t = a->tiles + 16 * i;
-    CHECK_ARG(t[1] >= 1 && t[1] <= 8, "tile row count out of range");
-    for (int r = 0; r < t[1]; ++r)
-      CHECK_ARG(t[2 + r] < MAX_SET, "tile slot out of range");
+  const bool tile_free = a->tiles == nullptr;
+  CHECK_ARG(!tile_free || a->group_id != nullptr, "tiles or group_id required");
+  if (!tile_free) {
+    if (!to_i32(a->tile_off, ni * WARP_PARTS + 1, tmp, "tile_off")) return IFGFB_ERR_ARG;
+    CHECK_ARG(a->tile_off[ni * WARP_PARTS] == a->n_tiles, "tile_off end != n_tiles");
+    RC(dev_upload(p, &L.tile_off, tmp.data(), tmp.size()));
+    for (int64_t i = 0; i < a->n_tiles; ++i) {
+      const uint8_t* t = a->tiles + 16 * i;
+      CHECK_ARG(t[1] >= 1 && t[1] <= 8, "tile row count out of range");
+      for (int r = 0; r < t[1]; ++r)
+        CHECK_ARG(t[2 + r] < MAX_SET, "tile slot out of range");
+    }
+    RC(dev_upload(p, &L.tiles, reinterpret_cast<const uint4*>(a->tiles), (size_t)a->n_tiles));
   }
-  RC(dev_upload(p, &L.tiles, reinterpret_cast<const uint4*>(a->tiles), (size_t)a->n_tiles));
+  if (a->group_id) RC(dev_upload(p, &L.gid, a->group_id, (size_t)nt * NN));
   for (int64_t i = 0; i < a->n_parent_rows * NN; ++i)
     CHECK_ARG(a->row_order[i] < NN, "row_order entry out of range");
   RC(dev_upload(p, &L.row_order, a->row_order, (size_t)a->n_parent_rows * NN));
@@ -274,10 +281,22 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
   // capacities of the kernel's per-warp staging (far.cu WarpStage)
   for (int64_t r = 0; r < a->n_parent_rows; ++r)
     CHECK_ARG(a->inst_off[r + 1] - a->inst_off[r] <= 31, "more than 31 instances per row");
+  std::vector<int> type_groups(a->group_id ? nt : 0, -1);
   for (int64_t i = 0; i < ni; ++i) {
     const int64_t ng = a->inst_crow_off[i + 1] - a->inst_crow_off[i];
     CHECK_ARG(ng >= 0 && ng <= NN, "more than 75 child segments in one instance");
     L.max_groups = std::max(L.max_groups, (int)ng);
+    if (a->group_id) {   // every node's group indexes the instance's crow list
+      int& tg = type_groups[a->inst_type[i]];
+      if (tg < 0) {
+        int gmax = -1;
+        for (int n = 0; n < NN; ++n)
+          gmax = std::max(gmax, (int)a->group_id[a->inst_type[i] * NN + n]);
+        tg = gmax + 1;
+      }
+      CHECK_ARG(tg == ng, "group_id inconsistent with the instance's child rows");
+    }
+    if (tile_free) continue;
     for (int w = 0; w < WARP_PARTS; ++w) {
       const int64_t k0 = a->tile_off[i * WARP_PARTS + w], k1 = a->tile_off[i * WARP_PARTS + w + 1];
       CHECK_ARG(k1 - k0 >= 0 && k1 - k0 <= MAX_SET, "more than 23 tiles per (instance, warp)");

@@ -188,7 +188,9 @@ int ifgfb_row_tiles_plan(int64_t n_rows, const int64_t* inst_off, const int64_t*
                          int64_t n_types, const uint8_t* group_id, uint8_t* row_order,
                          uint8_t* row_cuts, int64_t* tile_off, int32_t cut_radius,
                          int32_t n_threads) {
-  if (n_rows < 0 || !inst_off || (n_rows && (!row_order || !row_cuts || !tile_off)) ||
+  // tile_off == NULL: order and cuts only (tile-free plans form the tiles on
+  // the device)
+  if (n_rows < 0 || !inst_off || (n_rows && (!row_order || !row_cuts)) ||
       cut_radius < 0 || cut_radius > MAX_R) {
     ifgfb::set_error("ifgfb_row_tiles_plan: bad arguments");
     return IFGFB_ERR_ARG;
@@ -211,6 +213,7 @@ int ifgfb_row_tiles_plan(int64_t n_rows, const int64_t* inst_off, const int64_t*
       uint8_t* ord = row_order + r * NN;
       uint8_t* cut = row_cuts + r * (WP + 1);
       if (!row_partition(in, r, cut_radius, ord, cut)) { bad = true; continue; }
+      if (!tile_off) continue;
       for (int64_t i = inst_off[r]; i < inst_off[r + 1]; ++i)
         for (int w = 0; w < WP; ++w)
           tile_off[(i - inst_off[0]) * WP + w + 1] = warp_tiles(in, i, ord, cut, w, nullptr);
@@ -220,6 +223,7 @@ int ifgfb_row_tiles_plan(int64_t n_rows, const int64_t* inst_off, const int64_t*
     ifgfb::set_error("ifgfb_row_tiles_plan: more than 8 instances in a parent row");
     return IFGFB_ERR_ARG;
   }
+  if (!tile_off) return IFGFB_OK;
   tile_off[0] = 0;
   for (int64_t k = 1; k <= ni * WP; ++k) tile_off[k] += tile_off[k - 1];
   return IFGFB_OK;

@@ -14,13 +14,26 @@ import torch
 
 from . import _lib
 from . import octree
-from .octree import accumulation_plan, emission_plan, node_tables, row_tiles
+from .octree import (accumulation_plan, emission_plan, node_tables, row_order_cuts,
+                     row_tiles)
 
 __all__ = ["FarFieldPlan", "ifgf_apply", "device_stream"]
 
 
 def device_stream():
     return torch.cuda.current_stream().cuda_stream
+
+
+def k4_mode() -> str:
+    """Propagation kernel (env IFGFB_K4): "free" (default: ring-staged
+    kernel, tiles formed on the device, no tile records in the plan),
+    "ring" (ring-staged kernel reading host-built tile records) or "l1"
+    (the round-1 kernel streaming child blocks through L1)."""
+    import os
+    m = os.environ.get("IFGFB_K4", "free")
+    if m not in ("free", "ring", "l1"):
+        raise ValueError(f"IFGFB_K4: unknown propagation kernel {m!r}")
+    return m
 
 
 class _StageLog:
@@ -168,7 +181,9 @@ class FarFieldPlan:
         for d in levels:
             ap = accumulation_plan(self.tree, self.hier, d)
             info[d] = (ap.n_types * self.TYPE_TABLE_BYTES, ap.n_types / max(1, ap.n_instances))
-            fixed += ap.n_instances * (12 * 16 + 16) + int(ap.inst_crow_off[-1]) * 4
+            tile_bytes = 0 if k4_mode() == "free" else 12 * 16 + 20   # records + tile_off
+            fixed += (ap.n_instances * (tile_bytes + 8) + int(ap.inst_crow_off[-1]) * 4
+                      + ap.n_types * 75)                                  # group ids
         pairs = [self.hier.level(d).cpt_idx.size for d in range(3, self.depth + 1)]
         fixed += sum(pairs) * 80 + max(pairs, default=0) * 2 * 16 * 16
         budget = 0.55 * torch.cuda.get_device_properties(
@@ -196,7 +211,12 @@ class FarFieldPlan:
         self._log(f"accum plan {d}")
         # crow rows are reproduced exactly as the reference's searchsorted
         # picks them (ifgf.py:743-746), including any inexact hit.
-        row_order, row_cuts, tile_off, tiles = row_tiles(ap)
+        tile_free = k4_mode() == "free"
+        if tile_free:
+            row_order, row_cuts = row_order_cuts(ap)
+            tile_off = tiles = None
+        else:
+            row_order, row_cuts, tile_off, tiles = row_tiles(ap)
         self._log(f"row tiles {d}")
         node_geom, node_r = (None, None) if otf else node_tables(ap)
         u8 = __import__("ctypes").POINTER(__import__("ctypes").c_uint8)
@@ -204,25 +224,29 @@ class FarFieldPlan:
                  nr=None if otf else _c(node_r, np.float64),
                  oc=np.ascontiguousarray(ap.type_octant, dtype=np.uint8),
                  ro=np.ascontiguousarray(row_order),
-                 rc=np.ascontiguousarray(row_cuts), to=_c(tile_off, np.int64),
-                 tl=np.ascontiguousarray(tiles),
+                 rc=np.ascontiguousarray(row_cuts),
+                 to=None if tile_free else _c(tile_off, np.int64),
+                 tl=None if tile_free else np.ascontiguousarray(tiles),
+                 gid=np.ascontiguousarray(ap.gid, dtype=np.uint8),
                  io=_c(ap.inst_off, np.int64), it=_c(ap.inst_type, np.int64),
                  ico=_c(ap.inst_crow_off, np.int64), cr=_c(ap.crow, np.int64))
-        self._hold(*a.values())
+        self._hold(*[v for v in a.values() if v is not None])
         desc = _lib.AccumDesc(
             d, ap.n_types, _lib.dptr(a["ng"]), _lib.dptr(a["nr"]),
             self.hier.level(d - 1).n_segments, a["ro"].ctypes.data_as(u8),
             a["rc"].ctypes.data_as(u8),
             _lib.iptr(a["io"]), ap.n_instances, _lib.iptr(a["it"]),
             _lib.iptr(a["ico"]), _lib.iptr(a["cr"]), _lib.iptr(a["to"]),
-            tiles.shape[0], a["tl"].ctypes.data_as(u8), int(otf),
-            a["oc"].ctypes.data_as(u8))
+            0 if tile_free else tiles.shape[0],
+            None if tile_free else a["tl"].ctypes.data_as(u8), int(otf),
+            a["oc"].ctypes.data_as(u8), a["gid"].ctypes.data_as(u8))
         _lib.check(lib.ifgfb_plan_add_accum(self._h, desc),
                    f"ifgfb_plan_add_accum({d})")
         self._log(f"accum upload {d}")
         st = self.stats["levels"].setdefault(d, {})
         st.update(types=int(ap.n_types), instances=int(ap.n_instances),
-                  crow_misses=int(ap.crow_misses), tiles=int(tiles.shape[0]),
+                  crow_misses=int(ap.crow_misses),
+                  tiles=None if tile_free else int(tiles.shape[0]),
                   geometry_on_device=bool(otf))
 
     def _add_emission(self, lib, d, disp_t):

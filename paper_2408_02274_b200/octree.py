@@ -35,7 +35,7 @@ __all__ = ["ETA", "IfgfConfig", "BoxTree", "LevelBoxes", "ConeLevel",
            "ConeHierarchy", "morton_encode", "morton_decode",
            "build_box_tree", "build_cone_hierarchy", "cone_coords",
            "accumulation_plan", "emission_plan", "tree_stats", "TreeWindow",
-           "tree_window", "window_view", "level3_ancestors"]
+           "tree_window", "window_view", "level3_ancestors", "level_tables"]
 
 ETA = np.sqrt(3.0) / 3.0
 
@@ -529,10 +529,88 @@ def _chunks(off: np.ndarray, budget: int):
         b = e
 
 
-def build_cone_hierarchy(tree: BoxTree,
-                         config: IfgfConfig = IfgfConfig()) -> ConeHierarchy:
+def level_tables(cl) -> np.ndarray:
+    """Node tables of a cone level in the device layout: s_nodes | sin_t |
+    cos_t | sin_p | cos_p, from numpy's own sin / cos of the node angles
+    (the values segment_nodes_xyz uses)."""
+    return np.ascontiguousarray(np.concatenate([
+        np.ravel(cl.s_nodes), np.ravel(np.sin(cl.ang_nodes_t)),
+        np.ravel(np.cos(cl.ang_nodes_t)), np.ravel(np.sin(cl.ang_nodes_p)),
+        np.ravel(np.cos(cl.ang_nodes_p))]), dtype=np.float64)
+
+
+def _device_relevant(tree, d, cl, pcl, cpts, cbox):
+    """Relevant (box, segment) set of level d on the device
+    (csrc/planbuild.cu), edge cases decided here with numpy's expressions:
+    identical to the host pass below.  Returns (seg_ids, seg_off, n_edge)."""
+    import ctypes
+    from . import _lib
+    lib = _lib.load()
+    lvl = tree.level(d)
+    nb = lvl.n_boxes
+    desc = _lib.ConeLevelDesc(cl.n_s, cl.n_a, cl.delta_s, cl.delta_a,
+                              float(np.sqrt(3.0) / 2.0 * lvl.side), nb, 1 << 20)
+    h = ctypes.c_void_p()
+    _lib.check(lib.ifgfb_cones_begin(ctypes.byref(desc), ctypes.byref(h)), "ifgfb_cones_begin")
+    i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)
+    p32 = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    try:
+        centers = np.ascontiguousarray(lvl.centers, dtype=np.float64)
+        if cpts.size:
+            cb, cp_ = i32(cbox), i32(cpts)
+            pts = np.ascontiguousarray(tree.points, dtype=np.float64)
+            _lib.check(lib.ifgfb_cones_mark_points(h, cpts.size, p32(cb), p32(cp_),
+                                                   pts.shape[0], _lib.dptr(pts),
+                                                   _lib.dptr(centers)),
+                       "ifgfb_cones_mark_points")
+        if pcl is not None:
+            up = tree.level(d - 1)
+            cnt = pcl.seg_off[lvl.parent + 1] - pcl.seg_off[lvl.parent]
+            inst_off = np.zeros(nb + 1, dtype=np.int64)
+            np.cumsum(cnt, out=inst_off[1:])
+            row0 = np.ascontiguousarray(pcl.seg_off[lvl.parent], dtype=np.int64)
+            pbox, pseg = i32(lvl.parent), i32(pcl.seg_ids)
+            pctr = np.ascontiguousarray(up.centers, dtype=np.float64)
+            tabs = level_tables(pcl)
+            pd = _lib.ConeParentDesc(nb, _lib.iptr(inst_off), _lib.iptr(row0), p32(pbox),
+                                     pseg.size, p32(pseg), up.n_boxes, _lib.dptr(pctr),
+                                     _lib.dptr(centers), pcl.n_s, pcl.n_a, pcl.h,
+                                     _lib.dptr(tabs))
+            _lib.check(lib.ifgfb_cones_mark_parents(h, ctypes.byref(pd)),
+                       "ifgfb_cones_mark_parents")
+        n = ctypes.c_int64()
+        _lib.check(lib.ifgfb_cones_ambiguous(h, ctypes.byref(n), None, None),
+                   "ifgfb_cones_ambiguous")
+        n_edge = n.value
+        if n_edge:
+            box = np.empty(n_edge, dtype=np.int64)
+            dx = np.empty((n_edge, 3))
+            _lib.check(lib.ifgfb_cones_ambiguous(h, ctypes.byref(n), _lib.iptr(box),
+                                                 _lib.dptr(dx)), "ifgfb_cones_ambiguous")
+            s, th, ph, _ = cone_coords(dx, np.zeros(3), lvl.side)
+            key = np.ascontiguousarray(seg_index(cl, s, th, ph), dtype=np.int64)
+            _lib.check(lib.ifgfb_cones_set(h, n_edge, _lib.iptr(box), _lib.iptr(key)),
+                       "ifgfb_cones_set")
+        seg_off = np.zeros(nb + 1, dtype=np.int64)
+        total = ctypes.c_int64()
+        _lib.check(lib.ifgfb_cones_finish(h, _lib.iptr(seg_off), None, ctypes.byref(total)),
+                   "ifgfb_cones_finish")
+        seg_ids = np.empty(total.value, dtype=np.int64)
+        _lib.check(lib.ifgfb_cones_ids(h, _lib.iptr(seg_off), _lib.iptr(seg_ids)),
+                   "ifgfb_cones_ids")
+    finally:
+        lib.ifgfb_cones_free(h)
+    return seg_ids, seg_off, n_edge
+
+
+def build_cone_hierarchy(tree: BoxTree, config: IfgfConfig = IfgfConfig(),
+                         device: bool = False) -> ConeHierarchy:
     """Relevant segments per box: those holding a cousin point or a node of a
-    relevant parent segment (sorted per box)."""
+    relevant parent segment (sorted per box).
+
+    device=True runs the relevance pass on the GPU (csrc/planbuild.cu,
+    ifgfb_cones_*): bit-identical result, the edge cases decided on the host
+    with the same numpy expressions (hier.edge_cases counts them)."""
     counts = cone_counts(tree, config)
     hier = ConeHierarchy(config, tree.kappa_max, {})
     nn = config.n_nodes
@@ -552,6 +630,12 @@ def build_cone_hierarchy(tree: BoxTree,
         stride = np.int64(id_stride(cl))
         cpts, cpt_off, cbox = _cousin_points(tree, d)
         cl.cpt_idx, cl.cpt_off = cpts, cpt_off
+        if device:
+            cl.seg_ids, cl.seg_off, n_edge = _device_relevant(
+                tree, d, cl, hier.cone_levels.get(d - 1), cpts, cbox)
+            hier.__dict__.setdefault("edge_cases", {})[d] = n_edge
+            hier.cone_levels[d] = cl
+            continue
         keys = []
         if cpts.size:
             s, th, ph, _ = cone_coords(tree.points[cpts], lvl.centers[cbox],
@@ -821,6 +905,26 @@ def _warp_set_tiles(gid, t, orow, w, per):
     return tid, tid[:, -1] + 1, gs, order, pos
 
 
+def row_order_cuts(ap: AccumulationPlan, cut_radius: int = 4, n_threads: int = 0):
+    """The first half of ``row_tiles``: per parent row the signature order
+    and the warp cuts, without tile records (tile-free device plans form
+    the tiles in the kernel from the nodes' sigma groups)."""
+    from . import _lib
+    lib = _lib.load()
+    nn = 75
+    gid = np.ascontiguousarray(_local_group_ids(ap, nn), dtype=np.uint8)
+    n_rows = ap.inst_off.size - 1
+    io = np.ascontiguousarray(ap.inst_off, dtype=np.int64)
+    it = np.ascontiguousarray(ap.inst_type, dtype=np.int64)
+    row_order = np.empty((n_rows, nn), dtype=np.uint8)
+    row_cuts = np.empty((n_rows, WARP_PARTS + 1), dtype=np.uint8)
+    _lib.check(lib.ifgfb_row_tiles_plan(
+        n_rows, _lib.iptr(io), _lib.iptr(it), ap.n_types, _lib.u8ptr(gid),
+        _lib.u8ptr(row_order), _lib.u8ptr(row_cuts), None, cut_radius, n_threads),
+        "ifgfb_row_tiles_plan")
+    return row_order, row_cuts
+
+
 def row_tiles(ap: AccumulationPlan, cut_radius: int = 4, n_threads: int = 0):
     """Per parent row partition of its 75 nodes into 5 contiguous warp-owned
     sets and the MMA row tiles of every (instance, warp); native builder
@@ -973,44 +1077,65 @@ def emission_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
     keeps it on the undisplaced point's branch; "reference" takes it mod
     2 pi exactly as reference ifgf.py:647-651 (parity runs at seam-crossing
     configurations).  Rows whose displacement does not cross phi = 0 are
-    bitwise identical under both."""
+    bitwise identical under both.
+
+    Pairs are processed in chunks of whole boxes on the plan thread pool
+    (every element by the same expressions: bit-identical to one pass); a
+    chunk's segment rows are looked up among its own boxes' keys only."""
     if seam not in SEAM_MODES:
         raise ValueError(f"seam must be one of {SEAM_MODES}")
     cl, lvl = hier.level(d), tree.level(d)
     tg = cl.cpt_idx
-    box = np.repeat(np.arange(lvl.n_boxes, dtype=np.int64),
-                    np.diff(cl.cpt_off))
-    ctr = lvl.centers[box]
-    if tg.size == 0:
+    n_pairs = tg.size
+    if n_pairs == 0:
         z = np.empty((0, 4))
         return EmissionPlan(d, np.empty(0, np.int64), tg, z,
                             None if disp_points_t is None else z)
-    s, th, ph, r = cone_coords(tree.points[tg] - ctr, np.zeros(3), lvl.side)
-    flat = seg_index(cl, s, th, ph)
-    want = box * np.int64(id_stride(cl)) + flat
     keys = box_keys(cl)
-    row = np.searchsorted(keys, want).astype(np.int64)
-    misses = int(np.count_nonzero(keys[np.minimum(row, keys.size - 1)]
-                                  != want))
-    geom = np.stack(local_coords(cl, flat, s, th, ph) + (r,), axis=1)
-    gd = None
-    if disp_points_t is not None:
-        sd, td, pd, rd = cone_coords(disp_points_t[tg] - ctr, np.zeros(3),
-                                     lvl.side)
-        # Deliberate deviation from the reference (ifgf.py:647-651): the
-        # displaced point is evaluated with the undisplaced point's segment
-        # polynomial, but its phi is taken mod 2 pi, so a displacement
-        # across the phi = 0 seam lands ~2 n_a intervals away and the
-        # angular polynomial is extrapolated there (D_far = (S(x+hn) -
-        # S(x))/h then blows up by ~1e5 at those rows; GMRES stagnates from
-        # sphere(12,10) on).  Keep the displaced phi on the undisplaced
-        # point's branch.  Bitwise unchanged wherever the seam is not
-        # crossed (every golden configuration).
-        if seam == "unwrap":
-            pd = np.where(pd - ph > np.pi, pd - 2.0 * np.pi,
-                          np.where(ph - pd > np.pi, pd + 2.0 * np.pi, pd))
-        gd = np.stack(local_coords(cl, flat, sd, td, pd) + (rd,), axis=1)
-    return EmissionPlan(d, row, tg, geom, gd, misses)
+    stride = np.int64(id_stride(cl))
+    row = np.empty(n_pairs, dtype=np.int64)
+    geom = np.empty((n_pairs, 4))
+    gd = None if disp_points_t is None else np.empty((n_pairs, 4))
+    miss = []
+
+    def chunk(rng):
+        b0, b1 = rng
+        p0, p1 = int(cl.cpt_off[b0]), int(cl.cpt_off[b1])
+        if p1 == p0:
+            return
+        box = np.repeat(np.arange(b0, b1, dtype=np.int64), np.diff(cl.cpt_off[b0:b1 + 1]))
+        ctr = lvl.centers[box]
+        t = tg[p0:p1]
+        s, th, ph, r = cone_coords(tree.points[t] - ctr, np.zeros(3), lvl.side)
+        flat = seg_index(cl, s, th, ph)
+        want = box * stride + flat
+        k0, k1 = int(cl.seg_off[b0]), int(cl.seg_off[b1])
+        kk = keys[k0:k1]
+        rr = np.searchsorted(kk, want).astype(np.int64)
+        if kk.size:
+            miss.append(int(np.count_nonzero(kk[np.minimum(rr, kk.size - 1)] != want)))
+        else:
+            miss.append(int(want.size))
+        row[p0:p1] = rr + k0
+        geom[p0:p1] = np.stack(local_coords(cl, flat, s, th, ph) + (r,), axis=1)
+        if gd is not None:
+            sd, td, pd, rd = cone_coords(disp_points_t[t] - ctr, np.zeros(3), lvl.side)
+            # Deliberate deviation from the reference (ifgf.py:647-651): the
+            # displaced point is evaluated with the undisplaced point's
+            # segment polynomial, but its phi is taken mod 2 pi, so a
+            # displacement across the phi = 0 seam lands ~2 n_a intervals
+            # away and the angular polynomial is extrapolated there (D_far =
+            # (S(x+hn) - S(x))/h then blows up by ~1e5 at those rows; GMRES
+            # stagnates from sphere(12,10) on).  Keep the displaced phi on
+            # the undisplaced point's branch.  Bitwise unchanged wherever
+            # the seam is not crossed (every golden configuration).
+            if seam == "unwrap":
+                pd = np.where(pd - ph > np.pi, pd - 2.0 * np.pi,
+                              np.where(ph - pd > np.pi, pd + 2.0 * np.pi, pd))
+            gd[p0:p1] = np.stack(local_coords(cl, flat, sd, td, pd) + (rd,), axis=1)
+
+    list(_pool().map(chunk, list(_chunks(cl.cpt_off, 1 << 18))))
+    return EmissionPlan(d, row, tg, geom, gd, sum(miss))
 
 
 def tree_stats(tree: BoxTree, hier: ConeHierarchy | None = None) -> str:

@@ -51,6 +51,8 @@ STRUCTS = {
     "ifgfb_level_part": _lib.LevelPart,
     "ifgfb_partition_desc": _lib.PartitionDesc,
     "ifgfb_rank_desc": _lib.RankDesc,
+    "ifgfb_cone_level_desc": _lib.ConeLevelDesc,
+    "ifgfb_cone_parent_desc": _lib.ConeParentDesc,
 }
 
 
