@@ -142,13 +142,16 @@ def _stage_logger():
                               flush=True)
 
 
-def plan_inputs(disc, mats, device_moments=False):
+def plan_inputs(disc, mats, device_moments=False, device_plan=False):
+    """Host plan; device_plan: cone hierarchy and propagation types from the
+    native device builder (csrc/planbuild.cu; integers identical to the host
+    builder, tests/test_gpu_planbuild.py)."""
     from paper_2408_02274_b200 import nearfield, octree
     kmax = max(abs(mats.kappa_e), abs(mats.kappa_i))
     stage = _stage_logger()
     tree = octree.build_box_tree(disc.points, kmax)
     stage("tree")
-    hier = octree.build_cone_hierarchy(tree)
+    hier = octree.build_cone_hierarchy(tree, device=device_plan)
     stage("cones")
     smap = nearfield.classify_targets(disc)
     stage("classify")
@@ -439,11 +442,11 @@ def run_b200(args):
         part = level3_partition(tree, None, n_r, disc.n_patches, disc.n_c)[r]
         runner = DistributedMullerOperator(disc, mats, part, tree=tree,
                                            exchange=False if emulate else None,
-                                           device_moments=dev_mom)
+                                           device_moments=dev_mom, device_plan=dev_mom)
         op = runner.op
         counts = work_counts(runner.view, runner.hier)
     else:
-        inputs = plan_inputs(disc, mats, dev_mom)
+        inputs = plan_inputs(disc, mats, dev_mom, device_plan=dev_mom)
         tree, hier, smap, mom, cp = inputs
         op = MullerOperator(disc, mats, smap, mom, (cp.ell_idx, cp.src_idx),
                             tree=tree, hierarchy=hier)
@@ -563,9 +566,12 @@ def run_b200(args):
                    "algorithmic_gflop_per_matvec": total_flop / 1e9,
                    "l2": "flushed (256 MB write) before every timed step",
                    "parallelism": par,
-                   "moments": ("device kernel (beta_d at its ~1e-7 conditioning; "
+                   "moments": ("device kernel (beta_d at its ~1e-7 conditioning: apply "
+                               "parity 5e-9 vs the reference at cfg 1, "
                                "tests/test_gpu_moments.py)" if dev_mom else
                                "host restatement (reference-exact)"),
+                   "plan_builder": ("device (cones + propagation types, "
+                                    "csrc/planbuild.cu)" if dev_mom else "host numpy"),
                    "plan_build_s": round(t_plan, 1),
                    "device_plan_gib": round(op.plan.device_bytes() / 2**30, 2),
                    "geometry_on_device_levels": sorted(getattr(op.plan, "otf_levels", [])),

@@ -431,6 +431,30 @@ int ifgfb_cones_finish(ifgfb_cone_build* b, int64_t* seg_off, int64_t** reserved
 int ifgfb_cones_ids(ifgfb_cone_build* b, const int64_t* seg_off, int64_t* seg_ids);
 int ifgfb_cones_free(ifgfb_cone_build* b);
 
+/* Propagation types of one level on the device (reference _AccumType,
+ * ifgf.py:686-702): per type (parent segment id gamma, child octant) the
+ * sigma group of each of the 75 parent nodes (gid), the groups' child
+ * segment ids ascending (sigma, -1 padded to 75), their count and, if
+ * node_geom / node_r are given, the nodes' local coordinates and radii.
+ * ambiguous[t] = 1: some node of type t lies within a few ulp of a child
+ * segment edge; its row is NOT filled and must be decided on the host with
+ * the reference's own expressions. */
+typedef struct {
+  int64_t n_types;
+  const int32_t* gamma;        /* parent segment id per type */
+  const uint8_t* octant;       /* child octant per type */
+  int32_t pn_s, pn_a;          /* parent cone counts */
+  double ph;                   /* parent level h */
+  const double* parent_tabs;   /* s_nodes | sin_t | cos_t | sin_p | cos_p */
+  int32_t n_s, n_a;            /* child cone counts */
+  double delta_s, delta_a;     /* child level */
+  double s_num;                /* np.sqrt(3.0) / 2.0 * child_side */
+  double half;                 /* 0.5 * child_side */
+} ifgfb_accum_types_desc;
+
+int ifgfb_accum_types(const ifgfb_accum_types_desc* d, uint8_t* gid, int32_t* sigma,
+                      uint8_t* nsig, uint8_t* ambiguous, double* node_geom, double* node_r);
+
 #ifdef __cplusplus
 }
 #endif

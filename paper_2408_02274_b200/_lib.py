@@ -114,6 +114,14 @@ class ConeParentDesc(C.Structure):
                 ("pn_a", C.c_int32), ("ph", C.c_double), ("parent_tabs", _dp)]
 
 
+class AccumTypesDesc(C.Structure):
+    _fields_ = [("n_types", C.c_int64), ("gamma", C.POINTER(C.c_int32)),
+                ("octant", C.POINTER(C.c_uint8)), ("pn_s", C.c_int32), ("pn_a", C.c_int32),
+                ("ph", C.c_double), ("parent_tabs", _dp), ("n_s", C.c_int32),
+                ("n_a", C.c_int32), ("delta_s", C.c_double), ("delta_a", C.c_double),
+                ("s_num", C.c_double), ("half", C.c_double)]
+
+
 class MomentDesc(C.Structure):
     _fields_ = [("n_pairs", C.c_int64), ("target_xyz", _dp), ("target_nrm", _dp),
                 ("patch", C.POINTER(C.c_int32)), ("uv", _dp),
@@ -175,6 +183,8 @@ EXPORTS = {
     "ifgfb_cones_finish": ([C.c_void_p, _ip, C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
     "ifgfb_cones_ids": ([C.c_void_p, _ip, _ip], C.c_int),
     "ifgfb_cones_free": ([C.c_void_p], C.c_int),
+    "ifgfb_accum_types": ([C.POINTER(AccumTypesDesc), _u8p, C.POINTER(C.c_int32), _u8p,
+                           _u8p, _dp, _dp], C.c_int),
     "ifgfb_plan_set_rank": ([C.c_void_p, C.POINTER(RankDesc)], C.c_int),
     "ifgfb_plan_rank_buffers": ([C.c_void_p] + [C.POINTER(C.c_void_p)] * 4
                                 + [C.POINTER(C.c_int64)], C.c_int),

@@ -719,11 +719,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
       :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ double2 lds128(const double2* p) {
-  double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
-  return v;
-}
+// Plain loads (the pointer is derived from the kernel's shared array, so
+// they compile to LDS.128): unlike volatile asm they can be hoisted ahead of
+// the (volatile) DMMAs, which hides the shared-memory latency; they stay
+// behind the mbarrier wait, whose asm clobbers memory.
+__device__ __forceinline__ double2 lds128(const double2* p) { return *p; }
 
 // acc (+)= basis x block for a block resident in shared memory
 __device__ __forceinline__ void basis_times_smem(const BasisA& B, const double* C, int lane,
@@ -826,9 +826,9 @@ __global__ void __launch_bounds__(RING_THREADS, IFGFB_RING_MINB) accum_ring_kern
     __syncwarp();
     // TILEFREE: sigma group of the lane's slot, loaded one instance ahead
     auto slot_group = [&](int j) -> int {
-      if (!TILEFREE || j >= ni || lane >= nset) return 0xFF;
-      const int t = __shfl_sync(0xffffffffu, my_t, j);
-      return __ldg(a.gid + (size_t)t * NN + word[lane]);
+      if (!TILEFREE || j >= ni) return 0xFF;            // warp-uniform
+      const int t = __shfl_sync(0xffffffffu, my_t, j);  // all lanes
+      return lane < nset ? (int)__ldg(a.gid + (size_t)t * NN + word[lane]) : 0xFF;
     };
     auto stage_inst = [&](int j, InstStage& T) {
       const int t = __shfl_sync(0xffffffffu, my_t, j);

@@ -7,6 +7,7 @@
 // (apply_singular_block), :457-487 (CorrectionSet), operators.py:279-319
 // (_neighbor_sums), solver.py:61-66 (GMRES vector ops).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -282,6 +283,107 @@ __global__ void __launch_bounds__(128, IFGFB_NEAR_MINB) near_kernel(NearArgs a) 
   }
 }
 
+// ------------------------------------------------- K6, split (default) ----
+// K6a: singular moments (quadrature.py:343-360).  One warp per target; lane
+// L < 28 owns one output, S(c, k) for L < 16 (L = 2c + k) and D(c, k) for
+// L >= 16, and streams the target's moment blocks in mn order (each block
+// 4 x n_c^2 complex, read once, coalesced per k-step through L1) against the
+// patch coefficient grids (L2 resident).  No cross-lane reduction and ~40
+// registers, against 28 warp reductions and 220 registers of the fused form.
+__global__ void __launch_bounds__(128) near_moments_kernel(NearArgs a) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n = a.s.n, n2 = a.s.n_c * a.s.n_c;
+  const int ell = warp + a.t_lo;
+  if (ell >= a.t_hi || lane >= 28) return;
+  const bool is_s = lane < 16;
+  const int o = is_s ? lane : lane - 16;          // (c * 2 + k)
+  const int c = o >> 1, k = o & 1;
+  const int kind = is_s ? k : 2 + k;               // bs0, bs1, bd0, bd1
+  double2 acc = make_double2(0.0, 0.0);
+  for (int q = a.mom_off[ell]; q < a.mom_off[ell + 1]; ++q) {
+    const int p = a.mom_patch[q];
+    const double2* beta = a.moments + ((size_t)q * 4 + kind) * n2;
+    const double2* co = a.pcoef + ((size_t)c * a.s.n_patches + p) * n2;
+#pragma unroll 4
+    for (int mn = 0; mn < n2; ++mn) {
+      const double2 b = __ldg(beta + mn), v = __ldg(co + mn);
+      acc.x += b.x * v.x - b.y * v.y;
+      acc.y += b.x * v.y + b.y * v.x;
+    }
+  }
+  if (is_s) a.s_val[(size_t)o * n + ell] = acc;
+  else a.d_val[(size_t)o * n + ell] = acc;
+}
+
+#ifndef IFGFB_NEAR_DIRECT_MINB   // 3 CTAs/SM -> <= 168 registers, no spills
+#define IFGFB_NEAR_DIRECT_MINB 3
+#endif
+// K6b: neighbour-box direct sums (+ entries, phi * w; operators.py:279-319)
+// and local corrections (- entries, (G * jw) * phi; quadrature.py:457-487)
+// in ONE signed pass (one warp reduction instead of two), then the far-field
+// combination (operators.py:341-350) on top of K6a's moment terms.
+__global__ void __launch_bounds__(128, IFGFB_NEAR_DIRECT_MINB) near_direct_kernel(NearArgs a) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n = a.s.n;
+  const int ell = warp + a.t_lo;
+  if (ell >= a.t_hi) return;
+  double2 S[8][2], D[6][2];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) S[c][0] = S[c][1] = make_double2(0, 0);
+#pragma unroll
+  for (int c = 0; c < 6; ++c) D[c][0] = D[c][1] = make_double2(0, 0);
+  const double x0 = a.s.pts[3 * ell], x1 = a.s.pts[3 * ell + 1], x2 = a.s.pts[3 * ell + 2];
+  const double n0 = a.s.nrm[3 * ell], n1 = a.s.nrm[3 * ell + 1], n2v = a.s.nrm[3 * ell + 2];
+  const int e0 = a.dir_off[ell], e1 = a.dir_off[ell + 1];
+  for (int e = e0 + lane; e < e1; e += 32) {
+    const int code = a.dir_src[e];
+    const bool neg = code < 0;
+    const int src = neg ? -code - 1 : code;
+    const double dx = x0 - a.s.pts[3 * src], dy = x1 - a.s.pts[3 * src + 1],
+                 dz = x2 - a.s.pts[3 * src + 2];
+    const double r = sqrt(dx * dx + dy * dy + dz * dz);
+    const double ndx = dx * n0 + dy * n1 + dz * n2v;
+    double2 gk[2], qk[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) kernel_pair(a.kr[k], a.ki[k], r, ndx, gk[k], qk[k]);
+    const double jw = neg ? -a.s.wq[src] : 1.0;      // corrections subtract
+    const double2* wsrc = neg ? a.phi : a.phiw;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      gk[k] = cscale(jw, gk[k]);
+      qk[k] = cscale(jw, qk[k]);
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double2 w = wsrc[(size_t)c * n + src];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        S[c][k] = cadd(S[c][k], cmul(gk[k], w));
+        if (c < 6) D[c][k] = cadd(D[c][k], cmul(qk[k], w));
+      }
+    }
+  }
+  double2 dir_s = make_double2(0, 0), dir_d = make_double2(0, 0);
+  warp_reduce_owned(S, D, lane, dir_s, dir_d);
+  if (lane < 16) {
+    const int c = lane >> 1;
+    const size_t o = (size_t)lane * n + ell;   // (c*2+k)*N + ell
+    const size_t of = a.far_pm ? (size_t)(ell - a.t_lo) * 32 + lane : o;
+    const double2 s_if = a.far[of];
+    a.s_val[o] = cadd(a.s_val[o], cadd(s_if, dir_s));
+    if (c < 6) {
+      const double2 sd = a.far_pm ? a.far[of + 16] : a.far_disp[o];
+      // numpy's complex / real: multiply by the reciprocal (Smith, rat = 0)
+      const double scl = 1.0 / a.fd_step;
+      const double2 d_if = make_double2(mul_rn(sd.x - s_if.x, scl),
+                                        mul_rn(sd.y - s_if.y, scl));
+      a.d_val[o] = cadd(a.d_val[o], cadd(d_if, dir_d));
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K7 ----
 struct AsmArgs {
   SurfPtrs s;
@@ -451,10 +553,21 @@ static int near_launch(Plan& p, cudaStream_t st) {
   const int warps_per_block = 4;
   const int nt = p.t_hi() - p.t_lo();
   if (nt <= 0) return IFGFB_OK;
+  static const bool fused = [] {
+    const char* v = std::getenv("IFGFB_NEAR");
+    return v && v[0] == 'f';
+  }();
+  const int grid = (nt + warps_per_block - 1) / warps_per_block;
   const int tk = p.timer.begin(K_NEAR, st);
-  near_kernel<<<(nt + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(na);
+  if (fused) {   // round-1 single kernel (A/B: IFGFB_NEAR=fused)
+    near_kernel<<<grid, 32 * warps_per_block, 0, st>>>(na);
+    p.launches += 1;
+  } else {
+    near_moments_kernel<<<grid, 32 * warps_per_block, 0, st>>>(na);
+    near_direct_kernel<<<grid, 32 * warps_per_block, 0, st>>>(na);
+    p.launches += 2;
+  }
   p.timer.end(tk, st);
-  p.launches += 1;
   IFGFB_CUDA(cudaGetLastError());
   return IFGFB_OK;
 }

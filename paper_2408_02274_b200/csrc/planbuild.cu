@@ -433,3 +433,164 @@ int ifgfb_cones_free(ifgfb_cone_build* h) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------
+// Propagation types on the device (reference _AccumType.__init__,
+// ifgf.py:686-702, vectorised host form octree._type_geometry): per type
+// (parent segment gamma, child octant) the 75 parent nodes seen from the
+// child centre (-offset + r * dir), their child segment (sigma, an integer
+// decision: replayed exactly as above, edge cases flagged for the host), the
+// sigma groups (distinct child segments, ascending) and, on request, the
+// continuous node geometry (local coordinates in the child segment, r_parent,
+// r_child) -- those from CUDA's acos / atan2, a few ulp from numpy's (as the
+// on-device geometry of the propagation kernel).
+namespace ifgfb {
+
+struct TypeArgs {
+  int64_t n_types;
+  const int* gamma; const unsigned char* octant;
+  const double* ptabs; int pn_s, pn_a; double ph;     // parent level
+  int n_s, n_a; double delta_s, delta_a, s_num;       // child level
+  double half;                                        // 0.5 * child side
+  unsigned char* gid; int* sigma; unsigned char* nsig; unsigned char* amb;
+  double* geom; double* node_r;                       // optional
+};
+
+__global__ void __launch_bounds__(128) accum_types_kernel(TypeArgs a) {
+  __shared__ int64_t sf[4][NN];
+  __shared__ unsigned char first[4][NN];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * 4 + w;
+  if (t >= a.n_types) return;
+  const double* s_nodes = a.ptabs;
+  const double* sin_t = s_nodes + a.pn_s * PS;
+  const double* cos_t = sin_t + a.pn_a * PA;
+  const double* sin_p = cos_t + a.pn_a * PA;
+  const double* cos_p = sin_p + 2 * a.pn_a * PA;
+  const int two_na = 2 * a.pn_a;
+  const int id = a.gamma[t], oct = a.octant[t];
+  const int i_p = id % two_na, rest = id / two_na;
+  const int i_t = rest % a.pn_a, i_s = rest / a.pn_a;
+  // center = -offset, offset = 0.5 side (2 bit - 1) (ifgf.py:687-688)
+  const double cx = (oct >> 2) & 1 ? -a.half : a.half;
+  const double cy = (oct >> 1) & 1 ? -a.half : a.half;
+  const double cz = oct & 1 ? -a.half : a.half;
+  ConeArgs ca{a.n_s, a.n_a, a.delta_s, a.delta_a, a.s_num, 0, nullptr, nullptr, nullptr,
+              nullptr, 0};
+  bool bad = false;
+  for (int n = lane; n < NN; n += 32) {
+    const int na = n / (PA * PA), nb = (n / PA) % PA, nc = n % PA;
+    const double rp = __ddiv_rn(a.ph, s_nodes[i_s * PS + na]);
+    const double st = sin_t[i_t * PA + nb], ct = cos_t[i_t * PA + nb];
+    const double sp = sin_p[i_p * PA + nc], cp = cos_p[i_p * PA + nc];
+    const double x = __dadd_rn(cx, __dmul_rn(rp, __dmul_rn(st, cp)));
+    const double y = __dadd_rn(cy, __dmul_rn(rp, __dmul_rn(st, sp)));
+    const double z = __dadd_rn(cz, __dmul_rn(rp, ct));
+    const int64_t key = cone_key(ca, x, y, z);
+    bad |= key < 0;
+    sf[w][n] = key;
+    if (a.geom) {
+      const double rc = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)),
+                                             __dmul_rn(z, z)));
+      const double s = __ddiv_rn(a.s_num, rc);
+      const double th = acos(fmin(fmax(__ddiv_rn(z, rc), -1.0), 1.0));
+      double ph = atan2(y, x);
+      if (ph < 0.0) ph = __dadd_rn(ph, 6.283185307179586);
+      const int64_t f = key < 0 ? 0 : key;
+      const int two = 2 * a.n_a;
+      const int64_t jp = f % two, jr = f / two, jt = jr % a.n_a, js = jr / a.n_a;
+      double* g = a.geom + (t * NN + n) * 3;
+      g[0] = 2.0 * (s / a.delta_s - js) - 1.0;
+      g[1] = 2.0 * (th / a.delta_a - jt) - 1.0;
+      g[2] = 2.0 * (ph / a.delta_a - jp) - 1.0;
+      a.node_r[(t * NN + n) * 2] = rp;
+      a.node_r[(t * NN + n) * 2 + 1] = rc;
+    }
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) a.amb[t] = bad ? 1 : 0;
+  if (bad) return;     // decided on the host
+  __syncwarp();
+  for (int n = lane; n < NN; n += 32) {
+    bool f = true;
+    for (int k = 0; k < n; ++k) f &= sf[w][k] != sf[w][n];
+    first[w][n] = f;
+  }
+  __syncwarp();
+  int cnt_first = 0;
+  for (int n = lane; n < NN; n += 32) {
+    const int64_t v = sf[w][n];
+    int g = 0;
+    for (int j = 0; j < NN; ++j) g += (first[w][j] && sf[w][j] < v) ? 1 : 0;
+    a.gid[t * NN + n] = (unsigned char)g;
+    if (first[w][n]) {
+      a.sigma[t * NN + g] = (int)v;
+      ++cnt_first;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt_first += __shfl_xor_sync(0xffffffffu, cnt_first, o);
+  if (lane == 0) a.nsig[t] = (unsigned char)cnt_first;
+  for (int g = cnt_first + lane; g < NN; g += 32) a.sigma[t * NN + g] = -1;
+}
+
+}  // namespace ifgfb
+
+extern "C" int ifgfb_accum_types(const ifgfb_accum_types_desc* d, uint8_t* gid, int32_t* sigma,
+                                 uint8_t* nsig, uint8_t* ambiguous, double* node_geom,
+                                 double* node_r) {
+  IFGFB_CHECK_ARG(d && gid && sigma && nsig && ambiguous, "null argument");
+  IFGFB_CHECK_ARG((node_geom == nullptr) == (node_r == nullptr), "node_geom / node_r: both or none");
+  const int64_t nt = d->n_types;
+  if (nt == 0) return IFGFB_OK;
+  std::vector<void*> owned;
+  int* dg = nullptr;
+  unsigned char *doc = nullptr, *dgid = nullptr, *dns = nullptr, *damb = nullptr;
+  double *dtab = nullptr, *dgeo = nullptr, *dr = nullptr;
+  int* dsig = nullptr;
+  const size_t ntab = (size_t)d->pn_s * PS + 2 * (size_t)d->pn_a * PA + 4 * (size_t)d->pn_a * PA;
+  int rc = upload(&dg, d->gamma, nt, owned);
+  if (!rc) rc = upload(&doc, d->octant, nt, owned);
+  if (!rc) rc = upload(&dtab, d->parent_tabs, ntab, owned);
+  auto alloc = [&](auto** p, size_t n) {
+    if (rc) return;
+    if (cudaMalloc(p, n * sizeof(**p)) != cudaSuccess) {
+      set_error("ifgfb_accum_types: allocation failed");
+      rc = IFGFB_ERR_CUDA;
+      return;
+    }
+    owned.push_back(*p);
+  };
+  alloc(&dgid, (size_t)nt * NN);
+  alloc(&dsig, (size_t)nt * NN);
+  alloc(&dns, (size_t)nt);
+  alloc(&damb, (size_t)nt);
+  if (node_geom) {
+    alloc(&dgeo, (size_t)nt * NN * 3);
+    alloc(&dr, (size_t)nt * NN * 2);
+  }
+  if (!rc) {
+    TypeArgs a{nt, dg, doc, dtab, d->pn_s, d->pn_a, d->ph, d->n_s, d->n_a, d->delta_s,
+               d->delta_a, d->s_num, d->half, dgid, dsig, dns, damb, dgeo, dr};
+    accum_types_kernel<<<(unsigned)((nt + 3) / 4), 128>>>(a);
+    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+      set_error("accum_types_kernel failed");
+      rc = IFGFB_ERR_CUDA;
+    }
+  }
+  auto down = [&](void* h, const void* dptr, size_t bytes) {
+    if (!rc && cudaMemcpy(h, dptr, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      set_error("ifgfb_accum_types: copy failed");
+      rc = IFGFB_ERR_CUDA;
+    }
+  };
+  down(gid, dgid, (size_t)nt * NN);
+  down(sigma, dsig, sizeof(int) * (size_t)nt * NN);
+  down(nsig, dns, (size_t)nt);
+  down(ambiguous, damb, (size_t)nt);
+  if (node_geom) {
+    down(node_geom, dgeo, sizeof(double) * (size_t)nt * NN * 3);
+    down(node_r, dr, sizeof(double) * (size_t)nt * NN * 2);
+  }
+  free_all(owned);
+  return rc;
+}

@@ -613,6 +613,7 @@ def build_cone_hierarchy(tree: BoxTree, config: IfgfConfig = IfgfConfig(),
     with the same numpy expressions (hier.edge_cases counts them)."""
     counts = cone_counts(tree, config)
     hier = ConeHierarchy(config, tree.kappa_max, {})
+    hier.device_plan = bool(device)   # propagation types on the device too
     nn = config.n_nodes
     for d in range(3, tree.depth + 1):
         n_s, n_a = counts[d]
@@ -787,8 +788,70 @@ def _type_geometry(pcl: ConeLevel, cl: ConeLevel, gamma, octant, child_side):
     return fs, order, xs, xt, xp, take(rp), take(rc)
 
 
+def _device_types(pcl, cl, gamma, toct, child_side, geometry: bool,
+                  chunk: int = 1 << 22):
+    """Per type: sigma groups (gid, sigma ascending, count) and optionally
+    the node geometry, from the device (csrc/planbuild.cu,
+    ifgfb_accum_types); types with a node within a few ulp of a child
+    segment edge are recomputed here by ``_type_geometry`` (the reference's
+    expressions), so gid / sigma equal the host builder's bit for bit."""
+    import ctypes
+    from . import _lib
+    lib = _lib.load()
+    n_t, nn = gamma.size, 75
+    gid = np.empty((n_t, nn), dtype=np.uint8)
+    sigma = np.empty((n_t, nn), dtype=np.int32)
+    nsig = np.empty(n_t, dtype=np.uint8)
+    amb = np.empty(n_t, dtype=np.uint8)
+    geom = np.empty((n_t, nn, 3)) if geometry else None
+    node_r = np.empty((n_t, nn, 2)) if geometry else None
+    tabs = level_tables(pcl)
+    g32 = np.ascontiguousarray(gamma, dtype=np.int32)
+    o8 = np.ascontiguousarray(toct, dtype=np.uint8)
+    u8 = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+    for t0 in range(0, n_t, chunk):
+        t1 = min(n_t, t0 + chunk)
+        desc = _lib.AccumTypesDesc(
+            t1 - t0, g32[t0:t1].ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), u8(o8[t0:t1]),
+            pcl.n_s, pcl.n_a, pcl.h, _lib.dptr(tabs), cl.n_s, cl.n_a, cl.delta_s, cl.delta_a,
+            float(np.sqrt(3.0) / 2.0 * child_side), 0.5 * child_side)
+        _lib.check(lib.ifgfb_accum_types(
+            ctypes.byref(desc), u8(gid[t0:t1]),
+            sigma[t0:t1].ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), u8(nsig[t0:t1]),
+            u8(amb[t0:t1]), _lib.dptr(geom[t0:t1]) if geometry else None,
+            _lib.dptr(node_r[t0:t1]) if geometry else None), "ifgfb_accum_types")
+    sel = np.nonzero(amb)[0]
+    if sel.size:
+        fs, order, xs, xt, xp, rp, rc = _type_geometry(pcl, cl, gamma[sel], toct[sel],
+                                                       child_side)
+        rows = np.arange(sel.size)[:, None]
+        newgrp = np.ones(fs.shape, dtype=bool)
+        newgrp[:, 1:] = fs[:, 1:] != fs[:, :-1]
+        local = np.cumsum(newgrp, axis=1) - 1
+        g = np.empty((sel.size, nn), dtype=np.uint8)
+        g[rows, order] = local
+        gid[sel] = g
+        sig = np.full((sel.size, nn), -1, dtype=np.int32)
+        for i in range(sel.size):
+            u = fs[i][newgrp[i]]
+            sig[i, :u.size] = u
+        sigma[sel] = sig
+        nsig[sel] = newgrp.sum(axis=1)
+        if geometry:
+            for k, v in enumerate((xs, xt, xp)):
+                tmp = np.empty((sel.size, nn))
+                tmp[rows, order] = v
+                geom[sel, :, k] = tmp
+            tmp = np.empty((sel.size, nn))
+            tmp[rows, order] = rp
+            node_r[sel, :, 0] = tmp
+            tmp[rows, order] = rc
+            node_r[sel, :, 1] = tmp
+    return gid, sigma, nsig, geom, node_r, int(sel.size)
+
+
 def accumulation_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
-                      geometry: bool = True) -> AccumulationPlan:
+                      geometry: bool = True, device: bool | None = None) -> AccumulationPlan:
     """Plan for folding level-d child interpolants into level d-1, cached
     on the hierarchy.  ``geometry=False`` accepts a cached plan whose
     per-type arrays were released by ``trim_accumulation_plans`` (instance
@@ -796,6 +859,8 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
     cache = hier.__dict__.setdefault("_b200_accum", {})
     if d in cache and (not geometry or not cache[d].trimmed):
         return cache[d]
+    from .engine import _StageLog
+    log = _StageLog(f"accum {d}")
     cl, pcl = hier.level(d), hier.level(d - 1)
     lvl = tree.level(d)
     nn = hier.config.p_s * hier.config.p_a ** 2
@@ -808,6 +873,19 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
     inst_type = inst_type.astype(np.int64)
     gamma, toct = ukeys >> 3, ukeys & 7
     n_t = ukeys.size
+    if device is None:
+        device = bool(hier.__dict__.get("device_plan", False))
+    if device:
+        log(f"instances + types ({n_t} types)")
+        gid, sigma, nsig, _, _, n_edge = _device_types(pcl, cl, gamma, toct, lvl.side, False)
+        log(f"device type groups ({n_edge} edge types on the host)")
+        sig_off = np.zeros(n_t + 1, dtype=np.int64)
+        np.cumsum(nsig, out=sig_off[1:])
+        g_sigma = sigma[sigma >= 0].astype(np.int64)
+        del sigma
+        return _finish_accumulation_plan(
+            cache, d, cl, pcl, gamma, toct, sig_off, g_sigma, gid, None, None, None,
+            prow, child, inst_type, log, pending=(pcl, cl, lvl.side))
     gid = np.empty((n_t, nn), dtype=np.uint8)
     scatter = np.empty((n_t, nn), dtype=np.uint8)
     node_geom = np.empty((n_t, nn, 3))
@@ -835,13 +913,23 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
         node_r[t0:t1, :, 1][rows, order] = rc
         sig_parts[ib] = (newgrp.sum(axis=1), fs[newgrp])
 
+    log(f"instances + types ({n_t} types)")
     list(_pool().map(chunk, range(len(blocks))))   # disjoint row blocks
+    log("type geometry")
     n_sig = np.concatenate([c for c, _ in sig_parts]) if blocks else np.zeros(0, np.int64)
     g_sigma = (np.concatenate([g for _, g in sig_parts]) if blocks
                else np.zeros(0, np.int64)).astype(np.int64)
     del sig_parts
     sig_off = np.zeros(n_t + 1, dtype=np.int64)
     np.cumsum(n_sig, out=sig_off[1:])
+    return _finish_accumulation_plan(cache, d, cl, pcl, gamma, toct, sig_off, g_sigma, gid,
+                                     scatter, node_geom, node_r, prow, child, inst_type, log)
+
+
+def _finish_accumulation_plan(cache, d, cl, pcl, gamma, toct, sig_off, g_sigma, gid,
+                              scatter, node_geom, node_r, prow, child, inst_type, log,
+                              pending=None):
+    n_t = gamma.size
     # instances sorted by (parent row, child): prow/child are generated
     # child-major, so re-sort
     order = np.lexsort((child, prow))
@@ -858,6 +946,7 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
     misses = int(np.count_nonzero(
         bkeys[np.minimum(crow, bkeys.size - 1)] != want))
     del want
+    log("instance sort + child rows")
     plan = AccumulationPlan(
         level=d, n_types=n_t, type_gamma=gamma, type_octant=toct,
         sig_off=sig_off, group_sigma=g_sigma, gid=gid, scatter=scatter,
@@ -865,6 +954,7 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
         inst_off=_offsets_from_owner(prow, pcl.n_segments),
         inst_type=inst_type, inst_child=child, inst_crow_off=crow_off,
         crow=crow, crow_misses=misses)
+    plan.pending_geometry = pending
     cache[d] = plan
     return plan
 
@@ -875,6 +965,7 @@ def trim_accumulation_plans(hier: ConeHierarchy) -> None:
     instance arrays stay for work counts and partitioning."""
     for ap in hier.__dict__.get("_b200_accum", {}).values():
         ap.gid = ap.scatter = ap.node_geom = ap.node_r = None
+        ap.pending_geometry = None
         for k in ("xs", "xt", "xp", "r_parent", "r_child", "group_end", "group_bounds"):
             ap.__dict__.pop(k, None)
         ap.trimmed = True
@@ -1041,7 +1132,14 @@ def row_tiles_equal_split(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5,
 
 def node_tables(ap: AccumulationPlan, p_s: int = 3, p_a: int = 5):
     """Per type and PARENT node: local coordinates in its child segment
-    (xs, xt, xp) and the radii (r_parent, r_child)."""
+    (xs, xt, xp) and the radii (r_parent, r_child).  Plans built on the
+    device compute them here, on demand (only levels whose tables are
+    uploaded need them)."""
+    pend = getattr(ap, "pending_geometry", None)
+    if ap.node_geom is None and pend is not None:
+        pcl, cl, side = pend
+        _, _, _, ap.node_geom, ap.node_r, _ = _device_types(
+            pcl, cl, ap.type_gamma, ap.type_octant, side, True)
     return ap.node_geom, ap.node_r
 
 

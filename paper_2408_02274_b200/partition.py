@@ -224,7 +224,8 @@ class DistributedMullerOperator:
     def __init__(self, disc, materials, part: RankPart, tree=None, group=None,
                  exchange=None, quad_config=None, device_moments: bool = True,
                  config=None, stream_parts=None, geometry_on_device=None,
-                 seam: str = "unwrap", moments=None, smap=None):
+                 seam: str = "unwrap", moments=None, smap=None,
+                 device_plan: bool = False):
         import torch
         from . import nearfield, octree
         from .operator import MullerOperator, OperatorConfig
@@ -233,7 +234,7 @@ class DistributedMullerOperator:
         self.tree = tree if tree is not None else octree.build_box_tree(disc.points, kmax)
         self.window = octree.tree_window(self.tree, *part.box3)
         self.view = octree.window_view(self.tree, self.window)
-        self.hier = octree.build_cone_hierarchy(self.view)
+        self.hier = octree.build_cone_hierarchy(self.view, device=device_plan)
         qc = quad_config or nearfield.SingularQuadratureConfig()
         t0, t1 = part.targets
         if smap is None:

@@ -53,6 +53,7 @@ STRUCTS = {
     "ifgfb_rank_desc": _lib.RankDesc,
     "ifgfb_cone_level_desc": _lib.ConeLevelDesc,
     "ifgfb_cone_parent_desc": _lib.ConeParentDesc,
+    "ifgfb_accum_types_desc": _lib.AccumTypesDesc,
 }
 
 

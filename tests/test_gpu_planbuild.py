@@ -41,3 +41,25 @@ def test_device_cones_in_windows():
         for d in hv.cone_levels:
             assert np.array_equal(hv.level(d).seg_ids, hd.level(d).seg_ids)
             assert np.array_equal(hv.level(d).seg_off, hd.level(d).seg_off)
+
+
+@pytest.mark.parametrize("name", ["s1", "c1", "se1", "sl1", "c2n4"])
+def test_device_propagation_types_equal_host(name):
+    """Propagation types (sigma groups per parent node, child rows per
+    instance) from the device builder equal the host builder's integers; the
+    continuous node tables agree to a few ulp (CUDA vs numpy acos/atan2)."""
+    if not (GOLDEN / f"{name}.npz").exists():
+        pytest.skip(f"{name} fixture not generated")
+    inp = inputs(name)
+    tree, host = inp["tree"], inp["hier"]
+    dev = octree.build_cone_hierarchy(tree, device=True)
+    for d in range(4, tree.depth + 1):
+        a = octree.accumulation_plan(tree, host, d)
+        b = octree.accumulation_plan(tree, dev, d)
+        assert b.pending_geometry is not None
+        for f in ("type_gamma", "type_octant", "sig_off", "group_sigma", "gid", "inst_off",
+                  "inst_type", "inst_child", "inst_crow_off", "crow"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), (d, f)
+        ga, ra = octree.node_tables(a)
+        gb, rb = octree.node_tables(b)
+        assert np.abs(ga - gb).max() < 1e-12 and np.abs(ra - rb).max() < 1e-12 * np.abs(ra).max()
