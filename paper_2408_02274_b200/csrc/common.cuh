@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 #include <string>
 #include <vector>
 
@@ -84,6 +85,23 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
 }
+
+// Device-side bounds checks of the hand-written staging and index
+// arithmetic (build with -DIFGFB_DEVICE_CHECKS: tools/device_checks.sh).
+// compute-sanitizer is not available on the GPU pool, so these asserts are
+// the memory-safety net: a violated check prints and traps.
+#ifdef IFGFB_DEVICE_CHECKS
+#define IFGFB_DCHECK(cond)                                                     \
+  do {                                                                         \
+    if (!(cond)) {                                                             \
+      printf("IFGFB_DEVICE_CHECKS: %s failed at %s:%d (block %d thread %d)\n", \
+             #cond, __FILE__, __LINE__, (int)blockIdx.x, (int)threadIdx.x);    \
+      __trap();                                                                \
+    }                                                                          \
+  } while (0)
+#else
+#define IFGFB_DCHECK(cond) do { } while (0)
+#endif
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

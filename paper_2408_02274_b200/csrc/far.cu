@@ -463,6 +463,7 @@ struct AccArgs {
   int rows_per_cta;      // consecutive parent rows per CTA
   OtfGeom o;             // OTF instantiation only
   const unsigned char* gid;   // tile-free ring kernel: sigma group per (type, node)
+  int child_lo, child_hi;     // child rows present in coef_child (checks)
 };
 
 // cp.async (LDGSTS) helpers: global -> shared without a register round trip
@@ -525,7 +526,12 @@ __device__ __forceinline__ int tile_slot(const uint4& tl, int grp, bool& valid) 
 // WIDE: some instance of the level has more than MAX_GROUPS child segments
 // (coarse levels of large configurations); the extra rows are read from
 // global memory.  Kept out of the common instantiation (costs ~2%).
-template <int NK, bool WIDE, bool OTF>
+// TILEFREE: no tile records in the plan; each warp forms its row tiles per
+// sigma group from its slots' group ids (gid per type and node): distinct
+// groups ascending (__reduce_min_sync), slots of a group in slot order
+// (ballot), runs of <= 8 -- exactly the records ifgfb_row_tiles_fill writes,
+// so the result is bitwise the tile-record kernel's.
+template <int NK, bool WIDE, bool OTF, bool TILEFREE = false>
 __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
   __shared__ double2 acc[NN * NCOL];                        // 19.2 KB
   __shared__ RowStage stage[2];                             // 11.8 KB
@@ -547,11 +553,20 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
   int my_t = 0, my_ks = 0, my_ke = 0, my_co = 0;
   if (lane < ni) {
     my_t = a.inst_type[i0 + lane];
-    my_ks = a.tile_off[(i0 + lane) * WARP_PARTS + warp];
-    my_ke = a.tile_off[(i0 + lane) * WARP_PARTS + warp + 1];
+    if (!TILEFREE) {
+      my_ks = a.tile_off[(i0 + lane) * WARP_PARTS + warp];
+      my_ke = a.tile_off[(i0 + lane) * WARP_PARTS + warp + 1];
+    }
   }
   if (lane <= ni) my_co = a.inst_crow_off[i0 + lane];
   __syncwarp();
+  // TILEFREE: sigma group of the lane's slot (0xFFFFFFFF: no slot), one
+  // instance ahead
+  auto slot_group = [&](int j) -> unsigned {
+    if (!TILEFREE || j >= ni) return 0xFFFFFFFFu;       // warp-uniform
+    const int t = __shfl_sync(0xffffffffu, my_t, j);    // all lanes
+    return lane < nset ? (unsigned)__ldg(a.gid + (size_t)t * NN + word[lane]) : 0xFFFFFFFFu;
+  };
   auto stage_inst = [&](int j, RowStage& S) {
     const int t = __shfl_sync(0xffffffffu, my_t, j);
     const int ks = __shfl_sync(0xffffffffu, my_ks, j);
@@ -565,7 +580,7 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
       for (int e = lane; e < nset * NK; e += 32)
         cp_async16(&S.ratio[NK * pos0 + e], a.ratio + (tb + word[e / NK]) * NK + e % NK);
     }
-    if (lane < ke - ks) cp_async16(&S.tiles[pos0 + lane], a.tiles + ks + lane);
+    if (!TILEFREE && lane < ke - ks) cp_async16(&S.tiles[pos0 + lane], a.tiles + ks + lane);
     if (lane < min(ce - cs, MAX_GROUPS)) cp_async4(&S.crow[warp][lane], a.crow + cs + lane);
     cp_async_commit();
     if (IFGFB_ACC_L2PF) {   // warp w warms L2 with groups w, w + 5, ...
@@ -575,11 +590,14 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
       }
     }
   };
+  unsigned g_next = slot_group(0);
   if (ni > 0) stage_inst(0, stage[0]);
   for (int j = 0; j < ni; ++j) {
     RowStage& S = stage[j & 1];
+    const unsigned g_cur = g_next;
     if (j + 1 < ni) {
       stage_inst(j + 1, stage[(j + 1) & 1]);
+      g_next = slot_group(j + 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -587,7 +605,17 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
     __syncwarp();
     const int ntile = __shfl_sync(0xffffffffu, my_ke - my_ks, j);
     const int* crow_g = a.crow + __shfl_sync(0xffffffffu, my_co, j);
-    if (OTF) {   // slot -> sigma group from the tile records, then geometry
+    if (OTF && TILEFREE) {   // each lane: geometry of its own slot
+      const int pseg = a.o.parent_seg_id[p];
+      const int oct = a.o.type_octant[__shfl_sync(0xffffffffu, my_t, j)];
+      if (lane < nset) {
+        const int g = (int)g_cur;
+        const int cr = (!WIDE || g < MAX_GROUPS) ? S.crow[warp][g] : crow_g[g];
+        otf_node<NK>(a.o, pseg, oct, word[lane], a.o.child_seg_id[cr],
+                     &S.geom[(pos0 + lane) * 3], &S.ratio[(pos0 + lane) * NK]);
+      }
+      __syncwarp();
+    } else if (OTF) {   // slot -> sigma group from the tile records, then geometry
       for (int e = lane; e < ntile * 8; e += 32) {
         const uint4 tl = S.tiles[pos0 + (e >> 3)];
         const int r = e & 7;
@@ -608,18 +636,38 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
       }
       __syncwarp();
     }
-    for (int k = 0; k < ntile; ++k) {
-      const uint4 tl = S.tiles[pos0 + k];
+    unsigned g_at = TILEFREE ? __reduce_min_sync(0xffffffffu, g_cur) : 0u;
+    unsigned mask = TILEFREE && g_at != 0xFFFFFFFFu
+                        ? __ballot_sync(0xffffffffu, g_cur == g_at) : 0u;
+    for (int k = 0; TILEFREE ? (mask != 0u) : (k < ntile); ++k) {
       bool valid;
-      const int slot = tile_slot(tl, grp, valid);
+      int slot, g;
+      if (TILEFREE) {
+        // row grp of this tile = the grp-th slot of group g_at (slot order)
+        unsigned m = mask;
+        for (int i = 0; i < grp; ++i) m &= m - 1;
+        valid = m != 0u;
+        slot = valid ? __ffs(m) - 1 : __ffs(mask) - 1;
+        g = (int)g_at;
+        if (__popc(mask) > 8) {
+          for (int i = 0; i < 8; ++i) mask &= mask - 1;
+        } else {   // next distinct group of the warp's slots
+          g_at = __reduce_min_sync(0xffffffffu, g_cur > g_at ? g_cur : 0xFFFFFFFFu);
+          mask = g_at != 0xFFFFFFFFu ? __ballot_sync(0xffffffffu, g_cur == g_at) : 0u;
+        }
+      } else {
+        const uint4 tl = S.tiles[pos0 + k];
+        slot = tile_slot(tl, grp, valid);
+        g = tl.x & 0xff;
+      }
 #ifdef IFGFB_ACC_FAKEB   // diagnostic only: every tile reads the first owned child row
       const int crow_used = S.crow[warp][0] & 0;
 #else
-      const int g = tl.x & 0xff;
       const int crow_used = (!WIDE || g < MAX_GROUPS) ? S.crow[warp][g] : crow_g[g];
+      IFGFB_DCHECK(crow_used >= a.child_lo && crow_used < a.child_hi && slot < nset);
 #endif
 #if IFGFB_ACC_PF > 0 && defined(IFGFB_ACC_PFNEXT)
-      if (k + 1 < ntile) {   // warm L1 with the next tile's first k-steps
+      if (!TILEFREE && k + 1 < ntile) {   // warm L1 with the next tile's first k-steps
         const int gn = S.tiles[pos0 + k + 1].x & 0xff;
         const int crn = (!WIDE || gn < MAX_GROUPS) ? S.crow[warp][gn] : crow_g[gn];
         const double2* Fn = reinterpret_cast<const double2*>(
@@ -791,6 +839,7 @@ __global__ void __launch_bounds__(RING_THREADS, IFGFB_RING_MINB) accum_ring_kern
         for (int i = i0; i < i1; ++i) {
           const int c0 = a.inst_crow_off[i], c1 = a.inst_crow_off[i + 1];
           for (int c = c0; c < c1; ++c, ++seq) {
+            IFGFB_DCHECK(a.crow[c] >= a.child_lo && a.crow[c] < a.child_hi);
             const int slot = seq % NSLOT;
             const uint32_t use = seq / NSLOT;
             if (use > 0) mbar_wait(&S.empty[slot], (use - 1) & 1);
@@ -861,6 +910,8 @@ __global__ void __launch_bounds__(RING_THREADS, IFGFB_RING_MINB) accum_ring_kern
       const int ntile = __shfl_sync(0xffffffffu, my_ke - my_ks, j);
       const int cs = __shfl_sync(0xffffffffu, my_co, j);
       const int ng = __shfl_sync(0xffffffffu, my_co, j + 1) - cs;
+      IFGFB_DCHECK(ng >= 0 && ng <= NN && nset >= 1 && nset <= MAX_SET && pos0 + nset <= NN);
+      IFGFB_DCHECK(!TILEFREE || lane >= nset || g_cur < ng);
       if (OTF && TILEFREE) {
         const int pseg = a.o.parent_seg_id[p];
         const int oct = a.o.type_octant[__shfl_sync(0xffffffffu, my_t, j)];
@@ -918,6 +969,7 @@ __global__ void __launch_bounds__(RING_THREADS, IFGFB_RING_MINB) accum_ring_kern
             slot_n = tile_slot(tl, grp, valid);
             ++k;
           }
+          IFGFB_DCHECK(slot_n >= 0 && slot_n < nset);
           const double* ng3 = T.geom + (pos0 + slot_n) * 3;
           const BasisA B = make_basis<false>(ng3[0], ng3[1], ng3[2], tig);
           double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
@@ -1123,12 +1175,14 @@ struct EmitSync {
   cudaStream_t emit_stream() const { return on ? p.aux : st; }
 };
 
-// K4 implementation: the ring-staged kernel (default) or the round-1
-// L1-streaming kernel (IFGFB_K4=l1), for A/B measurements
+// K4 implementation (env IFGFB_K4, see engine.k4_mode): the L1-streaming
+// kernel (default "l1free" / "l1") or the ring-staged kernel ("ringfree" /
+// "ring": measured 45% slower, DESIGN 4); "...free" plans hold no tile
+// records (the host side decides, plan time)
 static bool use_ring() {
   static const bool ring = [] {
     const char* v = std::getenv("IFGFB_K4");
-    return !(v && v[0] == 'l');
+    return v && v[0] == 'r';
   }();
   return ring;
 }
@@ -1239,6 +1293,8 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
                        p.coef[cur ^ 1] - (size_t)U.seg_lo() * SEG_DOUBLES, U.seg_lo()};
             aa.row_end = U.seg_hi();
             aa.rows_per_cta = IFGFB_ACC_ROWS;
+            aa.child_lo = L.seg_lo();
+            aa.child_hi = L.seg_hi();
             const int nrows = U.seg_hi() - U.seg_lo();
             const int tk = p.timer.begin(K_ACCUM, st);
             const int grid = (nrows + IFGFB_ACC_ROWS - 1) / IFGFB_ACC_ROWS;
@@ -1247,18 +1303,27 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
               aa.o = OtfGeom{L.type_octant, U.seg_id, U.tabs, U.n_s, U.n_a, U.h, L.seg_id,
                              L.n_a, L.delta_s, L.delta_a, L.side, {kr[0], kr[1]}, {ki[0], ki[1]}};
             aa.gid = L.gid;
-            if (!L.tiles) {   // tile-free plan: the ring kernel forms the tiles
-              if (L.otf) IFGFB_RC((launch_ring<NK, true, true>(aa, nrows, st)));
-              else IFGFB_RC((launch_ring<NK, false, true>(aa, nrows, st)));
-            } else if (use_ring()) {
-              if (L.otf) IFGFB_RC((launch_ring<NK, true, false>(aa, nrows, st)));
-              else IFGFB_RC((launch_ring<NK, false, false>(aa, nrows, st)));
+            const bool tf = L.tiles == nullptr;   // tile-free plan
+            const dim3 blk(32 * WARP_PARTS);
+            if (use_ring()) {
+              if (L.otf) IFGFB_RC(tf ? (launch_ring<NK, true, true>(aa, nrows, st))
+                                     : (launch_ring<NK, true, false>(aa, nrows, st)));
+              else IFGFB_RC(tf ? (launch_ring<NK, false, true>(aa, nrows, st))
+                               : (launch_ring<NK, false, false>(aa, nrows, st)));
+            } else if (tf) {
+              if (L.otf) {
+                if (wide) accum_kernel<NK, true, true, true><<<grid, blk, 0, st>>>(aa);
+                else accum_kernel<NK, false, true, true><<<grid, blk, 0, st>>>(aa);
+              } else {
+                if (wide) accum_kernel<NK, true, false, true><<<grid, blk, 0, st>>>(aa);
+                else accum_kernel<NK, false, false, true><<<grid, blk, 0, st>>>(aa);
+              }
             } else if (L.otf) {
-              if (wide) accum_kernel<NK, true, true><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
-              else accum_kernel<NK, false, true><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
+              if (wide) accum_kernel<NK, true, true><<<grid, blk, 0, st>>>(aa);
+              else accum_kernel<NK, false, true><<<grid, blk, 0, st>>>(aa);
             } else {
-              if (wide) accum_kernel<NK, true, false><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
-              else accum_kernel<NK, false, false><<<grid, 32 * WARP_PARTS, 0, st>>>(aa);
+              if (wide) accum_kernel<NK, true, false><<<grid, blk, 0, st>>>(aa);
+              else accum_kernel<NK, false, false><<<grid, blk, 0, st>>>(aa);
             }
             p.timer.end(tk, st);
             ++launches;

@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(128) near_moments_kernel(NearArgs a) {
   double2 acc = make_double2(0.0, 0.0);
   for (int q = a.mom_off[ell]; q < a.mom_off[ell + 1]; ++q) {
     const int p = a.mom_patch[q];
+    IFGFB_DCHECK(p >= 0 && p < a.s.n_patches);
     const double2* beta = a.moments + ((size_t)q * 4 + kind) * n2;
     const double2* co = a.pcoef + ((size_t)c * a.s.n_patches + p) * n2;
 #pragma unroll 4
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(128, IFGFB_NEAR_DIRECT_MINB) near_direct_kerne
     const int code = a.dir_src[e];
     const bool neg = code < 0;
     const int src = neg ? -code - 1 : code;
+    IFGFB_DCHECK(src >= 0 && src < n && src != ell);
     const double dx = x0 - a.s.pts[3 * src], dy = x1 - a.s.pts[3 * src + 1],
                  dz = x2 - a.s.pts[3 * src + 2];
     const double r = sqrt(dx * dx + dy * dy + dz * dz);
@@ -553,13 +555,16 @@ static int near_launch(Plan& p, cudaStream_t st) {
   const int warps_per_block = 4;
   const int nt = p.t_hi() - p.t_lo();
   if (nt <= 0) return IFGFB_OK;
+  // fused single kernel (default); IFGFB_NEAR=split: moments kernel + direct
+  // kernel (measured slower: 1.26 vs 1.12 ms at sphere(8,10), 5.63 vs 4.12 ms
+  // on the r=2 slab; DESIGN 4)
   static const bool fused = [] {
     const char* v = std::getenv("IFGFB_NEAR");
-    return v && v[0] == 'f';
+    return !(v && v[0] == 's');
   }();
   const int grid = (nt + warps_per_block - 1) / warps_per_block;
   const int tk = p.timer.begin(K_NEAR, st);
-  if (fused) {   // round-1 single kernel (A/B: IFGFB_NEAR=fused)
+  if (fused) {
     near_kernel<<<grid, 32 * warps_per_block, 0, st>>>(na);
     p.launches += 1;
   } else {

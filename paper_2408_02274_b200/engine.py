@@ -24,14 +24,18 @@ def device_stream():
     return torch.cuda.current_stream().cuda_stream
 
 
+K4_MODES = ("l1free", "l1", "ringfree", "ring")
+
+
 def k4_mode() -> str:
-    """Propagation kernel (env IFGFB_K4): "free" (default: ring-staged
-    kernel, tiles formed on the device, no tile records in the plan),
-    "ring" (ring-staged kernel reading host-built tile records) or "l1"
-    (the round-1 kernel streaming child blocks through L1)."""
+    """Propagation kernel (env IFGFB_K4): "l1free" (default; child blocks
+    streamed through L1, MMA row tiles formed on the device from the nodes'
+    sigma groups: no tile records in the plan), "l1" (same kernel reading
+    host-built tile records), "ringfree" / "ring" (child blocks staged in a
+    shared-memory ring by TMA bulk copies; measured slower, DESIGN 4)."""
     import os
-    m = os.environ.get("IFGFB_K4", "free")
-    if m not in ("free", "ring", "l1"):
+    m = os.environ.get("IFGFB_K4", "l1free")
+    if m not in K4_MODES:
         raise ValueError(f"IFGFB_K4: unknown propagation kernel {m!r}")
     return m
 
@@ -181,7 +185,7 @@ class FarFieldPlan:
         for d in levels:
             ap = accumulation_plan(self.tree, self.hier, d)
             info[d] = (ap.n_types * self.TYPE_TABLE_BYTES, ap.n_types / max(1, ap.n_instances))
-            tile_bytes = 0 if k4_mode() == "free" else 12 * 16 + 20   # records + tile_off
+            tile_bytes = 0 if k4_mode().endswith("free") else 12 * 16 + 20   # records + tile_off
             fixed += (ap.n_instances * (tile_bytes + 8) + int(ap.inst_crow_off[-1]) * 4
                       + ap.n_types * 75)                                  # group ids
         pairs = [self.hier.level(d).cpt_idx.size for d in range(3, self.depth + 1)]
@@ -211,7 +215,7 @@ class FarFieldPlan:
         self._log(f"accum plan {d}")
         # crow rows are reproduced exactly as the reference's searchsorted
         # picks them (ifgf.py:743-746), including any inexact hit.
-        tile_free = k4_mode() == "free"
+        tile_free = k4_mode().endswith("free")
         if tile_free:
             row_order, row_cuts = row_order_cuts(ap)
             tile_off = tiles = None

@@ -238,3 +238,26 @@ def test_displaced_point_across_phi_seam():
         for k, kp in enumerate(kap):
             ref[:, k, j] = (np.exp(1j * kp * r) / (4 * np.pi * r) * wt[:, far]).sum(1)
     assert rel(od[:, :, idx], ref) < 1e-3
+
+
+@pytest.mark.parametrize("geometry_on_device", ["none", "all"])
+def test_tile_free_propagation_is_bitwise_tile_records(monkeypatch, geometry_on_device):
+    """Plans without MMA tile records (tiles formed in the propagation
+    kernel from the nodes' sigma groups, the default) give bitwise the
+    result of plans carrying ifgfb_row_tiles_fill's records."""
+    from paper_2408_02274_b200.engine import FarFieldPlan
+    inp, z = inputs("c1"), golden("c1")
+    outs = []
+    for mode in ("l1", "l1free"):
+        monkeypatch.setenv("IFGFB_K4", mode)
+        plan = FarFieldPlan(inp["tree"], inp["hier"], inp["disc"].normals, 1e-6,
+                            kappas=inp["kappas"], geometry_on_device=geometry_on_device)
+        import torch
+        dev = torch.device("cuda")
+        w = torch.from_numpy(np.ascontiguousarray(z["weights"])).to(dev)
+        out = torch.empty((w.shape[0], 2, w.shape[1]), dtype=torch.complex128, device=dev)
+        od = torch.empty_like(out)
+        plan.far_apply_device(w, inp["kappas"], out, od)
+        outs.append((out.cpu().numpy(), od.cpu().numpy(), plan.device_bytes()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    assert outs[1][2] < outs[0][2]        # no tile records on the device
