@@ -265,6 +265,7 @@ struct Plan {
   double* phi = nullptr;        // 8*N complex
   double* phiw = nullptr;       // 8*N complex (phi * weights)
   double* pcoef = nullptr;      // 8*P*n_c^2 complex
+  double* phi_pm = nullptr;     // N * [phi(8) | phi*w(8)] complex (point-major)
   double* far_out = nullptr;    // 16*N complex (8 ch x 2 k, original order)
   double* far_disp = nullptr;
   double* s_val = nullptr;      // 8*2*N complex

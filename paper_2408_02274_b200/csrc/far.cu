@@ -1086,13 +1086,31 @@ __global__ void emit_reduce(int n, int pair_lo, int pair_hi,
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * NCOL) return;
   const int t = idx / NCOL, m = idx % NCOL;
-  const int q0 = tgt_off[t], q1 = tgt_off[t + 1];
+  int q0 = tgt_off[t], q1 = tgt_off[t + 1];
   if (q0 == q1) return;
+  // a target's pairs are in box (= pair index) order, so the pairs of the
+  // active range [pair_lo, pair_hi) (a streaming part) are one contiguous run
+  // of its list: binary search both ends instead of scanning every pair
+  // once per part
+  if (tgt_pairs[q0] < pair_lo || tgt_pairs[q1 - 1] >= pair_hi) {
+    int lo = q0, hi = q1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (tgt_pairs[mid] < pair_lo) lo = mid + 1; else hi = mid;
+    }
+    int lo2 = lo, hi2 = q1;
+    while (lo2 < hi2) {
+      const int mid = (lo2 + hi2) >> 1;
+      if (tgt_pairs[mid] < pair_hi) lo2 = mid + 1; else hi2 = mid;
+    }
+    q0 = lo;
+    q1 = lo2;
+    if (q0 == q1) return;
+  }
   double2 s = out[idx];
   double2 sd = out_disp ? out_disp[idx] : make_double2(0.0, 0.0);
   for (int q = q0; q < q1; ++q) {
     const int pq = tgt_pairs[q];
-    if (pq < pair_lo || pq >= pair_hi) continue;   // another rank's source box
     const size_t pr = pq;
     const double2 v = partial[(pr * 2) * NCOL + m];
     s.x += v.x;

@@ -37,10 +37,13 @@ __device__ __forceinline__ double2 csub(double2 a, double2 b) {
 // One CTA per patch (n_c^2 threads): y -> (m, j) Cartesian, surface
 // divergences, phi (8,N), phi * weights (8,N) and per-patch Chebyshev
 // coefficient grids of phi (8,P,n_c,n_c).
+// Also writes phi_pm, point-major rows [phi(8) | phi*w(8)] (256 B per point)
+// for the near field's source gathers: one row per direct entry instead of
+// 8 channel-strided loads.
 __global__ void pack_kernel(SurfPtrs s, const double2* __restrict__ y,
                             const double2* __restrict__ phi_in,
                             double2* __restrict__ phi, double2* __restrict__ phiw,
-                            double2* __restrict__ pcoef) {
+                            double2* __restrict__ pcoef, double2* __restrict__ phi_pm) {
   extern __shared__ double2 sh[];
   const int nc = s.n_c, n2 = nc * nc;
   double2* gu = sh;            // 2 x n2 : J f^u for (j, m)
@@ -60,6 +63,8 @@ __global__ void pack_kernel(SurfPtrs s, const double2* __restrict__ y,
       const double2 v = phi_in[(size_t)c * n + ell];
       phi[(size_t)c * n + ell] = v;
       phiw[(size_t)c * n + ell] = cscale(wq, v);
+      phi_pm[(size_t)ell * 16 + c] = v;
+      phi_pm[(size_t)ell * 16 + 8 + c] = cscale(wq, v);
       gp[c * n2 + loc] = v;
     }
   }
@@ -110,6 +115,8 @@ __global__ void pack_kernel(SurfPtrs s, const double2* __restrict__ y,
     for (int c = 0; c < 8; ++c) {
       phi[(size_t)c * n + ell] = vals[c];
       phiw[(size_t)c * n + ell] = cscale(wq, vals[c]);
+      phi_pm[(size_t)ell * 16 + c] = vals[c];
+      phi_pm[(size_t)ell * 16 + 8 + c] = cscale(wq, vals[c]);
       gp[c * n2 + loc] = vals[c];
     }
   }
@@ -140,6 +147,7 @@ struct NearArgs {
   const int* mom_off; const int* mom_patch; const double2* moments;
   const int* dir_off; const int* dir_src;
   const double2* phi; const double2* phiw; const double2* pcoef;
+  const double2* phi_pm;                        // [N][phi(8) | phi*w(8)]
   const double2* far; const double2* far_disp;  // (8,2,N)
   double kr[2], ki[2];
   double fd_step;
@@ -245,7 +253,7 @@ __global__ void __launch_bounds__(128, IFGFB_NEAR_MINB) near_kernel(NearArgs a) 
 #pragma unroll
       for (int k = 0; k < 2; ++k) kernel_pair(a.kr[k], a.ki[k], r, ndx, gk[k], qk[k]);
       const double jw = neg ? a.s.wq[src] : 1.0;
-      const double2* wsrc = neg ? a.phi : a.phiw;
+      const double2* wrow = a.phi_pm + (size_t)src * 16 + (neg ? 0 : 8);
       if (neg) {
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -255,7 +263,7 @@ __global__ void __launch_bounds__(128, IFGFB_NEAR_MINB) near_kernel(NearArgs a) 
       }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const double2 w = wsrc[(size_t)c * n + src];
+        const double2 w = wrow[c];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           S[c][k] = cadd(S[c][k], cmul(gk[k], w));
@@ -351,7 +359,7 @@ __global__ void __launch_bounds__(128, IFGFB_NEAR_DIRECT_MINB) near_direct_kerne
 #pragma unroll
     for (int k = 0; k < 2; ++k) kernel_pair(a.kr[k], a.ki[k], r, ndx, gk[k], qk[k]);
     const double jw = neg ? -a.s.wq[src] : 1.0;      // corrections subtract
-    const double2* wsrc = neg ? a.phi : a.phiw;
+    const double2* wrow = a.phi_pm + (size_t)src * 16 + (neg ? 0 : 8);
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       gk[k] = cscale(jw, gk[k]);
@@ -359,7 +367,7 @@ __global__ void __launch_bounds__(128, IFGFB_NEAR_DIRECT_MINB) near_direct_kerne
     }
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      const double2 w = wsrc[(size_t)c * n + src];
+      const double2 w = wrow[c];
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         S[c][k] = cadd(S[c][k], cmul(gk[k], w));
@@ -542,6 +550,7 @@ static int near_launch(Plan& p, cudaStream_t st) {
               reinterpret_cast<const double2*>(p.phi),
               reinterpret_cast<const double2*>(p.phiw),
               reinterpret_cast<const double2*>(p.pcoef),
+              reinterpret_cast<const double2*>(p.phi_pm),
               reinterpret_cast<const double2*>(p.far_out),
               reinterpret_cast<const double2*>(p.far_disp),
               {p.kappa[0], p.kappa[2]}, {p.kappa[1], p.kappa[3]}, p.fd_step,
@@ -600,7 +609,8 @@ static int pack_launch(Plan& p, const double* y, const double* phi_in,
   pack_kernel<<<p.n_patches, threads, sm, st>>>(
       surf(p), reinterpret_cast<const double2*>(y),
       reinterpret_cast<const double2*>(phi_in), reinterpret_cast<double2*>(p.phi),
-      reinterpret_cast<double2*>(p.phiw), reinterpret_cast<double2*>(p.pcoef));
+      reinterpret_cast<double2*>(p.phiw), reinterpret_cast<double2*>(p.pcoef),
+      reinterpret_cast<double2*>(p.phi_pm));
   p.timer.end(tk, st);
   p.launches += 1;
   IFGFB_CUDA(cudaGetLastError());
@@ -694,6 +704,7 @@ int ifgfb_plan_set_surface(ifgfb_plan* h, const ifgfb_surface_desc* d) {
   RC(dev_upload<double>(p, &p.phi, nullptr, 16 * n));
   RC(dev_upload<double>(p, &p.phiw, nullptr, 16 * n));
   RC(dev_upload<double>(p, &p.pcoef, nullptr, 16 * n));
+  RC(dev_upload<double>(p, &p.phi_pm, nullptr, 32 * n));
   RC(dev_upload<double>(p, &p.far_out, nullptr, 32 * n));
   RC(dev_upload<double>(p, &p.far_disp, nullptr, 32 * n));
   RC(dev_upload<double>(p, &p.s_val, nullptr, 32 * n));
