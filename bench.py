@@ -575,6 +575,8 @@ def run_b200(args):
                    "plan_build_s": round(t_plan, 1),
                    "device_plan_gib": round(op.plan.device_bytes() / 2**30, 2),
                    "geometry_on_device_levels": sorted(getattr(op.plan, "otf_levels", [])),
+                   "k4_tiles": ("formed on the device (no tile records)"
+                                if getattr(op.plan, "tile_free", False) else "host records"),
                    "stream_parts": int(getattr(op.plan, "stream_parts", 1) or 1)},
         "roofline": {"kernel": "propagate (K4: child->parent re-interpolation on "
                                "FP64 DMMA + fused K3)" + (" of rank 0" if world > 1 else ""),

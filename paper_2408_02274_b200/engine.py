@@ -24,17 +24,18 @@ def device_stream():
     return torch.cuda.current_stream().cuda_stream
 
 
-K4_MODES = ("l1free", "l1", "ringfree", "ring")
+K4_MODES = ("auto", "l1", "l1free", "ring", "ringfree")
 
 
 def k4_mode() -> str:
-    """Propagation kernel (env IFGFB_K4): "l1free" (default; child blocks
-    streamed through L1, MMA row tiles formed on the device from the nodes'
-    sigma groups: no tile records in the plan), "l1" (same kernel reading
-    host-built tile records), "ringfree" / "ring" (child blocks staged in a
-    shared-memory ring by TMA bulk copies; measured slower, DESIGN 4)."""
+    """Propagation kernel (env IFGFB_K4): "auto" (default: the L1-streaming
+    kernel with host-built MMA tile records while the plan fits, else
+    "l1free"), "l1" (tile records), "l1free" (tiles formed on the device
+    from the nodes' sigma groups: no tile records in the plan, ~6% slower),
+    "ring" / "ringfree" (child blocks staged in a shared-memory ring by TMA
+    bulk copies; measured 45% slower, DESIGN 4)."""
     import os
-    m = os.environ.get("IFGFB_K4", "l1free")
+    m = os.environ.get("IFGFB_K4", "auto")
     if m not in K4_MODES:
         raise ValueError(f"IFGFB_K4: unknown propagation kernel {m!r}")
     return m
@@ -174,25 +175,34 @@ class FarFieldPlan:
         import os
         policy = policy or os.environ.get("IFGFB_GEOM_ON_DEVICE", "auto")
         levels = list(range(4, self.depth + 1))
-        if policy == "none":
-            return set()
-        if policy == "all":
-            return set(levels)
-        if policy != "auto":
+        mode = k4_mode()
+        self.tile_free = mode.endswith("free")
+        if policy not in ("none", "all", "auto"):
             raise ValueError(f"geometry_on_device: unknown policy {policy!r}")
         info = {}
-        fixed = 0
+        fixed = tile_total = 0
         for d in levels:
             ap = accumulation_plan(self.tree, self.hier, d)
             info[d] = (ap.n_types * self.TYPE_TABLE_BYTES, ap.n_types / max(1, ap.n_instances))
-            tile_bytes = 0 if k4_mode().endswith("free") else 12 * 16 + 20   # records + tile_off
-            fixed += (ap.n_instances * (tile_bytes + 8) + int(ap.inst_crow_off[-1]) * 4
+            fixed += (ap.n_instances * 8 + int(ap.inst_crow_off[-1]) * 4
                       + ap.n_types * 75)                                  # group ids
+            tile_total += ap.n_instances * (12 * 16 + 20)                 # records + tile_off
         pairs = [self.hier.level(d).cpt_idx.size for d in range(3, self.depth + 1)]
         fixed += sum(pairs) * 80 + max(pairs, default=0) * 2 * 16 * 16
         budget = 0.55 * torch.cuda.get_device_properties(
             torch.cuda.current_device()).total_memory
         tables = sum(b for b, _ in info.values())
+        if mode == "auto":
+            # tile records make the propagation ~6% faster (the kernel reads
+            # them instead of forming tiles); drop them when the plan would
+            # not fit with every level's node tables
+            self.tile_free = fixed + tables + tile_total > budget
+        if not self.tile_free:
+            fixed += tile_total
+        if policy == "none":
+            return set()
+        if policy == "all":
+            return set(levels)
         # a level whose tables are below min_frac of the device memory cannot
         # relieve it, while on-device geometry costs FP64 work (acos, atan2,
         # sincos per node and instance) on the pipe the DMMAs use: keep its
@@ -215,7 +225,7 @@ class FarFieldPlan:
         self._log(f"accum plan {d}")
         # crow rows are reproduced exactly as the reference's searchsorted
         # picks them (ifgf.py:743-746), including any inexact hit.
-        tile_free = k4_mode().endswith("free")
+        tile_free = self.tile_free
         if tile_free:
             row_order, row_cuts = row_order_cuts(ap)
             tile_off = tiles = None

@@ -100,27 +100,28 @@ def classify_targets(disc: SurfaceDiscretization,
     grid = cheb.nodes(disc.n_c)
     global _CLASSIFY_CTX
     _CLASSIFY_CTX = (disc, pts, delta, grid, on_surface, t0, t1, _point_index(pts))
-    found = [[] for _ in range(n_t)]
-    # per-patch work is independent; entries are sorted per target below, so
-    # the merge order does not matter (the golden-section loops are
-    # Python-bound: processes when fork is available, else in-process)
-    for hits in _map_patches(_classify_patch, disc.n_patches):
-        for ell, ent in hits:
-            found[ell - t0].append(ent)
+    # per-patch work is independent (the golden-section loops are
+    # Python-bound: processes when fork is available, else in-process); each
+    # patch returns its hits as arrays, merged here and sorted per target by
+    # patch id (a patch appears at most once per target)
+    parts = [(p, h) for p, h in enumerate(_map_patches(_classify_patch, disc.n_patches))
+             if h is not None and h[0].size]
     _CLASSIFY_CTX = None
+    if parts:
+        ell = np.concatenate([h[0] for _, h in parts]) - t0
+        pid = np.concatenate([np.full(h[0].size, p, dtype=np.int64) for p, h in parts])
+        uv = np.concatenate([h[1] for _, h in parts])
+        dist = np.concatenate([h[2] for _, h in parts])
+        order = np.lexsort((pid, ell))
+        ell, pid, uv, dist = ell[order], pid[order], uv[order], dist[order]
+    else:
+        ell = pid = np.empty(0, np.int64)
+        uv, dist = np.empty((0, 2)), np.empty(0)
     offsets = np.zeros(n_t + 1, dtype=np.int64)
-    ids, uvs, ds = [], [], []
-    for ell in range(n_t):
-        ent = sorted(found[ell])
-        offsets[ell + 1] = offsets[ell] + len(ent)
-        for p, u, v, dd in ent:
-            ids.append(p)
-            uvs.append((u, v))
-            ds.append(dd)
-    return SingularityMap(n_t, disc.n_patches, delta, offsets,
-                          np.asarray(ids, dtype=np.int32),
-                          np.asarray(uvs, dtype=float).reshape(-1, 2),
-                          np.asarray(ds, dtype=float), t0)
+    np.cumsum(np.bincount(ell, minlength=n_t), out=offsets[1:])
+    return SingularityMap(n_t, disc.n_patches, delta, offsets, pid.astype(np.int32),
+                          np.ascontiguousarray(uv, dtype=float).reshape(-1, 2),
+                          np.ascontiguousarray(dist, dtype=float), t0)
 
 
 _CLASSIFY_CTX = None
@@ -160,9 +161,19 @@ def _map_patches(fn, n_patches):
 
 
 def _classify_patch(p):
-    """Singular/near pairs of patch p (runs in a worker process); targets
-    outside [t0, t1) are searched (same batch as the full map) but not
-    reported."""
+    """Singular/near pairs of patch p (runs in a worker process): arrays
+    (targets, (u, v), distances), or None.  Targets outside [t0, t1) are
+    searched (same batch as the full map) but not reported."""
+    hits = _classify_patch_list(p)
+    if not hits:
+        return None
+    ell = np.array([h[0] for h in hits], dtype=np.int64)
+    uv = np.array([(h[1][1], h[1][2]) for h in hits], dtype=float).reshape(-1, 2)
+    dist = np.array([h[1][3] for h in hits], dtype=float)
+    return ell, uv, dist
+
+
+def _classify_patch_list(p):
     disc, pts, delta, grid, on_surface, t0, t1, kd = _CLASSIFY_CTX
     patch = disc.patches[p]
     hits = []
@@ -419,23 +430,24 @@ def correction_pairs(disc: SurfaceDiscretization, tree,
     yields its targets' entries in the same order)."""
     coords = tree.point_level_coords(tree.depth)
     n2 = disc.n_c**2
-    ells, srcs = [], []
-    # per-patch target lists in one pass (pairs_for_patch scans the whole
-    # map per patch)
+    # (patch, target) pairs in ascending patch order, targets ascending
+    # within a patch; chunks of pairs on the plan thread pool, each pair
+    # against the patch's n_c^2 sources (Chebyshev-box separation >= 2)
     order = np.argsort(smap.patch_ids, kind="stable")
-    bounds = np.searchsorted(smap.patch_ids[order],
-                             np.arange(disc.n_patches + 1))
-    tg_all = (np.repeat(np.arange(smap.n_targets, dtype=np.int64),
-                        np.diff(smap.offsets)) + smap.target_lo)
-    for p in np.nonzero(np.diff(bounds))[0]:
-        p = int(p)
-        tg = tg_all[order[bounds[p]:bounds[p + 1]]]
-        s0 = p * n2
-        sep = np.abs(coords[s0:s0 + n2][None, :, :] -
-                     coords[tg][:, None, :]).max(-1)
+    pid = smap.patch_ids[order].astype(np.int64)
+    tg = (np.repeat(np.arange(smap.n_targets, dtype=np.int64),
+                    np.diff(smap.offsets)) + smap.target_lo)[order]
+    step = max(1, (1 << 22) // n2)
+    chunks = [(i, min(pid.size, i + step)) for i in range(0, pid.size, step)]
+
+    def one(rng):
+        i0, i1 = rng
+        src = pid[i0:i1, None] * n2 + np.arange(n2)[None, :]
+        sep = np.abs(coords[src] - coords[tg[i0:i1]][:, None, :]).max(-1)
         ti, si = np.nonzero(sep >= 2)
-        ells.append(tg[ti])
-        srcs.append((s0 + si).astype(np.int64))
-    ell = np.concatenate(ells) if ells else np.empty(0, dtype=np.int64)
-    src = np.concatenate(srcs) if srcs else np.empty(0, dtype=np.int64)
-    return CorrectionPairs(ell, src)
+        return tg[i0:i1][ti], src[ti, si]
+
+    res = list(_pool().map(one, chunks))
+    ell = np.concatenate([r[0] for r in res]) if res else np.empty(0, dtype=np.int64)
+    src = np.concatenate([r[1] for r in res]) if res else np.empty(0, dtype=np.int64)
+    return CorrectionPairs(ell.astype(np.int64), src.astype(np.int64))

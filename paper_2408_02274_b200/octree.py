@@ -865,8 +865,7 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
     lvl = tree.level(d)
     nn = hier.config.p_s * hier.config.p_a ** 2
     octant = (lvl.codes & np.uint64(7)).astype(np.int64)
-    prow, child = _expand_ranges(pcl.seg_off[lvl.parent],
-                                 pcl.seg_off[lvl.parent + 1])
+    prow, child = _parent_row_major_instances(lvl.parent, pcl.seg_off)
     key = pcl.seg_ids[prow] * 8 + octant[child]
     ukeys, inst_type = np.unique(key, return_inverse=True)
     del key
@@ -926,27 +925,54 @@ def accumulation_plan(tree: BoxTree, hier: ConeHierarchy, d: int,
                                      scatter, node_geom, node_r, prow, child, inst_type, log)
 
 
+def _parent_row_major_instances(parent: np.ndarray, pseg_off: np.ndarray):
+    """(parent segment row, child box) of every propagation instance, sorted
+    by parent row then child, built directly: the children of a parent box
+    are consecutive boxes and its rows are consecutive, so each parent box
+    contributes a rows x children block in row-major order (the same order
+    np.lexsort((child, prow)) gives, without the sort)."""
+    nb = parent.size
+    if nb == 0:
+        z = np.empty(0, np.int64)
+        return z, z
+    new = np.ones(nb, dtype=bool)
+    new[1:] = parent[1:] != parent[:-1]
+    first = np.nonzero(new)[0]                      # first child of each parent box
+    kids = np.diff(np.append(first, nb))
+    pb = parent[first]
+    r0 = pseg_off[pb]
+    rows = pseg_off[pb + 1] - r0
+    local, own = _expand_ranges(np.zeros(pb.size, np.int64), rows * kids)
+    k = kids[own]
+    return r0[own] + local // k, first[own] + local % k
+
+
 def _finish_accumulation_plan(cache, d, cl, pcl, gamma, toct, sig_off, g_sigma, gid,
                               scatter, node_geom, node_r, prow, child, inst_type, log,
                               pending=None):
     n_t = gamma.size
-    # instances sorted by (parent row, child): prow/child are generated
-    # child-major, so re-sort
-    order = np.lexsort((child, prow))
-    prow, child, inst_type = prow[order], child[order], inst_type[order]
-    del order
+    # instances are already sorted by (parent row, child)
     nsig = np.diff(sig_off)[inst_type]
     crow_off = np.zeros(prow.size + 1, dtype=np.int64)
     np.cumsum(nsig, out=crow_off[1:])
-    gidx, g_own = _expand_ranges(sig_off[inst_type], sig_off[inst_type + 1])
     bkeys = box_keys(cl)
-    want = child[g_own] * np.int64(id_stride(cl)) + g_sigma[gidx]
-    del gidx, g_own
-    crow = np.searchsorted(bkeys, want).astype(np.int64)
-    misses = int(np.count_nonzero(
-        bkeys[np.minimum(crow, bkeys.size - 1)] != want))
-    del want
-    log("instance sort + child rows")
+    stride = np.int64(id_stride(cl))
+    crow = np.empty(int(crow_off[-1]), dtype=np.int64)
+    misses = []
+
+    def rows_of(rng):      # child segment row of every (instance, group)
+        i0, i1 = rng
+        gidx, g_own = _expand_ranges(sig_off[inst_type[i0:i1]], sig_off[inst_type[i0:i1] + 1])
+        want = child[i0:i1][g_own] * stride + g_sigma[gidx]
+        c = np.searchsorted(bkeys, want)
+        misses.append(int(np.count_nonzero(bkeys[np.minimum(c, bkeys.size - 1)] != want)))
+        crow[crow_off[i0]:crow_off[i1]] = c
+
+    step = 1 << 20
+    list(_pool().map(rows_of, [(i, min(prow.size, i + step))
+                               for i in range(0, prow.size, step)]))
+    misses = sum(misses)
+    log("child rows")
     plan = AccumulationPlan(
         level=d, n_types=n_t, type_gamma=gamma, type_octant=toct,
         sig_off=sig_off, group_sigma=g_sigma, gid=gid, scatter=scatter,
