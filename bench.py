@@ -412,7 +412,7 @@ def run_b200(args):
     import torch
     import torch.distributed as dist
     from paper_2408_02274_b200.build import build
-    from paper_2408_02274_b200.engine import kernel_times, set_kernel_timing
+    from paper_2408_02274_b200.engine import kernel_times, level_times, set_kernel_timing
     from paper_2408_02274_b200.operator import MullerOperator
 
     rank, world, local = dist_env()
@@ -491,6 +491,7 @@ def run_b200(args):
     ms_steps = [a.elapsed_time(b) for a, b in evs]
     ms = sum(ms_steps) / len(ms_steps)
     ktimes = kernel_times(op.plan)
+    ltimes = level_times(op.plan)
     set_kernel_timing(op.plan, False)
     rank_info = {"ms": ms, "plan_s": t_plan, "device_gib": op.plan.device_bytes() / 2**30,
                  "prop_gflop": counts["prop"] / 1e9, "total_gflop": counts["total"] / 1e9}
@@ -566,9 +567,9 @@ def run_b200(args):
                    "algorithmic_gflop_per_matvec": total_flop / 1e9,
                    "l2": "flushed (256 MB write) before every timed step",
                    "parallelism": par,
-                   "moments": ("device kernel (beta_d at its ~1e-7 conditioning: apply "
-                               "parity 5e-9 vs the reference at cfg 1, "
-                               "tests/test_gpu_moments.py)" if dev_mom else
+                   "moments": ("device kernel, exact mode (host graded nodes, reference "
+                               "operation order: beta_s/beta_d to rounding, apply parity "
+                               "< 1e-10 at c1/c2n4, tests/test_gpu_moments.py)" if dev_mom else
                                "host restatement (reference-exact)"),
                    "plan_builder": ("device (cones + propagation types, "
                                     "csrc/planbuild.cu)" if dev_mom else "host numpy"),
@@ -589,7 +590,14 @@ def run_b200(args):
                      "peak_source": "FP64 mma.sync m8n8k4 measured on B200 "
                                     "(tools/fp64_peak.cu, profiles/fp64_peak_r01.txt); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
-                     "share_of_step": prop_ms / args.steps / ms},
+                     "share_of_step": prop_ms / args.steps / ms,
+                     "by_level": {
+                         str(d): {"ms_per_step": round(t / args.steps, 3),
+                                  "tflops": (round(counts["prop_by_level"][d] * args.steps
+                                                   / (t * 1e-3) / 1e12, 2)
+                                             if t > 0 and d in counts["prop_by_level"] else None),
+                                  "geometry_on_device": d in getattr(op.plan, "otf_levels", [])}
+                         for d, (t, _n) in sorted(ltimes.items())}},
         "kernels": kern,
         "e2e": {"value": unknowns / e2e_s, "unit": "unknowns*matvec/s",
                 "h2d_bytes_per_step": unknowns * 16 * world,

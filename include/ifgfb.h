@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define IFGFB_ABI_VERSION 6
+#define IFGFB_ABI_VERSION 7
 
 enum {
   IFGFB_OK = 0,
@@ -223,6 +223,18 @@ typedef struct {
   const double* base;           /* n_beta */
   const double* weights;        /* n_beta */
   const double* kappas;         /* 2 complex */
+  /* ABI 7, exact mode: when nodes is non-null it holds per pair the graded
+   * nodes the reference computes on the host (quadrature.py:203-228
+   * clustered_nodes: np.power is not reproducible on the device) as
+   * [xi_u, dxi_u, xi_v, dxi_v] x n_beta, and the device evaluates the patch
+   * geometry in the reference's float64 operation order (numpy elementwise,
+   * OpenBLAS dgemm: sequential FMA over k, except result columns >= gemm_tail
+   * which use 8 k-interleaved lanes + a pairwise tree; 0 = no tail), so beta_d
+   * matches the reference to rounding instead of to its ~1e-7 conditioning.
+   * nodes == NULL: graded map on the device (uv used). */
+  const double* nodes;          /* n_pairs*4*n_beta, or NULL */
+  int32_t gemm_tail_u;          /* u contraction (tu @ coeff): column of the tail, 0 = none */
+  int32_t gemm_tail_v;          /* v contraction ((.) @ tv^T): column of the tail, 0 = none */
 } ifgfb_moment_desc;
 int ifgfb_singular_moments(const ifgfb_moment_desc* desc, double* out);
 
@@ -314,6 +326,9 @@ int ifgfb_basis_combine_rows(const double* const* rows, int k, int64_t n,
 #define IFGFB_KERNEL_KINDS 8
 int ifgfb_plan_set_timing(ifgfb_plan* plan, int enable);
 int ifgfb_plan_kernel_times(ifgfb_plan* plan, double* ms, int64_t* counts);
+/* Propagation (class 1) time split by CHILD level d (ms[d], counts[d] for
+ * d < max_levels; levels whose K4 writes level d-1), same accumulators. */
+int ifgfb_plan_level_times(ifgfb_plan* plan, int max_levels, double* ms, int64_t* counts);
 
 /* Number of kernels launched by the last apply on this plan. */
 int64_t ifgfb_plan_last_launches(const ifgfb_plan* plan);

@@ -128,7 +128,8 @@ class MomentDesc(C.Structure):
                 ("n_patches", C.c_int32), ("n_p", C.c_int32),
                 ("patch_coeffs", _dp), ("n_c", C.c_int32),
                 ("n_beta", C.c_int32), ("grading", C.c_int32),
-                ("base", _dp), ("weights", _dp), ("kappas", _dp)]
+                ("base", _dp), ("weights", _dp), ("kappas", _dp),
+                ("nodes", _dp), ("gemm_tail_u", C.c_int32), ("gemm_tail_v", C.c_int32)]
 
 
 EXPORTS = {
@@ -148,6 +149,7 @@ EXPORTS = {
     "ifgfb_plan_last_launches": ([C.c_void_p], C.c_int64),
     "ifgfb_plan_set_timing": ([C.c_void_p, C.c_int], C.c_int),
     "ifgfb_plan_kernel_times": ([C.c_void_p, _dp, _ip], C.c_int),
+    "ifgfb_plan_level_times": ([C.c_void_p, C.c_int, _dp, _ip], C.c_int),
     "ifgfb_far_apply": ([C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int,
                          C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_potentials": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -199,7 +201,7 @@ EXPORTS = {
                          C.c_void_p], C.c_int),
 }
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 _lib = None
 
 

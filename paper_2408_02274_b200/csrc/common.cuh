@@ -128,8 +128,12 @@ struct KTimer {
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
   std::vector<int> kinds;
+  std::vector<int> lvls;
   double ms[K_NKINDS] = {};
   int64_t count[K_NKINDS] = {};
+  static constexpr int MAXLV = 32;
+  double lvl_ms[MAXLV] = {};          // propagation (K_ACCUM) per child level
+  int64_t lvl_count[MAXLV] = {};
 
   cudaEvent_t next() {
     if (used == pool.size()) {
@@ -140,11 +144,12 @@ struct KTimer {
     return pool[used++];
   }
   // returns a token (index of the start event) or -1 when off
-  int begin(int kind, cudaStream_t st) {
+  int begin(int kind, cudaStream_t st, int level = -1) {
     if (!on) return -1;
     const int tok = (int)used;
     cudaEventRecord(next(), st);
     kinds.push_back(kind);
+    lvls.push_back(level);
     return tok;
   }
   void end(int tok, cudaStream_t st) {
@@ -159,13 +164,19 @@ struct KTimer {
       cudaEventElapsedTime(&t, pool[2 * i], pool[2 * i + 1]);
       ms[kinds[i]] += t;
       count[kinds[i]] += 1;
+      if (lvls[i] >= 0 && lvls[i] < MAXLV) {
+        lvl_ms[lvls[i]] += t;
+        lvl_count[lvls[i]] += 1;
+      }
     }
     kinds.clear();
+    lvls.clear();
     used = 0;
   }
   void reset() {
     collect();
     for (int k = 0; k < K_NKINDS; ++k) { ms[k] = 0; count[k] = 0; }
+    for (int k = 0; k < MAXLV; ++k) { lvl_ms[k] = 0; lvl_count[k] = 0; }
   }
 };
 

@@ -1314,7 +1314,7 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
             aa.child_lo = L.seg_lo();
             aa.child_hi = L.seg_hi();
             const int nrows = U.seg_hi() - U.seg_lo();
-            const int tk = p.timer.begin(K_ACCUM, st);
+            const int tk = p.timer.begin(K_ACCUM, st, d);
             const int grid = (nrows + IFGFB_ACC_ROWS - 1) / IFGFB_ACC_ROWS;
             const bool wide = L.max_groups > MAX_GROUPS;
             if (L.otf)

@@ -28,7 +28,33 @@ struct MomArgs {
   double kr[2], ki[2];
   double2* out;                 // pair x 4 x nc x nc
   int64_t pair0;
+  const double* nodes;          // optional: pair x 4 x nb (xi_u, dxi_u, xi_v, dxi_v)
+  int tail_u, tail_v;           // first column of the 8-lane gemm order (exact mode)
 };
+
+// Exact mode (nodes given): the geometry at the clustered grid reproduces the
+// reference's float64 values bit for bit.  The graded map (np.power) comes
+// from the host; the device replays numpy's elementwise operation order
+// without contraction (chebyshev_basis, np.cross, norm, sum over axis 0,
+// einsum "cbij,bc->bij") and OpenBLAS's dgemm order for the two position
+// products (tu @ coeff, (.) @ tv^T): a sequential FMA chain over k per
+// column, except the columns of an N-tail (>= tail) which OpenBLAS 0.3.30
+// (SkylakeX) reduces as 8 k-interleaved FMA lanes + a pairwise tree
+// (verified for n_p = 8, 10, 20 in this build's tests).  This matters because
+// (x - y(u, v)).n_x loses ~8 digits at the clustered nodes: any other
+// rounding of y moves beta_d by ~1e-7.
+__device__ __forceinline__ double dot_exact(const double* a, int sa, const double* b, int sb,
+                                            int k, bool tail) {
+  if (!tail) {
+    double s = 0.0;
+    for (int m = 0; m < k; ++m) s = __fma_rn(a[m * sa], b[m * sb], s);
+    return s;
+  }
+  double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int m = 0; m < k; ++m) q[m & 7] = __fma_rn(a[m * sa], b[m * sb], q[m & 7]);
+  return __dadd_rn(__dadd_rn(__dadd_rn(q[0], q[1]), __dadd_rn(q[2], q[3])),
+                   __dadd_rn(__dadd_rn(q[4], q[5]), __dadd_rn(q[6], q[7])));
+}
 
 __device__ __forceinline__ double nu(double tau, double d) {
   const double q = (M_PI - tau) / M_PI;
@@ -96,29 +122,35 @@ __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a) {
     const int i = e % nb;
     const bool isv = e >= nb;
     double xi, dxi;
-    clustered(isv ? v0 : u0, a.base[i], a.d, xi, dxi);
+    if (a.nodes) {
+      const double* nd = a.nodes + ((size_t)blockIdx.x * 4 + (isv ? 2 : 0)) * nb;
+      xi = nd[i];
+      dxi = nd[nb + i];
+    } else {
+      clustered(isv ? v0 : u0, a.base[i], a.d, xi, dxi);
+    }
+    // reference chebyshev_basis: out[i] = 2.0 * x * out[i-1] - out[i-2]
+    const double x2 = 2.0 * xi;   // exact
     double* T = (isv ? tv : tu) + i * np_;
     T[0] = 1.0;
     if (np_ > 1) T[1] = xi;
-    for (int m = 2; m < np_; ++m) T[m] = 2.0 * xi * T[m - 1] - T[m - 2];
-    const double sc = dxi * a.wb[i];
+    for (int m = 2; m < np_; ++m) T[m] = __dsub_rn(__dmul_rn(x2, T[m - 1]), T[m - 2]);
+    const double sc = __dmul_rn(dxi, a.wb[i]);
     double t0 = 1.0, t1 = xi;
     for (int m = 0; m < nc; ++m) {
       double tm;
       if (m == 0) tm = 1.0;
       else if (m == 1) tm = xi;
-      else { tm = 2.0 * xi * t1 - t0; t0 = t1; t1 = tm; }
-      if (isv) pvw[i * nc + m] = tm * sc;
-      else put[m * nb + i] = tm * sc;
+      else { tm = __dsub_rn(__dmul_rn(x2, t1), t0); t0 = t1; t1 = tm; }
+      if (isv) pvw[i * nc + m] = __dmul_rn(tm, sc);
+      else put[m * nb + i] = __dmul_rn(tm, sc);
     }
   }
   __syncthreads();
   // A[c][i][n] = sum_m tu[i][m] cf[c][m][n]  (numpy: tu @ cf[c])
   for (int e = tid; e < 9 * nb * np_; e += blockDim.x) {
     const int n = e % np_, i = (e / np_) % nb, c = e / (np_ * nb);
-    double s = 0.0;
-    for (int m = 0; m < np_; ++m) s += tu[i * np_ + m] * cf[(c * np_ + m) * np_ + n];
-    A[e] = s;
+    A[e] = dot_exact(tu + i * np_, 1, cf + c * np_ * np_ + n, np_, np_, n >= a.tail_u);
   }
   __syncthreads();
   const double x0 = a.txyz[3 * pair], x1 = a.txyz[3 * pair + 1], x2 = a.txyz[3 * pair + 2];
@@ -130,35 +162,44 @@ __global__ void __launch_bounds__(MOM_THREADS) moments_kernel(MomArgs a) {
     for (int e = tid; e < rc * nb; e += blockDim.x) {
       const int ii = e / nb, j = e % nb, i = i0 + ii;
       double g[9];
+      const bool tl = j >= a.tail_v;
 #pragma unroll
-      for (int c = 0; c < 9; ++c) {
-        const double* Ar = A + (c * nb + i) * np_;
-        const double* tr = tv + j * np_;
-        double s = 0.0;
-        for (int n = 0; n < np_; ++n) s += Ar[n] * tr[n];
-        g[c] = s;
-      }
-      // g[0..2] position, g[3..5] e_u, g[6..8] e_v
-      const double cx = g[4] * g[8] - g[5] * g[7];
-      const double cy = g[5] * g[6] - g[3] * g[8];
-      const double cz = g[3] * g[7] - g[4] * g[6];
-      const double jac = sqrt(cx * cx + cy * cy + cz * cz);
-      const double dx = x0 - g[0], dy = x1 - g[1], dz = x2 - g[2];
-      const double r2 = dx * dx + dy * dy + dz * dz;
+      for (int c = 0; c < 9; ++c)
+        g[c] = dot_exact(A + (c * nb + i) * np_, 1, tv + j * np_, 1, np_, tl);
+      // g[0..2] position, g[3..5] e_u, g[6..8] e_v; numpy's np.cross and
+      // norm / sum orders, no contraction (reference quadrature.py:310-317)
+      const double cx = __dsub_rn(__dmul_rn(g[4], g[8]), __dmul_rn(g[5], g[7]));
+      const double cy = __dsub_rn(__dmul_rn(g[5], g[6]), __dmul_rn(g[3], g[8]));
+      const double cz = __dsub_rn(__dmul_rn(g[3], g[7]), __dmul_rn(g[4], g[6]));
+      const double jac = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy)),
+                                        __dmul_rn(cz, cz)));
+      const double dx = __dsub_rn(x0, g[0]), dy = __dsub_rn(x1, g[1]), dz = __dsub_rn(x2, g[2]);
+      const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                  __dmul_rn(dz, dz));
       const double r = sqrt(r2);
-      const double ndx = dx * n0 + dy * n1 + dz * n2;
+      const double ndx = __dadd_rn(__dadd_rn(__dmul_rn(dx, n0), __dmul_rn(dy, n1)),
+                                   __dmul_rn(dz, n2));
+      // phase = exp(1j kappa r) / (4 pi r); numpy divides a complex by a real
+      // as a multiply by the reciprocal (Smith's rule with a zero imaginary part)
+      const double inv4pr = __ddiv_rn(1.0, __dmul_rn(4.0 * M_PI, r));
+      const double rr = __dmul_rn(r, r);
+      const double inv_rr = __ddiv_rn(1.0, rr);
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
+        const double tre = -__dmul_rn(a.ki[k], r), tim = __dmul_rn(a.kr[k], r);   // 1j kappa r
         double s, c;
-        sincos(a.kr[k] * r, &s, &c);
-        const double damp = a.ki[k] != 0.0 ? exp(-a.ki[k] * r) : 1.0;
-        const double f = damp / (4.0 * M_PI * r) * jac;
-        const double2 ks = make_double2(c * f, s * f);
-        // (i kappa r - 1) / r^2 * ndx
-        const double2 fac = make_double2((-a.ki[k] * r - 1.0) * ndx / r2,
-                                         a.kr[k] * r * ndx / r2);
+        sincos(tim, &s, &c);
+        const double damp = a.ki[k] != 0.0 ? exp(tre) : 1.0;
+        const double2 ph = make_double2(__dmul_rn(__dmul_rn(damp, c), inv4pr),
+                                        __dmul_rn(__dmul_rn(damp, s), inv4pr));
+        const double2 ks = make_double2(__dmul_rn(ph.x, jac), __dmul_rn(ph.y, jac));
+        // ndx * (1j kappa r - 1) / r**2
+        const double2 fac = make_double2(__dmul_rn(__dmul_rn(ndx, __dsub_rn(tre, 1.0)), inv_rr),
+                                         __dmul_rn(__dmul_rn(ndx, tim), inv_rr));
         K[(k * RC + ii) * nb + j] = ks;
-        K[((2 + k) * RC + ii) * nb + j] = cmul(ks, fac);
+        K[((2 + k) * RC + ii) * nb + j] =
+            make_double2(__fma_rn(ks.x, fac.x, -__dmul_rn(ks.y, fac.y)),
+                         __fma_rn(ks.x, fac.y, __dmul_rn(ks.y, fac.x)));
       }
     }
     __syncthreads();
@@ -212,6 +253,10 @@ extern "C" {
 int ifgfb_singular_moments(const ifgfb_moment_desc* m, double* out) {
   using namespace ifgfb;
   if (!m || !out) { set_error("ifgfb_singular_moments: null argument"); return IFGFB_ERR_ARG; }
+  if (m->gemm_tail_u < 0 || m->gemm_tail_v < 0) {
+    set_error("ifgfb_singular_moments: negative gemm tail");
+    return IFGFB_ERR_ARG;
+  }
   if (m->n_pairs < 0 || m->n_p < 1 || m->n_p > 32 || m->n_c < 1 || m->n_c > 16 ||
       m->n_beta < 1 || m->n_beta > 128 || m->grading < 2 || m->n_patches < 1) {
     set_error("ifgfb_singular_moments: sizes out of range (n_p <= 32, n_c <= 16, "
@@ -264,16 +309,31 @@ int ifgfb_singular_moments(const ifgfb_moment_desc* m, double* out) {
     fail(e, "cudaMemcpy");
   } else {
     MomArgs a{d_x, d_n, d_p, d_uv, d_cf, d_b, d_w, np_, nc, nb, m->grading,
-              {m->kappas[0], m->kappas[2]}, {m->kappas[1], m->kappas[3]}, d_out, 0};
+              {m->kappas[0], m->kappas[2]}, {m->kappas[1], m->kappas[3]}, d_out, 0,
+              nullptr, m->gemm_tail_u > 0 ? m->gemm_tail_u : np_,
+              m->gemm_tail_v > 0 ? m->gemm_tail_v : nb};
+    double* d_nodes = nullptr;
+    if (m->nodes &&
+        (e = cudaMalloc(&d_nodes, std::min<int64_t>(n, chunk) * 4 * nb * sizeof(double))))
+      fail(e, "cudaMalloc");
     for (int64_t c0 = 0; c0 < n && rc == IFGFB_OK; c0 += chunk) {
       const int64_t cn = std::min(chunk, n - c0);
       a.pair0 = c0;
+      if (m->nodes) {
+        if ((e = cudaMemcpy(d_nodes, m->nodes + (size_t)c0 * 4 * nb,
+                            cn * 4 * nb * sizeof(double), cudaMemcpyHostToDevice))) {
+          fail(e, "cudaMemcpy");
+          break;
+        }
+        a.nodes = d_nodes;
+      }
       moments_kernel<<<(unsigned)cn, MOM_THREADS, smem>>>(a);
       if ((e = cudaGetLastError()) ||
           (e = cudaMemcpy(out + (size_t)c0 * out_per * 2, d_out, cn * out_per * sizeof(double2),
                           cudaMemcpyDeviceToHost)))
         fail(e, "moments_kernel");
     }
+    cudaFree(d_nodes);
   }
   cudaFree(d_x); cudaFree(d_n); cudaFree(d_uv); cudaFree(d_p); cudaFree(d_cf);
   cudaFree(d_b); cudaFree(d_w); cudaFree(d_out);

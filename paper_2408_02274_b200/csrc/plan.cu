@@ -401,6 +401,17 @@ int ifgfb_plan_kernel_times(ifgfb_plan* h, double* ms, int64_t* counts) {
   return IFGFB_OK;
 }
 
+int ifgfb_plan_level_times(ifgfb_plan* h, int max_levels, double* ms, int64_t* counts) {
+  CHECK_ARG(h && ms && counts && max_levels >= 0, "null argument");
+  h->p.timer.collect();
+  for (int d = 0; d < max_levels; ++d) {
+    const bool in = d < KTimer::MAXLV;
+    ms[d] = in ? h->p.timer.lvl_ms[d] : 0.0;
+    counts[d] = in ? h->p.timer.lvl_count[d] : 0;
+  }
+  return IFGFB_OK;
+}
+
 int64_t ifgfb_plan_last_launches(const ifgfb_plan* h) {
   return h ? h->p.launches : 0;
 }

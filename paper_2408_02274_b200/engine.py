@@ -421,3 +421,13 @@ def kernel_times(plan: FarFieldPlan) -> dict:
         plan.handle, _lib.dptr(ms), _lib.iptr(cnt)), "ifgfb_plan_kernel_times")
     return {k: (float(ms[i]), int(cnt[i]))
             for i, k in enumerate(_lib.KERNEL_KINDS)}
+
+
+def level_times(plan: FarFieldPlan, max_levels: int = 32) -> dict:
+    """{child level d: (propagation ms, launches)} since the last
+    set_kernel_timing (the propagation class split by the level it reads)."""
+    ms = np.zeros(max_levels)
+    cnt = np.zeros(max_levels, dtype=np.int64)
+    _lib.check(_lib.load().ifgfb_plan_level_times(
+        plan.handle, max_levels, _lib.dptr(ms), _lib.iptr(cnt)), "ifgfb_plan_level_times")
+    return {d: (float(ms[d]), int(cnt[d])) for d in range(max_levels) if cnt[d]}

@@ -276,6 +276,27 @@ def clustered_nodes(alpha, base, d: int):
     return xi, dxi
 
 
+def clustered_nodes_many(alpha, base, d: int):
+    """``clustered_nodes`` for many alphas at once, bitwise equal to it: the
+    graded map (np.power, the costly part) depends on the base node only, so
+    it is evaluated once on one row of base nodes and broadcast; the
+    alpha-dependent remainder is the same elementwise expressions."""
+    t = np.asarray(base, dtype=float)[None, :]
+    a = np.asarray(alpha, dtype=float).reshape(-1)[:, None]
+    sg = np.sign(t)
+    arg = np.pi * np.abs(t)
+    w_mid, g_mid = graded_map(arg, d), _graded_map_prime(arg, d)
+    xi = a + (sg - a) / np.pi * w_mid
+    dxi = (1.0 - a * sg) * g_mid
+    for mask, arg, sign in (((a >= 1.0 - 1e-12)[:, 0], np.pi * np.abs(t - 1.0) / 2.0, 1.0),
+                            ((a <= -1.0 + 1e-12)[:, 0], np.pi * np.abs(t + 1.0) / 2.0, -1.0)):
+        if mask.any():
+            w = graded_map(arg, d)
+            xi[mask] = (1.0 - (2.0 / np.pi) * w) if sign > 0 else (-1.0 + (2.0 / np.pi) * w)
+            dxi[mask] = _graded_map_prime(arg, d)
+    return xi, dxi
+
+
 @dataclass
 class MomentGroup:
     targets: np.ndarray          # (B,)
@@ -348,11 +369,17 @@ def compute_moments(disc: SurfaceDiscretization, smap: SingularityMap,
 def compute_moments_device(disc: SurfaceDiscretization, smap: SingularityMap,
                            config: SingularQuadratureConfig, kappas,
                            target_points=None, target_normals=None,
-                           groups: bool = True):
+                           groups: bool = True, exact: bool = True):
     """``compute_moments`` on the GPU (csrc/moments.cu): same table, the
-    pairs' moments computed by one CTA each.  beta_s agrees with the host
-    restatement to rounding; beta_d to the ~1e-7 conditioning of its
-    integrand at the clustered nodes (tests/test_gpu_moments.py).
+    pairs' moments computed by one CTA each.
+
+    exact=True (default): the graded nodes come from the host
+    (``clustered_nodes``, the reference's np.power expressions) and the
+    device replays the reference's float64 operation order for the patch
+    geometry (csrc/moments.cu ``dot_exact``), so beta_s and beta_d agree with
+    the reference to rounding.  exact=False: graded map on the device; beta_d
+    then carries the ~1e-7 conditioning of (x - y).n_x at the clustered nodes
+    (tests/test_gpu_moments.py).
 
     groups=False skips the per-patch regrouping: the table then carries the
     blocks in the singularity map's CSR order (``csr_blocks``, n_mom x 4 x
@@ -387,13 +414,29 @@ def compute_moments_device(disc: SurfaceDiscretization, smap: SingularityMap,
                     complex(kappas[1]).real, complex(kappas[1]).imag])
     out = np.empty((n_pairs, 4, n_c, n_c), dtype=np.complex128)
     dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-    desc = _lib.MomentDesc(n_pairs, dp(txyz), dp(tnrm),
-                           pid.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                           dp(uv), disc.n_patches, npg, dp(cf), n_c, nb,
-                           int(config.d), dp(base), dp(wb), dp(kap))
+    # OpenBLAS's N-tail columns (empirical, OpenBLAS 0.3.30 SkylakeX: the
+    # 20 x 20 patch products reduce columns 16..19 in 8 interleaved lanes)
+    tail = lambda n: n - n % 16 if (n > 16 and n % 16) else 0
     lib = _lib.load()
-    _lib.check(lib.ifgfb_singular_moments(ctypes.byref(desc), dp(out.view(np.float64))),
-               "ifgfb_singular_moments")
+    step = n_pairs if not exact else 1 << 20
+    for c0 in range(0, max(n_pairs, 1), max(step, 1)):
+        c1 = min(n_pairs, c0 + step)
+        if c1 <= c0:
+            break
+        nodes = None
+        if exact:
+            nodes = np.empty((c1 - c0, 4, nb))
+            nodes[:, 0], nodes[:, 1] = clustered_nodes_many(uv[c0:c1, 0], base, config.d)
+            nodes[:, 2], nodes[:, 3] = clustered_nodes_many(uv[c0:c1, 1], base, config.d)
+        desc = _lib.MomentDesc(c1 - c0, dp(txyz[c0:c1]), dp(tnrm[c0:c1]),
+                               pid[c0:c1].ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                               dp(uv[c0:c1]), disc.n_patches, npg, dp(cf), n_c, nb,
+                               int(config.d), dp(base), dp(wb), dp(kap),
+                               dp(nodes) if exact else None,
+                               tail(npg) if exact else 0, tail(nb) if exact else 0)
+        _lib.check(lib.ifgfb_singular_moments(ctypes.byref(desc),
+                                              dp(out[c0:c1].view(np.float64))),
+                   "ifgfb_singular_moments")
     table = SingularMomentTable(n_c, kappas)
     if not groups:
         table.csr_blocks = out.reshape(n_pairs, 4, n_c * n_c)

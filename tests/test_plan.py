@@ -246,3 +246,21 @@ def test_seam_modes_bitwise_outside_crossings():
     assert n_cross >= 5
     with pytest.raises(ValueError):
         octree.emission_plan(tree, hier, 3, disp, seam="bogus")
+
+
+def test_clustered_nodes_many_is_bitwise_per_patch_evaluation():
+    """The device-moment path's host graded nodes (one graded-map row,
+    broadcast) equal the reference's per-patch evaluation bit for bit."""
+    from _support import inputs
+    from paper_2408_02274_b200 import cheb, nearfield
+    cfg = nearfield.SingularQuadratureConfig()
+    for name in ("s1", "se1"):
+        smap = inputs(name)["smap"]
+        base = cheb.nodes(cfg.resolve_n_beta(inputs(name)["disc"].n_c))
+        for col in (0, 1):
+            many = nearfield.clustered_nodes_many(smap.closest_uv[:, col], base, cfg.d)
+            for p in np.unique(smap.patch_ids):
+                sel = np.nonzero(smap.patch_ids == p)[0]
+                one = nearfield.clustered_nodes(smap.closest_uv[sel, col], base, cfg.d)
+                np.testing.assert_array_equal(many[0][sel], one[0])
+                np.testing.assert_array_equal(many[1][sel], one[1])
