@@ -43,8 +43,9 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-FP64_PEAK_TFLOPS = 37.0   # DMMA m8n8k4 f64, measured (profiles/fp64_peak_r01.txt)
+FP64_PEAK_TFLOPS = 37.0   # DMMA m8n8k4 f64, measured (profiles/fp64_peak_r02.txt)
 W_PROP = 75 * 75 * 16 * 4          # FLOP per (parent segment, child) instance
+SEG_BYTES = 19_456                 # one segment's coefficients in HBM (80 x 16 complex, padded)
 W_COEF = 16 * (3 * 3 * 25 + 5 * 5 * 15 + 5 * 5 * 15) * 4   # K3 per segment
 W_EMIT = 2 * 75 * 16 * 4           # per (box, target) pair, x and x + h n
 W_LEAF = 128                       # per (node, source) pair (2 kernels x 8 ch)
@@ -171,14 +172,17 @@ def work_counts(tree, hier):
     window's plan: that rank's share)."""
     from paper_2408_02274_b200 import octree
     D = tree.depth
-    prop = {}
+    prop, pbytes = {}, {}
     for d in range(4, D + 1):
         ap = octree.accumulation_plan(tree, hier, d, geometry=False)
         prop[d] = W_PROP * ap.n_instances + W_COEF * hier.level(d - 1).n_segments
+        # algorithmic HBM bytes of K4: child level read once, parent written once
+        pbytes[d] = SEG_BYTES * (hier.level(d).n_segments + hier.level(d - 1).n_segments)
     cl, lvl = hier.level(D), tree.level(D)
     leaf = W_LEAF * 75 * int((cl.seg_off[1:] - cl.seg_off[:-1]) @ lvl.pt_count)
     emit = W_EMIT * sum(hier.level(d).cpt_idx.size for d in range(3, D + 1))
     return {"prop_by_level": prop, "prop": sum(prop.values()), "leaf": leaf,
+            "prop_bytes": sum(pbytes.values()),
             "leaf_coef": W_COEF * cl.n_segments, "emit": emit,
             "total": sum(prop.values()) + leaf + W_COEF * cl.n_segments + emit}
 
@@ -585,11 +589,12 @@ def run_b200(args):
                      "unit": "TFLOP/s", "frac": (achieved / FP64_PEAK_TFLOPS
                                                  if achieved else None),
                      "traffic": traffic, "traffic_source": tsrc,
+                     "traffic_algorithmic": counts["prop_bytes"] / max(1, prop_n // args.steps),
                      "flop_per_launch": counts["prop"] / max(1, prop_n // args.steps),
                      "ms_per_launch": prop_ms / max(1, prop_n),
-                     "peak_source": "FP64 mma.sync m8n8k4 measured on B200 "
-                                    "(tools/fp64_peak.cu, profiles/fp64_peak_r01.txt); "
-                                    "MEASURED_PEAKS.json has no FP64 entry",
+                     "peak_source": "FP64 mma.sync m8n8k4 measured on B200 at 1965 MHz "
+                                    "(tools/fp64_peak.cu, profiles/fp64_peak_r02.txt with "
+                                    "its clock record); MEASURED_PEAKS.json has no FP64 entry",
                      "share_of_step": prop_ms / args.steps / ms,
                      "by_level": {
                          str(d): {"ms_per_step": round(t / args.steps, 3),

@@ -394,6 +394,77 @@ __global__ void __launch_bounds__(128, IFGFB_NEAR_DIRECT_MINB) near_direct_kerne
   }
 }
 
+// K6b, thread per target: the same signed pass with one THREAD per target
+// and its 28 complex sums in registers -- no warp reductions (the warp form
+// spends ~40% of its instructions in 3 x 28 shuffle trees).  Consecutive
+// targets lie on one patch and walk overlapping, ascending source lists, so
+// the per-lane gathers of source positions and phi rows hit L1.
+#ifndef IFGFB_NEAR_THREAD_MINB
+#define IFGFB_NEAR_THREAD_MINB 3
+#endif
+__global__ void __launch_bounds__(128, IFGFB_NEAR_THREAD_MINB)
+near_direct_thread_kernel(NearArgs a) {
+  const int ell = blockIdx.x * blockDim.x + threadIdx.x + a.t_lo;
+  if (ell >= a.t_hi) return;
+  const int n = a.s.n;
+  double2 S[8][2], D[6][2];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) S[c][0] = S[c][1] = make_double2(0, 0);
+#pragma unroll
+  for (int c = 0; c < 6; ++c) D[c][0] = D[c][1] = make_double2(0, 0);
+  const double x0 = a.s.pts[3 * ell], x1 = a.s.pts[3 * ell + 1], x2 = a.s.pts[3 * ell + 2];
+  const double n0 = a.s.nrm[3 * ell], n1 = a.s.nrm[3 * ell + 1], n2v = a.s.nrm[3 * ell + 2];
+  const int e0 = a.dir_off[ell], e1 = a.dir_off[ell + 1];
+#pragma unroll 1
+  for (int e = e0; e < e1; ++e) {
+    const int code = __ldg(a.dir_src + e);
+    const bool neg = code < 0;
+    const int src = neg ? -code - 1 : code;
+    IFGFB_DCHECK(src >= 0 && src < n && src != ell);
+    const double dx = x0 - __ldg(a.s.pts + 3 * src), dy = x1 - __ldg(a.s.pts + 3 * src + 1),
+                 dz = x2 - __ldg(a.s.pts + 3 * src + 2);
+    const double r = sqrt(dx * dx + dy * dy + dz * dz);
+    const double ndx = dx * n0 + dy * n1 + dz * n2v;
+    double2 gk[2], qk[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) kernel_pair(a.kr[k], a.ki[k], r, ndx, gk[k], qk[k]);
+    const double jw = neg ? -__ldg(a.s.wq + src) : 1.0;      // corrections subtract
+    const double2* wrow = a.phi_pm + (size_t)src * 16 + (neg ? 0 : 8);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      gk[k] = cscale(jw, gk[k]);
+      qk[k] = cscale(jw, qk[k]);
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double2 w = __ldg(wrow + c);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        S[c][k] = cadd(S[c][k], cmul(gk[k], w));
+        if (c < 6) D[c][k] = cadd(D[c][k], cmul(qk[k], w));
+      }
+    }
+  }
+  const double scl = 1.0 / a.fd_step;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int lane = c * 2 + k;
+      const size_t o = (size_t)lane * n + ell;
+      const size_t of = a.far_pm ? (size_t)(ell - a.t_lo) * 32 + lane : o;
+      const double2 s_if = a.far[of];
+      a.s_val[o] = cadd(a.s_val[o], cadd(s_if, S[c][k]));
+      if (c < 6) {
+        const double2 sd = a.far_pm ? a.far[of + 16] : a.far_disp[o];
+        // numpy's complex / real: multiply by the reciprocal (Smith, rat = 0)
+        const double2 d_if = make_double2(mul_rn(sd.x - s_if.x, scl),
+                                          mul_rn(sd.y - s_if.y, scl));
+        a.d_val[o] = cadd(a.d_val[o], cadd(d_if, D[c][k]));
+      }
+    }
+}
+
 // ---------------------------------------------------------------- K7 ----
 struct AsmArgs {
   SurfPtrs s;
@@ -567,15 +638,20 @@ static int near_launch(Plan& p, cudaStream_t st) {
   // fused single kernel (default); IFGFB_NEAR=split: moments kernel + direct
   // kernel (measured slower: 1.26 vs 1.12 ms at sphere(8,10), 5.63 vs 4.12 ms
   // on the r=2 slab; DESIGN 4)
-  static const bool fused = [] {
+  // IFGFB_NEAR=thread: moments kernel + thread-per-target direct kernel
+  static const int mode = [] {
     const char* v = std::getenv("IFGFB_NEAR");
-    return !(v && v[0] == 's');
+    return (v && v[0] == 's') ? 1 : (v && v[0] == 't') ? 2 : 0;
   }();
   const int grid = (nt + warps_per_block - 1) / warps_per_block;
   const int tk = p.timer.begin(K_NEAR, st);
-  if (fused) {
+  if (mode == 0) {
     near_kernel<<<grid, 32 * warps_per_block, 0, st>>>(na);
     p.launches += 1;
+  } else if (mode == 2) {
+    near_moments_kernel<<<grid, 32 * warps_per_block, 0, st>>>(na);
+    near_direct_thread_kernel<<<(nt + 127) / 128, 128, 0, st>>>(na);
+    p.launches += 2;
   } else {
     near_moments_kernel<<<grid, 32 * warps_per_block, 0, st>>>(na);
     near_direct_kernel<<<grid, 32 * warps_per_block, 0, st>>>(na);
