@@ -195,6 +195,20 @@ int ifgfb_row_tiles_plan(int64_t n_rows, const int64_t* inst_off,
                          const uint8_t* group_id, uint8_t* row_order,
                          uint8_t* row_cuts, int64_t* tile_off,
                          int32_t cut_radius, int32_t n_threads);
+/* Wide-warp propagation kernel (IFGFB_K4=wide): the same signature order,
+ * cut into n_warps (= ifgfb_wide_warps()) contiguous sets of <= 32 nodes,
+ * cut k within +-cut_radius (<= 8) of 75k/n_warps, minimising
+ * balance_weight * n_warps * (largest per-warp tile count) + total_weight *
+ * (the row's tile count).  row_cuts keeps the 6-byte record per row:
+ * entries 0..n_warps are the cuts, the rest 75. */
+int ifgfb_row_cuts_wide(int64_t n_rows, const int64_t* inst_off,
+                        const int64_t* inst_type, int64_t n_types,
+                        const uint8_t* group_id, uint8_t* row_order,
+                        uint8_t* row_cuts, int32_t n_warps, int32_t cut_radius,
+                        int32_t total_weight, int32_t balance_weight,
+                        int32_t n_threads);
+/* owner warps per parent row the wide propagation kernel was built with */
+int ifgfb_wide_warps(void);
 int ifgfb_row_tiles_fill(int64_t n_rows, const int64_t* inst_off,
                          const int64_t* inst_type, int64_t n_types,
                          const uint8_t* group_id, const uint8_t* row_order,

@@ -193,6 +193,9 @@ EXPORTS = {
     "ifgfb_rank_unpack": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ifgfb_row_tiles_plan": ([C.c_int64, _ip, _ip, C.c_int64, _u8p, _u8p, _u8p,
                               _ip, C.c_int32, C.c_int32], C.c_int),
+    "ifgfb_row_cuts_wide": ([C.c_int64, _ip, _ip, C.c_int64, _u8p, _u8p, _u8p,
+                             C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32], C.c_int),
+    "ifgfb_wide_warps": ([], C.c_int),
     "ifgfb_row_tiles_fill": ([C.c_int64, _ip, _ip, C.c_int64, _u8p, _u8p, _u8p,
                               _ip, _u8p, C.c_int32], C.c_int),
     "ifgfb_layer_fields": ([C.c_int64, _dp, C.c_int64, _dp, _dp, _dp, _dp],

@@ -207,6 +207,7 @@ struct Level {
   int* tile_off = nullptr;     // n_instances*WARP_PARTS+1
   unsigned char* row_order = nullptr;  // parent rows x NN
   unsigned char* row_cuts = nullptr;   // parent rows x (WARP_PARTS+1)
+  int cut_warps = 0, cut_max_set = 0;  // sets per row / largest set of row_cuts
   int max_groups = 0;                  // most child segments of one instance
   bool otf = false;                    // node geometry computed on the device
   unsigned char* type_octant = nullptr;  // per type (otf levels)

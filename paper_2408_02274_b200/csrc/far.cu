@@ -158,6 +158,36 @@ __device__ __forceinline__ void store_segment(double* dst, const double2* V,
   }
 }
 
+// The same store for CTAs of exactly 128 threads: element idx = 128 ks + tid,
+// so a thread's fragment lane and column tile are fixed and the k-step loop
+// unrolls into one shared load and one coalesced store per k-step (the
+// generic loop spends ~37 instructions per element on index arithmetic).
+template <bool OWNER, int RS = NCOL>
+__device__ __forceinline__ void store_segment128(double* dst, const double2* V,
+                                                 const unsigned char* inv, int tid) {
+  const int lane = (tid >> 1) & 31, nt = ((tid >> 5) & 2) | (tid & 1);
+  const int tig = lane & 3, col = 8 * nt + (lane >> 2);
+  const double* Vd = reinterpret_cast<const double*>(V) + (col >> 1) * 2 + (col & 1);
+#pragma unroll
+  for (int ks = 0; ks < KSTEPS; ++ks) {
+    int ab, c;
+    if (ks < KMAIN) {
+      ab = 4 * (ks / PA) + tig;
+      c = ks % PA;
+    } else {
+      const int st = ks - KMAIN;
+      ab = tig < 3 ? 12 + tig : (st < 3 ? 12 + st : PS * PA);   // (s=3, tig=3): zero row
+      c = tig < 3 ? st : PA - 1;
+    }
+    double v = 0.0;
+    if (ab < PS * PA) {
+      const int node = ab * PA + c;
+      v = Vd[(OWNER ? (int)inv[node] : node) * (RS * 2)];
+    }
+    dst[ks * 128 + tid] = v;
+  }
+}
+
 // ------------------------------------------------------------ weights ----
 // wt[t][c] = w[c][perm[t]] (tree order, CH channel slots, zero padded)
 __global__ void pack_weights(const double2* __restrict__ w, int nch, int n,
@@ -708,6 +738,291 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
                       32 * WARP_PARTS);
   __syncthreads();
   }
+}
+
+// ------------------------------------------------- K4, wide warps ----
+// The same owner-computes propagation with FEWER, WIDER owner warps
+// (IFGFB_K4=wide): WW warps per parent row, each owning NN/WW (25 for WW = 3)
+// consecutive positions of the row's signature order.  A parent row's 75
+// nodes fall into only 2-3 child segments per child (tools/group_analysis.py),
+// so a warp's nodes of one sigma group fill up to 4 MMA row tiles; the warp
+// runs them TOGETHER: one pair of 512-byte B-fragment loads per k-step feeds
+// 4 x NT DMMAs (NT = 1..4 row tiles), instead of every 8-row tile pulling
+// its own copy of the 19 KB child block through L1 (the 5-warp kernel moves
+// ~4.5 KB of L2 -> SM traffic per DMMA k-step and sits at 72% of the L2
+// bandwidth; this one ~1/NT of it).  The Chebyshev values of a node
+// (T_0..2(xs), T_0..4(xt), T_0..4(xp)) are computed once per (instance,
+// node) into shared memory by the node's owner lane; a tile's A values are
+// two shared loads and two multiplies per k-step (the 5-warp kernel
+// recomputes the recurrences in all 4 lanes of a row, per tile).  Tiles are
+// formed in the kernel from the nodes' sigma groups (tile-free plans).  The
+// per-node arithmetic (basis products, k order, accumulation order over the
+// row's instances) is the 5-warp kernel's, so results are bitwise equal.
+#ifndef IFGFB_WIDE_WARPS
+#define IFGFB_WIDE_WARPS 4
+#endif
+#ifndef IFGFB_WIDE_MINB
+#define IFGFB_WIDE_MINB 4
+#endif
+#ifndef IFGFB_WIDE_MAXNT   // row tiles of one sigma group run together (1..4)
+#define IFGFB_WIDE_MAXNT 4
+#endif
+constexpr int WW = IFGFB_WIDE_WARPS;
+constexpr int WIDE_MAXNT = IFGFB_WIDE_MAXNT;
+static_assert(WIDE_MAXNT >= 1 && WIDE_MAXNT <= 4, "1..4 row tiles per pass");
+constexpr int NT_STRIDE = PS + 2 * PA;   // 13 doubles per node
+static_assert((NN + WW - 1) / WW <= 32, "a wide warp owns at most 32 nodes");
+
+struct __align__(16) WideStage {
+  double2 ratio[NN * 2];        // [position][kappa]
+  double geom[NN * 3];          // [position][xs, xt, xp]
+  int crow[WW][MAX_GROUPS];     // per-warp copy of the instance's child rows
+};
+
+// A operand of k-step KS for the node whose Chebyshev values are T (see
+// BasisA): main block ks = 5q + c -> (T_a(xs) T_b(xt)) T_c(xp) with ab = 4q +
+// tig; tail ks = 15 + s -> (ab, c) = (12 + tig, s) for tig < 3, (12 + s, 4) for
+// tig = 3 (s = 3: the zero row).  tst caches T_a T_b of the current q.
+#ifndef IFGFB_WIDE_PIN   // pin the A-value multiplies between the DMMA groups
+#define IFGFB_WIDE_PIN 1
+#endif
+__device__ __forceinline__ double wide_mul(double a, double b) {
+#if IFGFB_WIDE_PIN
+  double r;
+  asm volatile("mul.rn.f64 %0, %1, %2;\n" : "=d"(r) : "d"(a), "d"(b));
+  return r;
+#else
+  return a * b;
+#endif
+}
+
+template <int KS>
+__device__ __forceinline__ double wide_tst(const double* T, int tig) {
+  if (KS < KMAIN) {
+    const int ab = 4 * (KS / PA) + tig;
+    const int ia = ab / PA, ib = ab - PA * ia;
+    return wide_mul(T[ia], T[PS + ib]);
+  }
+  const int s = KS - KMAIN;
+  return wide_mul(T[2], T[PS + 2 + (tig < 3 ? tig : (s < 3 ? s : 0))]);
+}
+
+template <int KS>
+__device__ __forceinline__ double wide_av(const double* T, double tst, int tig) {
+  if (KS < KMAIN) return wide_mul(tst, T[PS + PA + KS % PA]);
+  const int s = KS - KMAIN;
+  const double av = wide_mul(tst, T[PS + PA + (tig < 3 ? s : PA - 1)]);
+  return (s == 3 && tig == 3) ? 0.0 : av;
+}
+
+// one k-step of NT row tiles: the 4 x NT DMMAs of k-step KS, each tile's A
+// value for k-step KS + 1 computed right behind its DMMAs (its latency hides
+// under the next tile's), the B fragments of KS + 1 loaded ahead
+template <int NT, int KS>
+__device__ __forceinline__ void wide_kstep(const double2* F, const double* const (&T)[NT],
+                                           double (&tst)[NT], double (&av)[NT],
+                                           double2& b01, double2& b23,
+                                           double (&c0)[NT][4], double (&c1)[NT][4], int tig) {
+  if (IFGFB_ACC_PF > 0 && KS + IFGFB_ACC_PF < KSTEPS) {
+    prefetch_l1(F + (KS + IFGFB_ACC_PF) * 64);
+    prefetch_l1(F + (KS + IFGFB_ACC_PF) * 64 + 32);
+  }
+  double2 n01 = b01, n23 = b23;
+  if (KS + 1 < KSTEPS) {
+    n01 = F[(KS + 1) * 64];
+    n23 = F[(KS + 1) * 64 + 32];
+  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    dmma(c0[i][0], c1[i][0], av[i], b01.x);
+    dmma(c0[i][1], c1[i][1], av[i], b01.y);
+    dmma(c0[i][2], c1[i][2], av[i], b23.x);
+    dmma(c0[i][3], c1[i][3], av[i], b23.y);
+    if (KS + 1 < KSTEPS) {
+      if ((KS + 1) % PA == 0 || KS + 1 >= KMAIN) tst[i] = wide_tst<KS + 1>(T[i], tig);
+      av[i] = wide_av<KS + 1>(T[i], tst[i], tig);
+    }
+  }
+  b01 = n01;
+  b23 = n23;
+  if constexpr (KS + 1 < KSTEPS)
+    wide_kstep<NT, KS + 1>(F, T, tst, av, b01, b23, c0, c1, tig);
+}
+
+// NT row tiles of one sigma group against the group's child block: 19
+// k-steps, per k-step one B fragment pair and 4 x NT DMMAs
+template <int NT, int NK>
+__device__ __forceinline__ void wide_pass(const double* __restrict__ C, const double* T0,
+                                          const int (&slot)[4], int nrows,
+                                          const double2* ratio, double2* mine,
+                                          int lane) {
+  const int grp = lane >> 2, tig = lane & 3;
+  const double2* F = reinterpret_cast<const double2*>(C) + lane;
+  double2 b01 = F[0], b23 = F[32];
+  double c0[NT][4], c1[NT][4], tst[NT], av[NT];
+  const double* T[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    T[i] = T0 + slot[i] * NT_STRIDE;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) c0[i][nt] = c1[i][nt] = 0.0;
+    tst[i] = wide_tst<0>(T[i], tig);
+    av[i] = wide_av<0>(T[i], tst[i], tig);
+  }
+#ifndef IFGFB_DIAG_NODMMA
+  wide_kstep<NT, 0>(F, T, tst, av, b01, b23, c0, c1, tig);
+#else
+#pragma unroll
+  for (int i = 0; i < NT; ++i) c0[i][0] = av[i] + b01.x + b23.y;
+#endif
+#ifndef IFGFB_DIAG_NOACC
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    if (8 * i + grp < nrows) {
+      const double2 r0 = ratio[slot[i] * NK];
+      const double2 r1 = NK > 1 ? ratio[slot[i] * NK + NK - 1] : r0;
+      double2* dst = mine + slot[i] * NCOL;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int m = 4 * nt + tig;
+        const double2 v = cmul(make_double2(c0[i][nt], c1[i][nt]),
+                               (NK > 1 && (tig & 1)) ? r1 : r0);
+        dst[m].x += v.x;
+        dst[m].y += v.y;
+      }
+    }
+  }
+#else
+  if (c0[0][0] == 1.2345e300) mine[0].x = c1[NT - 1][3];
+#endif
+}
+
+template <int NK, bool WIDE, bool OTF>
+__global__ void __launch_bounds__(32 * WW, IFGFB_WIDE_MINB) accum_wide_kernel(AccArgs a) {
+  __shared__ double2 acc[NN * NCOL];                        // 19.2 KB
+  __shared__ WideStage stage[2];                            // 9.2 KB
+  __shared__ double nodeT[NN * NT_STRIDE];                  // 7.8 KB
+  __shared__ unsigned char ord[NN], inv[NN];
+  __shared__ unsigned char rank2slot[WW][32];
+  __shared__ unsigned char sgid[8][NN];                     // [instance][position]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 2;
+  const int p = a.row0 + blockIdx.x;
+  if (p >= a.row_end) return;
+  // warp w owns positions cuts[w] .. cuts[w+1]-1 of the signature order
+  // (ifgfb_row_cuts_wide: <= 32 nodes, first WW + 1 entries of the 6-byte record)
+  const int pos0 = a.row_cuts[(size_t)p * (WARP_PARTS + 1) + warp];
+  const int nset = a.row_cuts[(size_t)p * (WARP_PARTS + 1) + warp + 1] - pos0;
+  IFGFB_DCHECK(nset >= 1 && nset <= 32 && pos0 + nset <= NN);
+  double2* mine = acc + pos0 * NCOL;
+  const unsigned char* word = ord + pos0;
+  if (lane < nset) ord[pos0 + lane] = a.row_order[(size_t)p * NN + pos0 + lane];
+  for (int i = lane; i < nset * NCOL; i += 32) mine[i] = make_double2(0.0, 0.0);
+  // the row's instance scalars, lane j <-> instance i0 + j (<= 8 per row)
+  const int i0 = a.inst_off[p], ni = a.inst_off[p + 1] - i0;
+  int my_t = 0, my_co = 0;
+  if (lane < ni) my_t = a.inst_type[i0 + lane];
+  if (lane <= ni) my_co = a.inst_crow_off[i0 + lane];
+  __syncwarp();
+  // sigma group of every owned slot under every instance of the row: the
+  // (<= 8) loads of a lane are independent and complete under the first
+  // instance's staging; each warp reads only what it wrote
+  for (int j = 0; j < ni; ++j) {
+    const int t = __shfl_sync(0xffffffffu, my_t, j);
+    if (lane < nset) sgid[j][pos0 + lane] = __ldg(a.gid + (size_t)t * NN + word[lane]);
+  }
+  auto stage_inst = [&](int j, WideStage& S) {
+    const int t = __shfl_sync(0xffffffffu, my_t, j);
+    const int cs = __shfl_sync(0xffffffffu, my_co, j);
+    const int ce = __shfl_sync(0xffffffffu, my_co, j + 1);
+    const size_t tb = (size_t)t * NN;
+    if (!OTF && lane < nset) {   // one lane per owned node
+      const size_t nd = tb + word[lane];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) cp_async8(&S.geom[3 * (pos0 + lane) + k], a.node_geom + nd * 3 + k);
+#pragma unroll
+      for (int k = 0; k < NK; ++k) cp_async16(&S.ratio[NK * (pos0 + lane) + k], a.ratio + nd * NK + k);
+    }
+    if (lane < min(ce - cs, MAX_GROUPS)) cp_async4(&S.crow[warp][lane], a.crow + cs + lane);
+    cp_async_commit();
+  };
+  if (ni > 0) stage_inst(0, stage[0]);
+  __syncwarp();
+  for (int j = 0; j < ni; ++j) {
+    WideStage& S = stage[j & 1];
+    const unsigned g_cur = lane < nset ? (unsigned)sgid[j][pos0 + lane] : 0xFFFFFFFFu;
+    if (j + 1 < ni) {
+      stage_inst(j + 1, stage[(j + 1) & 1]);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    const int* crow_g = a.crow + __shfl_sync(0xffffffffu, my_co, j);
+    if (OTF) {   // each lane: geometry of its own slot
+      const int pseg = a.o.parent_seg_id[p];
+      const int oct = a.o.type_octant[__shfl_sync(0xffffffffu, my_t, j)];
+      if (lane < nset) {
+        const int g = (int)g_cur;
+        const int cr = (!WIDE || g < MAX_GROUPS) ? S.crow[warp][g] : crow_g[g];
+        otf_node<NK>(a.o, pseg, oct, word[lane], a.o.child_seg_id[cr],
+                     &S.geom[(pos0 + lane) * 3], &S.ratio[(pos0 + lane) * NK]);
+      }
+    }
+    if (lane < nset) {   // Chebyshev values of the lane's node (make_basis<false>)
+      const double* ng = S.geom + (pos0 + lane) * 3;
+      const double xs = ng[0], xt = ng[1], xp = ng[2];
+      double* T = nodeT + (pos0 + lane) * NT_STRIDE;
+      double tt[PA], tp[PA];
+      tt[0] = 1.0; tt[1] = xt;
+      tp[0] = 1.0; tp[1] = xp;
+#pragma unroll
+      for (int i = 2; i < PA; ++i) {
+        tt[i] = 2.0 * xt * tt[i - 1] - tt[i - 2];
+        tp[i] = 2.0 * xp * tp[i - 1] - tp[i - 2];
+      }
+      T[0] = 1.0; T[1] = xs; T[2] = 2.0 * xs * xs - 1.0;
+#pragma unroll
+      for (int i = 0; i < PA; ++i) { T[PS + i] = tt[i]; T[PS + PA + i] = tp[i]; }
+    }
+    __syncwarp();
+    unsigned g_at = __reduce_min_sync(0xffffffffu, g_cur);
+    while (g_at != 0xFFFFFFFFu) {
+      const unsigned mask = __ballot_sync(0xffffffffu, g_cur == g_at);
+      const int nrows = __popc(mask);
+      if (g_cur == g_at) rank2slot[warp][__popc(mask & ((1u << lane) - 1u))] = (unsigned char)lane;
+      __syncwarp();
+      const int g = (int)g_at;
+      const int crow_used = (!WIDE || g < MAX_GROUPS) ? S.crow[warp][g] : crow_g[g];
+      IFGFB_DCHECK(crow_used >= a.child_lo && crow_used < a.child_hi && nrows <= nset);
+      const double* C = a.coef_child + (size_t)crow_used * SEG_DOUBLES;
+      const double* T0 = nodeT + pos0 * NT_STRIDE;
+      const double2* rt = S.ratio + pos0 * NK;
+      for (int r0 = 0; r0 < nrows; r0 += 8 * WIDE_MAXNT) {   // one pass unless MAXNT < 4
+        const int nr = min(nrows - r0, 8 * WIDE_MAXNT);
+        int slot[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          slot[i] = rank2slot[warp][r0 + (8 * i + grp < nr ? 8 * i + grp : 0)];
+        if (nr <= 8) wide_pass<1, NK>(C, T0, slot, nr, rt, mine, lane);
+        else if (WIDE_MAXNT < 3 || nr <= 16) wide_pass<2, NK>(C, T0, slot, nr, rt, mine, lane);
+        else if (WIDE_MAXNT < 4 || nr <= 24) wide_pass<3, NK>(C, T0, slot, nr, rt, mine, lane);
+        else wide_pass<4, NK>(C, T0, slot, nr, rt, mine, lane);
+      }
+      __syncwarp();
+      g_at = __reduce_min_sync(0xffffffffu, g_cur > g_at ? g_cur : 0xFFFFFFFFu);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < NN) inv[ord[threadIdx.x]] = (unsigned char)threadIdx.x;
+  __syncthreads();
+#ifndef IFGFB_DIAG_NOK3      // diagnostic builds only (tools/ab_wide.sh): timing without a phase
+  to_coeffs_smem<true>(acc, inv, threadIdx.x, 32 * WW);
+#endif
+#ifndef IFGFB_DIAG_NOSTORE
+  if (WW == 4) store_segment128<true>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, inv, threadIdx.x);
+  else store_segment<true>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, inv, threadIdx.x, 32 * WW);
+#endif
 }
 
 // ------------------------------------------------- K4, ring-staged ----
@@ -1323,7 +1638,22 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
             aa.gid = L.gid;
             const bool tf = L.tiles == nullptr;   // tile-free plan
             const dim3 blk(32 * WARP_PARTS);
-            if (use_ring()) {
+            if (tf && WW != WARP_PARTS && L.cut_warps == WW) {
+              // the level's rows were cut for the wide-warp kernel
+              // (ifgfb_row_cuts_wide; the plan builder decides per level)
+              const dim3 wblk(32 * WW);
+              if (L.otf) {
+                if (wide) accum_wide_kernel<NK, true, true><<<nrows, wblk, 0, st>>>(aa);
+                else accum_wide_kernel<NK, false, true><<<nrows, wblk, 0, st>>>(aa);
+              } else {
+                if (wide) accum_wide_kernel<NK, true, false><<<nrows, wblk, 0, st>>>(aa);
+                else accum_wide_kernel<NK, false, false><<<nrows, wblk, 0, st>>>(aa);
+              }
+            } else if (L.cut_warps != WARP_PARTS || L.cut_max_set > MAX_SET) {
+              set_error("the 5-warp propagation kernels need 5 row sets of <= 23 nodes "
+                        "(this plan was cut for IFGFB_K4=wide)");
+              return IFGFB_ERR_STATE;
+            } else if (use_ring()) {
               if (L.otf) IFGFB_RC(tf ? (launch_ring<NK, true, true>(aa, nrows, st))
                                      : (launch_ring<NK, true, false>(aa, nrows, st)));
               else IFGFB_RC(tf ? (launch_ring<NK, false, true>(aa, nrows, st))
@@ -1386,3 +1716,5 @@ int far_apply(Plan& p, const double* w, int nch, const double* kappas, int nk,
 }
 
 }  // namespace ifgfb
+
+extern "C" int ifgfb_wide_warps(void) { return ifgfb::WW; }

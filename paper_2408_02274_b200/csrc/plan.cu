@@ -246,11 +246,25 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
     CHECK_ARG(a->row_order[i] < NN, "row_order entry out of range");
   RC(dev_upload(p, &L.row_order, a->row_order, (size_t)a->n_parent_rows * NN));
   CHECK_ARG(a->row_cuts != nullptr, "row_cuts missing");
+  // 5-warp kernels: 5 sets of 1..23 nodes; wide-warp kernel
+  // (ifgfb_row_cuts_wide): W <= 5 sets of 1..32 nodes, then 75s
+  L.cut_warps = 0;
+  L.cut_max_set = 0;
   for (int64_t r = 0; r < a->n_parent_rows; ++r) {
     const uint8_t* c = a->row_cuts + r * (WARP_PARTS + 1);
     CHECK_ARG(c[0] == 0 && c[WARP_PARTS] == NN, "row_cuts must start at 0 and end at 75");
-    for (int w = 0; w < WARP_PARTS; ++w)
-      CHECK_ARG(c[w + 1] > c[w] && c[w + 1] - c[w] <= MAX_SET, "row_cuts: warp set size out of 1..23");
+    int used = 0;
+    for (int w = 0; w < WARP_PARTS; ++w) {
+      if (c[w] == NN) {
+        CHECK_ARG(c[w + 1] == NN, "row_cuts: entries after 75 must be 75");
+        continue;
+      }
+      CHECK_ARG(c[w + 1] > c[w] && c[w + 1] - c[w] <= 32, "row_cuts: warp set size out of 1..32");
+      L.cut_max_set = std::max(L.cut_max_set, (int)(c[w + 1] - c[w]));
+      ++used;
+    }
+    CHECK_ARG(L.cut_warps == 0 || used == L.cut_warps, "row_cuts: rows differ in their number of sets");
+    L.cut_warps = used;
   }
   RC(dev_upload(p, &L.row_cuts, a->row_cuts, (size_t)a->n_parent_rows * (WARP_PARTS + 1)));
   L.otf = a->geometry_on_device != 0;

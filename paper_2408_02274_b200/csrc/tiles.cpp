@@ -42,7 +42,78 @@ struct RowIn {
 };
 
 // order + cuts of row r; returns false on malformed input
-bool row_partition(const RowIn& in, int64_t r, int R, uint8_t* order, uint8_t* cuts) {
+// Wide-warp cuts (IFGFB_K4=wide): W contiguous sets of the signature order,
+// cut k within +-R of the even position 75k/W, every set 1..32 nodes (one
+// lane per node).  The wide kernel runs up to 4 row tiles of one sigma group
+// together, so what a split costs is executed DMMA work: the DP minimises
+// balance_w * W * (largest per-warp tile count) + total_w * (the row's tile
+// count) (weights 1/0: the 5-warp rule; 0/1: fewest tiles), ties by the
+// other term, then by the earliest cuts.
+bool wide_cuts(int ni, const uint8_t (*gs)[NN], int W, int R, int total_w, int balance_w,
+               uint8_t* cuts) {
+  constexpr int MAXW = 5, MAXR = 8, NO = 2 * MAXR + 1, WIDE_SET = 32;
+  if (W < 1 || W > MAXW || R < 0 || R > MAXR) return false;
+  auto sweep = [&](int a, int bmax, int* tiles_upto) {
+    uint8_t cnt[MAX_INST][MAX_GROUPS];
+    std::memset(cnt, 0, sizeof(cnt));
+    int tot = 0;
+    tiles_upto[0] = 0;
+    for (int b = a; b < bmax; ++b) {
+      for (int i = 0; i < ni; ++i)
+        if (cnt[i][gs[i][b]]++ % 8 == 0) ++tot;
+      tiles_upto[b + 1 - a] = tot;
+    }
+  };
+  int pos[MAXW + 1][NO], npos[MAXW + 1];
+  int bmax_[MAXW + 1][NO], btot_[MAXW + 1][NO], from[MAXW + 1][NO];
+  npos[0] = 1; pos[0][0] = 0; bmax_[0][0] = 0; btot_[0][0] = 0;
+  for (int k = 1; k <= W; ++k) {
+    npos[k] = 0;
+    if (k < W) {
+      const int even = (NN * k) / W;
+      for (int o = -R; o <= R; ++o) {
+        const int c = even + o;
+        if (c >= k && c <= NN - (W - k)) pos[k][npos[k]++] = c;
+      }
+    } else {
+      pos[k][npos[k]++] = NN;
+    }
+    for (int c = 0; c < npos[k]; ++c) { bmax_[k][c] = INT32_MAX; btot_[k][c] = INT32_MAX; from[k][c] = -1; }
+    for (int pidx = 0; pidx < npos[k - 1]; ++pidx) {
+      if (bmax_[k - 1][pidx] == INT32_MAX) continue;
+      const int a = pos[k - 1][pidx];
+      const int bmax = std::min(pos[k][npos[k] - 1], a + WIDE_SET);
+      if (bmax <= a) continue;
+      int upto[WIDE_SET + 1];
+      sweep(a, bmax, upto);
+      for (int c = 0; c < npos[k]; ++c) {
+        const int b = pos[k][c];
+        if (b - a < 1 || b - a > WIDE_SET) continue;
+        const int t = upto[b - a];
+        const int m = std::max(bmax_[k - 1][pidx], t), tt = btot_[k - 1][pidx] + t;
+        const int64_t score = (int64_t)balance_w * W * m + (int64_t)total_w * tt;
+        const int64_t best = bmax_[k][c] == INT32_MAX ? INT64_MAX
+            : (int64_t)balance_w * W * bmax_[k][c] + (int64_t)total_w * btot_[k][c];
+        const bool better = score < best ||
+            (score == best && (m < bmax_[k][c] || (m == bmax_[k][c] && tt < btot_[k][c])));
+        if (better) { bmax_[k][c] = m; btot_[k][c] = tt; from[k][c] = pidx; }
+      }
+    }
+  }
+  if (from[W][0] < 0) return false;
+  cuts[0] = 0;
+  cuts[W] = NN;
+  int c = 0;
+  for (int k = W; k >= 2; --k) {
+    c = from[k][c];
+    cuts[k - 1] = (uint8_t)pos[k - 1][c];
+  }
+  for (int k = W + 1; k <= WP; ++k) cuts[k] = NN;   // unused entries of the 6-byte record
+  return true;
+}
+
+bool row_partition(const RowIn& in, int64_t r, int R, uint8_t* order, uint8_t* cuts,
+                   int wide_w = 0, int total_w = 0, int balance_w = 1) {
   const int64_t i0 = in.inst_off[r], ni = in.inst_off[r + 1] - i0;
   if (ni < 0 || ni > MAX_INST) return false;
   int64_t key[NN];
@@ -64,6 +135,7 @@ bool row_partition(const RowIn& in, int64_t r, int R, uint8_t* order, uint8_t* c
     const uint8_t* g = in.group_id + in.inst_type[i0 + i] * NN;
     for (int n = 0; n < NN; ++n) gs[i][n] = g[idx[n]];
   }
+  if (wide_w > 0) return wide_cuts((int)ni, gs, wide_w, R, total_w, balance_w, cuts);
   // tiles of [a, b) summed over instances, for b swept upward from a
   auto sweep = [&](int a, int bmax, int* tiles_upto /* index b - a */) {
     uint8_t cnt[MAX_INST][MAX_GROUPS];
@@ -226,6 +298,42 @@ int ifgfb_row_tiles_plan(int64_t n_rows, const int64_t* inst_off, const int64_t*
   if (!tile_off) return IFGFB_OK;
   tile_off[0] = 0;
   for (int64_t k = 1; k <= ni * WP; ++k) tile_off[k] += tile_off[k - 1];
+  return IFGFB_OK;
+}
+
+int ifgfb_row_cuts_wide(int64_t n_rows, const int64_t* inst_off, const int64_t* inst_type,
+                        int64_t n_types, const uint8_t* group_id, uint8_t* row_order,
+                        uint8_t* row_cuts, int32_t n_warps, int32_t cut_radius,
+                        int32_t total_weight, int32_t balance_weight, int32_t n_threads) {
+  if (n_rows < 0 || !inst_off || (n_rows && (!row_order || !row_cuts)) || n_warps < 1 ||
+      n_warps > WP || (NN + n_warps - 1) / n_warps > 32 || cut_radius < 0 || cut_radius > 8 ||
+      total_weight < 0 || balance_weight < 0 || total_weight + balance_weight == 0) {
+    ifgfb::set_error("ifgfb_row_cuts_wide: bad arguments");
+    return IFGFB_ERR_ARG;
+  }
+  if (!check_groups(group_id, n_types)) {
+    ifgfb::set_error("ifgfb_row_cuts_wide: sigma group id >= 75");
+    return IFGFB_ERR_ARG;
+  }
+  const int64_t ni = inst_off[n_rows] - inst_off[0];
+  for (int64_t i = 0; i < ni; ++i)
+    if (inst_type[inst_off[0] + i] < 0 || inst_type[inst_off[0] + i] >= n_types) {
+      ifgfb::set_error("ifgfb_row_cuts_wide: inst_type out of range");
+      return IFGFB_ERR_ARG;
+    }
+  RowIn in{inst_off, inst_type, group_id};
+  std::atomic<bool> bad{false};
+  parallel_rows(n_rows, n_threads, [&](int64_t r0, int64_t r1) {
+    for (int64_t r = r0; r < r1; ++r)
+      if (!row_partition(in, r, cut_radius, row_order + r * NN, row_cuts + r * (WP + 1),
+                         n_warps, total_weight, balance_weight))
+        bad = true;
+  });
+  if (bad) {
+    ifgfb::set_error("ifgfb_row_cuts_wide: more than 8 instances in a parent row, or no "
+                     "feasible cuts");
+    return IFGFB_ERR_ARG;
+  }
   return IFGFB_OK;
 }
 

@@ -24,7 +24,7 @@ def device_stream():
     return torch.cuda.current_stream().cuda_stream
 
 
-K4_MODES = ("auto", "l1", "l1free", "ring", "ringfree")
+K4_MODES = ("auto", "l1", "l1free", "ring", "ringfree", "wide")
 
 
 def k4_mode() -> str:
@@ -176,7 +176,7 @@ class FarFieldPlan:
         policy = policy or os.environ.get("IFGFB_GEOM_ON_DEVICE", "auto")
         levels = list(range(4, self.depth + 1))
         mode = k4_mode()
-        self.tile_free = mode.endswith("free")
+        self.tile_free = mode.endswith("free") or mode == "wide"
         if policy not in ("none", "all", "auto"):
             raise ValueError(f"geometry_on_device: unknown policy {policy!r}")
         info = {}
@@ -227,7 +227,12 @@ class FarFieldPlan:
         # picks them (ifgf.py:743-746), including any inexact hit.
         tile_free = self.tile_free
         if tile_free:
-            row_order, row_cuts = row_order_cuts(ap)
+            # wide-warp kernel on levels with node tables; on-device geometry
+            # (FP64 work per node and instance) is hidden better by the 5-warp
+            # kernel's 30 resident warps (IFGFB_WIDE_OTF=1 forces wide there too)
+            import os
+            wide = k4_mode() == "wide" and (not otf or os.environ.get("IFGFB_WIDE_OTF") == "1")
+            row_order, row_cuts = row_order_cuts(ap, wide=wide)
             tile_off = tiles = None
         else:
             row_order, row_cuts, tile_off, tiles = row_tiles(ap)

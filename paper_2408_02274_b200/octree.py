@@ -1022,10 +1022,15 @@ def _warp_set_tiles(gid, t, orow, w, per):
     return tid, tid[:, -1] + 1, gs, order, pos
 
 
-def row_order_cuts(ap: AccumulationPlan, cut_radius: int = 4, n_threads: int = 0):
+def row_order_cuts(ap: AccumulationPlan, cut_radius: int = 4, n_threads: int = 0,
+                   wide: bool = False):
     """The first half of ``row_tiles``: per parent row the signature order
     and the warp cuts, without tile records (tile-free device plans form
-    the tiles in the kernel from the nodes' sigma groups)."""
+    the tiles in the kernel from the nodes' sigma groups).  ``wide``: cuts
+    for the wide-warp kernel (``ifgfb_row_cuts_wide``: ifgfb_wide_warps()
+    sets of <= 32 nodes; env IFGFB_WIDE_CUT = radius, IFGFB_WIDE_TW /
+    IFGFB_WIDE_BW = weights of the row's tile count / the largest per-warp
+    count)."""
     from . import _lib
     lib = _lib.load()
     nn = 75
@@ -1035,6 +1040,14 @@ def row_order_cuts(ap: AccumulationPlan, cut_radius: int = 4, n_threads: int = 0
     it = np.ascontiguousarray(ap.inst_type, dtype=np.int64)
     row_order = np.empty((n_rows, nn), dtype=np.uint8)
     row_cuts = np.empty((n_rows, WARP_PARTS + 1), dtype=np.uint8)
+    if wide:
+        import os
+        _lib.check(lib.ifgfb_row_cuts_wide(
+            n_rows, _lib.iptr(io), _lib.iptr(it), ap.n_types, _lib.u8ptr(gid),
+            _lib.u8ptr(row_order), _lib.u8ptr(row_cuts), lib.ifgfb_wide_warps(),
+            int(os.environ.get("IFGFB_WIDE_CUT", "6")), int(os.environ.get("IFGFB_WIDE_TW", "2")),
+            int(os.environ.get("IFGFB_WIDE_BW", "1")), n_threads), "ifgfb_row_cuts_wide")
+        return row_order, row_cuts
     _lib.check(lib.ifgfb_row_tiles_plan(
         n_rows, _lib.iptr(io), _lib.iptr(it), ap.n_types, _lib.u8ptr(gid),
         _lib.u8ptr(row_order), _lib.u8ptr(row_cuts), None, cut_radius, n_threads),

@@ -261,3 +261,43 @@ def test_tile_free_propagation_is_bitwise_tile_records(monkeypatch, geometry_on_
         outs.append((out.cpu().numpy(), od.cpu().numpy(), plan.device_bytes()))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
     assert outs[1][2] < outs[0][2]        # no tile records on the device
+
+
+@pytest.mark.parametrize("geometry_on_device", ["none", "all"])
+@pytest.mark.parametrize("case", ["c1", "rand"])
+def test_wide_warp_propagation_is_bitwise_five_warp(monkeypatch, geometry_on_device, case):
+    """The wide-warp propagation kernel (IFGFB_K4=wide: 3 owner warps per
+    parent row, up to 4 MMA row tiles of one sigma group sharing each B
+    fragment load) performs the 5-warp kernel's per-node arithmetic in the
+    same order: the far field is bitwise equal (2 kernels at c1, the
+    1-kernel instantiation on the random 2-channel case)."""
+    import torch
+    from paper_2408_02274_b200.engine import FarFieldPlan
+    if case == "c1":
+        inp, z = inputs("c1"), golden("c1")
+        tree, hier, normals, kappas, w_h = (inp["tree"], inp["hier"], inp["disc"].normals,
+                                            inp["kappas"], z["weights"])
+    else:
+        from paper_2408_02274_b200 import octree, surface
+        disc = surface.make_sphere_surface(2, 6)
+        kappas = (3 * np.pi,)
+        tree = octree.build_box_tree(disc.points, max(kappas))
+        hier = octree.build_cone_hierarchy(tree)
+        rng = np.random.default_rng(11)
+        w_h = rng.normal(size=(5, disc.n_points)) + 1j * rng.normal(size=(5, disc.n_points))
+        normals = disc.normals
+    outs = []
+    monkeypatch.setenv("IFGFB_WIDE_OTF", "1")   # wide kernel on on-device-geometry levels too
+    for mode in ("l1free", "wide"):
+        monkeypatch.setenv("IFGFB_K4", mode)
+        plan = FarFieldPlan(tree, hier, normals, 1e-6, kappas=kappas,
+                            geometry_on_device=geometry_on_device)
+        dev = torch.device("cuda")
+        w = torch.from_numpy(np.ascontiguousarray(w_h)).to(dev)
+        out = torch.empty((w.shape[0], len(kappas), w.shape[1]), dtype=torch.complex128,
+                          device=dev)
+        od = torch.empty_like(out)
+        plan.far_apply_device(w, kappas, out, od)
+        outs.append((out.cpu().numpy(), od.cpu().numpy()))
+    assert np.isfinite(outs[1][0]).all() and np.abs(outs[1][0]).max() > 0
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
