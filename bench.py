@@ -416,6 +416,7 @@ def run_b200(args):
     import torch
     import torch.distributed as dist
     from paper_2408_02274_b200.build import build
+    from paper_2408_02274_b200 import engine
     from paper_2408_02274_b200.engine import kernel_times, level_times, set_kernel_timing
     from paper_2408_02274_b200.operator import MullerOperator
 
@@ -582,6 +583,7 @@ def run_b200(args):
                    "geometry_on_device_levels": sorted(getattr(op.plan, "otf_levels", [])),
                    "k4_tiles": ("formed on the device (no tile records)"
                                 if getattr(op.plan, "tile_free", False) else "host records"),
+                   "k4_kernel": engine.k4_mode(),
                    "stream_parts": int(getattr(op.plan, "stream_parts", 1) or 1)},
         "roofline": {"kernel": "propagate (K4: child->parent re-interpolation on "
                                "FP64 DMMA + fused K3)" + (" of rank 0" if world > 1 else ""),

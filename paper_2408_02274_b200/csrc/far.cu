@@ -783,6 +783,9 @@ struct __align__(16) WideStage {
 // BasisA): main block ks = 5q + c -> (T_a(xs) T_b(xt)) T_c(xp) with ab = 4q +
 // tig; tail ks = 15 + s -> (ab, c) = (12 + tig, s) for tig < 3, (12 + s, 4) for
 // tig = 3 (s = 3: the zero row).  tst caches T_a T_b of the current q.
+#ifndef IFGFB_WIDE_PF    // L1 prefetch distance of the B fragments, in k-steps
+#define IFGFB_WIDE_PF IFGFB_ACC_PF
+#endif
 #ifndef IFGFB_WIDE_PIN   // pin the A-value multiplies between the DMMA groups
 #define IFGFB_WIDE_PIN 1
 #endif
@@ -823,9 +826,9 @@ __device__ __forceinline__ void wide_kstep(const double2* F, const double* const
                                            double (&tst)[NT], double (&av)[NT],
                                            double2& b01, double2& b23,
                                            double (&c0)[NT][4], double (&c1)[NT][4], int tig) {
-  if (IFGFB_ACC_PF > 0 && KS + IFGFB_ACC_PF < KSTEPS) {
-    prefetch_l1(F + (KS + IFGFB_ACC_PF) * 64);
-    prefetch_l1(F + (KS + IFGFB_ACC_PF) * 64 + 32);
+  if (IFGFB_WIDE_PF > 0 && KS + IFGFB_WIDE_PF < KSTEPS) {
+    prefetch_l1(F + (KS + IFGFB_WIDE_PF) * 64);
+    prefetch_l1(F + (KS + IFGFB_WIDE_PF) * 64 + 32);
   }
   double2 n01 = b01, n23 = b23;
   if (KS + 1 < KSTEPS) {
@@ -927,9 +930,17 @@ __global__ void __launch_bounds__(32 * WW, IFGFB_WIDE_MINB) accum_wide_kernel(Ac
   // sigma group of every owned slot under every instance of the row: the
   // (<= 8) loads of a lane are independent and complete under the first
   // instance's staging; each warp reads only what it wrote
-  for (int j = 0; j < ni; ++j) {
-    const int t = __shfl_sync(0xffffffffu, my_t, j);
-    if (lane < nset) sgid[j][pos0 + lane] = __ldg(a.gid + (size_t)t * NN + word[lane]);
+  {
+    unsigned char gv[8];
+    const int node = lane < nset ? word[lane] : 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {   // all loads first, then the stores
+      const int t = __shfl_sync(0xffffffffu, my_t, j);
+      gv[j] = (j < ni && lane < nset) ? __ldg(a.gid + (size_t)t * NN + node) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < ni && lane < nset) sgid[j][pos0 + lane] = gv[j];
   }
   auto stage_inst = [&](int j, WideStage& S) {
     const int t = __shfl_sync(0xffffffffu, my_t, j);

@@ -48,7 +48,9 @@ struct RowIn {
 // together, so what a split costs is executed DMMA work: the DP minimises
 // balance_w * W * (largest per-warp tile count) + total_w * (the row's tile
 // count) (weights 1/0: the 5-warp rule; 0/1: fewest tiles), ties by the
-// other term, then by the earliest cuts.
+// other term, then by the earliest cuts.  One (max, total) label per DP
+// state: exact for the two pure objectives, a heuristic (within ~1% of the
+// brute-force optimum, tests/test_plan.py) for mixed weights.
 bool wide_cuts(int ni, const uint8_t (*gs)[NN], int W, int R, int total_w, int balance_w,
                uint8_t* cuts) {
   constexpr int MAXW = 5, MAXR = 8, NO = 2 * MAXR + 1, WIDE_SET = 32;

@@ -28,17 +28,19 @@ K4_MODES = ("auto", "l1", "l1free", "ring", "ringfree", "wide")
 
 
 def k4_mode() -> str:
-    """Propagation kernel (env IFGFB_K4): "auto" (default: the L1-streaming
-    kernel with host-built MMA tile records while the plan fits, else
-    "l1free"), "l1" (tile records), "l1free" (tiles formed on the device
-    from the nodes' sigma groups: no tile records in the plan, ~6% slower),
-    "ring" / "ringfree" (child blocks staged in a shared-memory ring by TMA
-    bulk copies; measured 45% slower, DESIGN 4)."""
+    """Propagation kernel (env IFGFB_K4): "auto" (default) = "wide": the
+    wide-warp kernel (4 owner warps per parent row, up to 4 MMA row tiles of
+    one sigma group per B-fragment load; tile-free plan) on levels with node
+    tables and the 5-warp tile-free kernel on levels with on-device geometry;
+    "l1" (5-warp kernel with host-built tile records), "l1free" (5-warp
+    kernel, tiles formed on the device); "ring" / "ringfree" (child blocks
+    staged in a shared-memory ring by TMA bulk copies; measured 45% slower,
+    DESIGN 4)."""
     import os
     m = os.environ.get("IFGFB_K4", "auto")
     if m not in K4_MODES:
         raise ValueError(f"IFGFB_K4: unknown propagation kernel {m!r}")
-    return m
+    return "wide" if m == "auto" else m
 
 
 class _StageLog:
@@ -192,11 +194,6 @@ class FarFieldPlan:
         budget = 0.55 * torch.cuda.get_device_properties(
             torch.cuda.current_device()).total_memory
         tables = sum(b for b, _ in info.values())
-        if mode == "auto":
-            # tile records make the propagation ~6% faster (the kernel reads
-            # them instead of forming tiles); drop them when the plan would
-            # not fit with every level's node tables
-            self.tile_free = fixed + tables + tile_total > budget
         if not self.tile_free:
             fixed += tile_total
         if policy == "none":

@@ -199,6 +199,59 @@ def test_row_tiles_balanced_cuts_valid_and_no_worse():
             assert np.array_equal(u, v)
 
 
+def _wide_cost(ap, order, cuts, r):
+    """(row's tile count, largest per-warp tile count) of parent row r."""
+    per = []
+    for w in range(len(cuts) - 1):
+        t = 0
+        for i in range(ap.inst_off[r], ap.inst_off[r + 1]):
+            g = ap.gid[ap.inst_type[i]][order[cuts[w]:cuts[w + 1]]]
+            t += int(((np.unique(g, return_counts=True)[1] + 7) // 8).sum())
+        per.append(t)
+    return sum(per), max(per)
+
+
+def test_wide_cuts_minimise_the_stated_objective(monkeypatch):
+    """ifgfb_row_cuts_wide (csrc/tiles.cpp): same signature order as the
+    5-warp builder, valid cuts (W sets of 1..32 nodes, trailing 75s), and
+    per row the DP's cuts against brute force over all cuts within the
+    radius: exact for the pure objectives (total tiles; largest per-warp
+    count), within 3% for the default weighted one (one (max, total) label
+    per DP state is a heuristic there) and never worse than even cuts."""
+    import itertools
+    from paper_2408_02274_b200 import _lib
+    W = _lib.load().ifgfb_wide_warps()
+    inp = inputs("s1")
+    rad = 3
+    monkeypatch.setenv("IFGFB_WIDE_CUT", str(rad))
+    rng = np.random.default_rng(0)
+    for d, (tw, bw) in itertools.product(range(4, inp["tree"].depth + 1),
+                                         [(2, 1), (1, 0), (0, 1)]):
+        monkeypatch.setenv("IFGFB_WIDE_TW", str(tw))
+        monkeypatch.setenv("IFGFB_WIDE_BW", str(bw))
+        ap = octree.accumulation_plan(inp["tree"], inp["hier"], d)
+        order5, _ = octree.row_order_cuts(ap)
+        order, cuts = octree.row_order_cuts(ap, wide=True, n_threads=3)
+        assert np.array_equal(order, order5)
+        c = cuts.astype(int)
+        assert np.all(c[:, 0] == 0) and np.all(c[:, W:] == 75)
+        sizes = np.diff(c[:, :W + 1], axis=1)
+        assert sizes.min() >= 1 and sizes.max() <= 32
+        o2, c2 = octree.row_order_cuts(ap, wide=True, n_threads=1)
+        assert np.array_equal(o2, order) and np.array_equal(c2, cuts)
+        rows = np.nonzero(np.diff(ap.inst_off) > 0)[0]
+        for r in rng.choice(rows, min(6, rows.size), replace=False):
+            o = order[r].astype(int)
+            score = lambda tm: bw * W * tm[1] + tw * tm[0]
+            got = score(_wide_cost(ap, o, c[r, :W + 1], r))
+            cand = [range(75 * k // W - rad, 75 * k // W + rad + 1) for k in range(1, W)]
+            best = min(score(_wide_cost(ap, o, (0, *mid, 75), r))
+                       for mid in itertools.product(*cand))
+            even = score(_wide_cost(ap, o, [75 * k // W for k in range(W + 1)], r))
+            assert got <= even
+            assert got == best if 0 in (tw, bw) else got <= 1.03 * best, (d, r, tw, bw)
+
+
 def test_row_tiles_rejects_bad_radius():
     inp = inputs("s1")
     ap = octree.accumulation_plan(inp["tree"], inp["hier"], 4)
