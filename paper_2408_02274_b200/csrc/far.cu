@@ -70,60 +70,80 @@ __device__ __forceinline__ void k3_sync() {
   else __syncthreads();
 }
 
+// One axis transform c = M v (values at the Chebyshev nodes -> coefficients,
+// M = (2/n) T_i(x_j), row 0 halved) using the node symmetry x_{n-1-j} = -x_j:
+// T_i(x_{n-1-j}) = (-1)^i T_i(x_j), so even rows act on v_j + v_{n-1-j} and
+// odd rows on v_j - v_{n-1-j} (and T_i(0) = 0 for odd i): 14 / 34 FP64
+// operations per complex value for n = 3 / 5 instead of 18 / 50.
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 rfma(double m, double2 v, double2 acc) {
+  return make_double2(fma(m, v.x, acc.x), fma(m, v.y, acc.y));
+}
+__device__ __forceinline__ double2 rmul(double m, double2 v) { return make_double2(m * v.x, m * v.y); }
+
+__device__ __forceinline__ void xform3(double2 (&v)[PS]) {
+  const double2 s = cadd(v[0], v[2]), d = csub(v[0], v[2]), mid = v[1];
+  v[0] = rfma(c_ms[0], s, rmul(c_ms[1], mid));
+  v[1] = rmul(c_ms[PS], d);
+  v[2] = rfma(c_ms[2 * PS], s, rmul(c_ms[2 * PS + 1], mid));
+}
+
+__device__ __forceinline__ void xform5(double2 (&v)[PA]) {
+  const double2 s0 = cadd(v[0], v[4]), s1 = cadd(v[1], v[3]);
+  const double2 d0 = csub(v[0], v[4]), d1 = csub(v[1], v[3]), mid = v[2];
+#pragma unroll
+  for (int i = 0; i < PA; ++i) {
+    if (i & 1) v[i] = rfma(c_ma[i * PA], d0, rmul(c_ma[i * PA + 1], d1));
+    else v[i] = rfma(c_ma[i * PA], s0, rfma(c_ma[i * PA + 1], s1, rmul(c_ma[i * PA + 2], mid)));
+  }
+}
+
 template <bool OWNER, int RS = NCOL, bool NAMED = false>
 __device__ void to_coeffs_smem(double2* V, const unsigned char* inv, int tid, int nthr) {
   for (int task = tid; task < PA * PA * NCOL; task += nthr) {
     const int bc = task / NCOL, m = task % NCOL;
     const int b = bc / PA, c = bc % PA;
     double2 v[PS];
-#pragma unroll
-    for (int a = 0; a < PS; ++a) v[a] = V[node_row<OWNER>(inv, a, b, c) * RS + m];
+    int row[PS];
 #pragma unroll
     for (int a = 0; a < PS; ++a) {
-      double2 s = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int q = 0; q < PS; ++q) {
-        s.x += c_ms[a * PS + q] * v[q].x;
-        s.y += c_ms[a * PS + q] * v[q].y;
-      }
-      V[node_row<OWNER>(inv, a, b, c) * RS + m] = s;
+      row[a] = node_row<OWNER>(inv, a, b, c) * RS + m;
+      v[a] = V[row[a]];
     }
+    xform3(v);
+#pragma unroll
+    for (int a = 0; a < PS; ++a) V[row[a]] = v[a];
   }
   k3_sync<NAMED>();
   for (int task = tid; task < PS * PA * NCOL; task += nthr) {
     const int ac = task / NCOL, m = task % NCOL;
     const int a = ac / PA, c = ac % PA;
     double2 v[PA];
-#pragma unroll
-    for (int b = 0; b < PA; ++b) v[b] = V[node_row<OWNER>(inv, a, b, c) * RS + m];
+    int row[PA];
 #pragma unroll
     for (int b = 0; b < PA; ++b) {
-      double2 s = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int q = 0; q < PA; ++q) {
-        s.x += c_ma[b * PA + q] * v[q].x;
-        s.y += c_ma[b * PA + q] * v[q].y;
-      }
-      V[node_row<OWNER>(inv, a, b, c) * RS + m] = s;
+      row[b] = node_row<OWNER>(inv, a, b, c) * RS + m;
+      v[b] = V[row[b]];
     }
+    xform5(v);
+#pragma unroll
+    for (int b = 0; b < PA; ++b) V[row[b]] = v[b];
   }
   k3_sync<NAMED>();
   for (int task = tid; task < PS * PA * NCOL; task += nthr) {
     const int ab = task / NCOL, m = task % NCOL;
     const int a = ab / PA, b = ab % PA;
     double2 v[PA];
-#pragma unroll
-    for (int c = 0; c < PA; ++c) v[c] = V[node_row<OWNER>(inv, a, b, c) * RS + m];
+    int row[PA];
 #pragma unroll
     for (int c = 0; c < PA; ++c) {
-      double2 s = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int q = 0; q < PA; ++q) {
-        s.x += c_ma[c * PA + q] * v[q].x;
-        s.y += c_ma[c * PA + q] * v[q].y;
-      }
-      V[node_row<OWNER>(inv, a, b, c) * RS + m] = s;
+      row[c] = node_row<OWNER>(inv, a, b, c) * RS + m;
+      v[c] = V[row[c]];
     }
+    xform5(v);
+#pragma unroll
+    for (int c = 0; c < PA; ++c) V[row[c]] = v[c];
   }
   k3_sync<NAMED>();
 }
@@ -323,6 +343,15 @@ __device__ __forceinline__ BasisA make_basis(double xs, double xt, double xp,
   const double vu = (tig == 0) ? tt[2] : (tig == 1) ? tt[3] : tt[4];
   B.u = EXACT ? mul_rn(ts[2], vu) : ts[2] * vu;
   return B;
+}
+
+// dst += c * r (complex) in 4 FMAs: the K4 accumulate of one re-interpolated
+// value times the re-centering ratio.  (The separate multiply-then-add took
+// 6 FP64 instructions; scalar FP64 shares the DMMA pipe and costs ~5 pipe
+// cycles each when interleaved with DMMAs, tools/dmma_mix.cu.)
+__device__ __forceinline__ void cmul_acc(double2& dst, double c_re, double c_im, double2 r) {
+  dst.x = fma(c_re, r.x, fma(-c_im, r.y, dst.x));
+  dst.y = fma(c_re, r.y, fma(c_im, r.x, dst.y));
 }
 
 // acc[nt] (+)= sum_i basis_i * C[i][8nt + grp]: 19 k-steps x 4 column tiles
@@ -721,10 +750,7 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
           const int m = 4 * nt + tig;
-          const double2 v = cmul(make_double2(c0[nt], c1[nt]),
-                                 (NK > 1 && (tig & 1)) ? r1 : r0);
-          dst[m].x += v.x;
-          dst[m].y += v.y;
+          cmul_acc(dst[m], c0[nt], c1[nt], (NK > 1 && (tig & 1)) ? r1 : r0);
         }
       }
       __syncwarp();
@@ -888,10 +914,7 @@ __device__ __forceinline__ void wide_pass(const double* __restrict__ C, const do
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
         const int m = 4 * nt + tig;
-        const double2 v = cmul(make_double2(c0[i][nt], c1[i][nt]),
-                               (NK > 1 && (tig & 1)) ? r1 : r0);
-        dst[m].x += v.x;
-        dst[m].y += v.y;
+        cmul_acc(dst[m], c0[i][nt], c1[i][nt], (NK > 1 && (tig & 1)) ? r1 : r0);
       }
     }
   }
@@ -1307,10 +1330,7 @@ __global__ void __launch_bounds__(RING_THREADS, IFGFB_RING_MINB) accum_ring_kern
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt) {
               const int m = 4 * nt + tig;
-              const double2 v = cmul(make_double2(c0[nt], c1[nt]),
-                                     (NK > 1 && (tig & 1)) ? r1 : r0);
-              dst[m].x += v.x;
-              dst[m].y += v.y;
+              cmul_acc(dst[m], c0[nt], c1[nt], (NK > 1 && (tig & 1)) ? r1 : r0);
             }
           }
           __syncwarp();
