@@ -788,13 +788,17 @@ __global__ void __launch_bounds__(160, IFGFB_ACC_MINB) accum_kernel(AccArgs a) {
 #define IFGFB_WIDE_WARPS 4
 #endif
 #ifndef IFGFB_WIDE_MINB
-#define IFGFB_WIDE_MINB 4
+#define IFGFB_WIDE_MINB 5
 #endif
 #ifndef IFGFB_WIDE_MAXNT   // row tiles of one sigma group run together (1..4)
-#define IFGFB_WIDE_MAXNT 4
+#define IFGFB_WIDE_MAXNT 2
 #endif
 constexpr int WW = IFGFB_WIDE_WARPS;
 constexpr int WIDE_MAXNT = IFGFB_WIDE_MAXNT;
+#ifndef IFGFB_WIDE_RS   // accumulator row stride in complex values: 17 spreads the 8 rows of a
+#define IFGFB_WIDE_RS 17   // tile over the banks (16: every row on the same 64 bytes)
+#endif
+constexpr int WIDE_RS = IFGFB_WIDE_RS;
 static_assert(WIDE_MAXNT >= 1 && WIDE_MAXNT <= 4, "1..4 row tiles per pass");
 constexpr int NT_STRIDE = PS + 2 * PA;   // 13 doubles per node
 static_assert((NN + WW - 1) / WW <= 32, "a wide warp owns at most 32 nodes");
@@ -910,7 +914,7 @@ __device__ __forceinline__ void wide_pass(const double* __restrict__ C, const do
     if (8 * i + grp < nrows) {
       const double2 r0 = ratio[slot[i] * NK];
       const double2 r1 = NK > 1 ? ratio[slot[i] * NK + NK - 1] : r0;
-      double2* dst = mine + slot[i] * NCOL;
+      double2* dst = mine + slot[i] * WIDE_RS;
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
         const int m = 4 * nt + tig;
@@ -925,7 +929,7 @@ __device__ __forceinline__ void wide_pass(const double* __restrict__ C, const do
 
 template <int NK, bool WIDE, bool OTF>
 __global__ void __launch_bounds__(32 * WW, IFGFB_WIDE_MINB) accum_wide_kernel(AccArgs a) {
-  __shared__ double2 acc[NN * NCOL];                        // 19.2 KB
+  __shared__ double2 acc[NN * WIDE_RS];                     // 20.4 KB (padded rows)
   __shared__ WideStage stage[2];                            // 9.2 KB
   __shared__ double nodeT[NN * NT_STRIDE];                  // 7.8 KB
   __shared__ unsigned char ord[NN], inv[NN];
@@ -940,10 +944,10 @@ __global__ void __launch_bounds__(32 * WW, IFGFB_WIDE_MINB) accum_wide_kernel(Ac
   const int pos0 = a.row_cuts[(size_t)p * (WARP_PARTS + 1) + warp];
   const int nset = a.row_cuts[(size_t)p * (WARP_PARTS + 1) + warp + 1] - pos0;
   IFGFB_DCHECK(nset >= 1 && nset <= 32 && pos0 + nset <= NN);
-  double2* mine = acc + pos0 * NCOL;
+  double2* mine = acc + pos0 * WIDE_RS;
   const unsigned char* word = ord + pos0;
   if (lane < nset) ord[pos0 + lane] = a.row_order[(size_t)p * NN + pos0 + lane];
-  for (int i = lane; i < nset * NCOL; i += 32) mine[i] = make_double2(0.0, 0.0);
+  for (int i = lane; i < nset * WIDE_RS; i += 32) mine[i] = make_double2(0.0, 0.0);
   // the row's instance scalars, lane j <-> instance i0 + j (<= 8 per row)
   const int i0 = a.inst_off[p], ni = a.inst_off[p + 1] - i0;
   int my_t = 0, my_co = 0;
@@ -1051,11 +1055,11 @@ __global__ void __launch_bounds__(32 * WW, IFGFB_WIDE_MINB) accum_wide_kernel(Ac
   if (threadIdx.x < NN) inv[ord[threadIdx.x]] = (unsigned char)threadIdx.x;
   __syncthreads();
 #ifndef IFGFB_DIAG_NOK3      // diagnostic builds only (tools/ab_wide.sh): timing without a phase
-  to_coeffs_smem<true>(acc, inv, threadIdx.x, 32 * WW);
+  to_coeffs_smem<true, WIDE_RS>(acc, inv, threadIdx.x, 32 * WW);
 #endif
 #ifndef IFGFB_DIAG_NOSTORE
-  if (WW == 4) store_segment128<true>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, inv, threadIdx.x);
-  else store_segment<true>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, inv, threadIdx.x, 32 * WW);
+  if (WW == 4) store_segment128<true, WIDE_RS>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, inv, threadIdx.x);
+  else store_segment<true, WIDE_RS>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, inv, threadIdx.x, 32 * WW);
 #endif
 }
 
