@@ -29,13 +29,11 @@ K4_MODES = ("auto", "l1", "l1free", "ring", "ringfree", "wide")
 
 def k4_mode() -> str:
     """Propagation kernel (env IFGFB_K4): "auto" (default) = "wide": the
-    wide-warp kernel (4 owner warps per parent row, up to 4 MMA row tiles of
-    one sigma group per B-fragment load; tile-free plan) on levels with node
-    tables and the 5-warp tile-free kernel on levels with on-device geometry;
-    "l1" (5-warp kernel with host-built tile records), "l1free" (5-warp
-    kernel, tiles formed on the device); "ring" / "ringfree" (child blocks
-    staged in a shared-memory ring by TMA bulk copies; measured 45% slower,
-    DESIGN 4)."""
+    wide-warp kernel (4 owner warps per parent row, up to 2 MMA row tiles of
+    one sigma group per B-fragment load; tile-free plan); "l1" (5-warp
+    kernel with host-built tile records), "l1free" (5-warp kernel, tiles
+    formed on the device); "ring" / "ringfree" (child blocks staged in a
+    shared-memory ring by TMA bulk copies; measured 45% slower, DESIGN 4)."""
     import os
     m = os.environ.get("IFGFB_K4", "auto")
     if m not in K4_MODES:
@@ -224,11 +222,11 @@ class FarFieldPlan:
         # picks them (ifgf.py:743-746), including any inexact hit.
         tile_free = self.tile_free
         if tile_free:
-            # wide-warp kernel on levels with node tables; on-device geometry
-            # (FP64 work per node and instance) is hidden better by the 5-warp
-            # kernel's 30 resident warps (IFGFB_WIDE_OTF=1 forces wide there too)
+            # the wide-warp kernel on every level (on-device-geometry levels
+            # included: 24.3 vs 26.5 ms with every level on-device at (4,10));
+            # IFGFB_WIDE_OTF=0 keeps the 5-warp kernel on those levels
             import os
-            wide = k4_mode() == "wide" and (not otf or os.environ.get("IFGFB_WIDE_OTF") == "1")
+            wide = k4_mode() == "wide" and (not otf or os.environ.get("IFGFB_WIDE_OTF", "1") != "0")
             row_order, row_cuts = row_order_cuts(ap, wide=wide)
             tile_off = tiles = None
         else:

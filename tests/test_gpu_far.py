@@ -287,7 +287,6 @@ def test_wide_warp_propagation_is_bitwise_five_warp(monkeypatch, geometry_on_dev
         w_h = rng.normal(size=(5, disc.n_points)) + 1j * rng.normal(size=(5, disc.n_points))
         normals = disc.normals
     outs = []
-    monkeypatch.setenv("IFGFB_WIDE_OTF", "1")   # wide kernel on on-device-geometry levels too
     for mode in ("l1free", "wide"):
         monkeypatch.setenv("IFGFB_K4", mode)
         plan = FarFieldPlan(tree, hier, normals, 1e-6, kappas=kappas,
