@@ -293,8 +293,15 @@ __global__ void __launch_bounds__(leaf_threads<NK>(), IFGFB_LEAF_MINB) leaf_kern
   }
   __syncthreads();
   to_coeffs_smem<false, LEAF_RS>(V, nullptr, tid, blockDim.x);
-  store_segment<false, LEAF_RS>(a.coef + (size_t)row * SEG_DOUBLES, V, nullptr, tid,
-                                blockDim.x);
+  // unrolled store by the first 128 threads (element 128 ks + tid): 6 instead
+  // of 37 instructions per element of the generic index arithmetic
+  constexpr int LEAF_THREADS = ((NN * NK + 31) / 32) * 32;
+  if (LEAF_THREADS >= 128) {
+    if (tid < 128) store_segment128<false, LEAF_RS>(a.coef + (size_t)row * SEG_DOUBLES, V, nullptr, tid);
+  } else {
+    store_segment<false, LEAF_RS>(a.coef + (size_t)row * SEG_DOUBLES, V, nullptr, tid,
+                                  blockDim.x);
+  }
 }
 
 // ------------------------------------------------------- DMMA helpers ----

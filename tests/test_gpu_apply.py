@@ -78,6 +78,29 @@ def test_apply_vs_oracle_on_host():
     assert rel(op.apply(y), ref) < 1e-10
 
 
+@pytest.mark.parametrize("n_c", [13, 16])
+def test_apply_high_patch_order_vs_oracle(n_c):
+    """n_c = 13..16: the per-patch kernels (K1 packing, K7 assembly) need more
+    than the default 48 KB of dynamic shared memory (20 n_c^2 and 16 n_c^2
+    complex values); sphere(1, n_c) against the oracle on this host."""
+    from paper_2408_02274_b200 import nearfield, octree, surface
+    from paper_2408_02274_b200.operator import MaterialPair
+    disc = surface.make_sphere_surface(1, n_c)
+    mats = MaterialPair(1.0, 1.0, 2.25, 1.0, 2 * np.pi)
+    tree = octree.build_box_tree(disc.points, max(abs(mats.kappa_e), abs(mats.kappa_i)))
+    hier = octree.build_cone_hierarchy(tree)
+    smap = nearfield.classify_targets(disc)
+    mom = nearfield.compute_moments(disc, smap, nearfield.SingularQuadratureConfig(),
+                                    mats.kappas)
+    cp = nearfield.correction_pairs(disc, tree, smap)
+    op = MullerOperator(disc, mats, smap, mom, (cp.ell_idx, cp.src_idx), tree=tree,
+                        hierarchy=hier)
+    y = np.random.default_rng(n_c).normal(size=(op.n_unknowns, 2)) @ [1, 1j]
+    ref = oracle.muller_apply(oracle.OperatorData(
+        disc, mats, smap, mom, cp.ell_idx, cp.src_idx, tree, hier), y)
+    assert rel(op.apply(y), ref) < 1e-10
+
+
 def test_device_and_host_paths_bitwise_equal_and_deterministic():
     op = device_op("c1")
     y = golden("c1")["y"]

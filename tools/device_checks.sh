@@ -14,7 +14,7 @@ cmd = [b._nvcc(), *b.NVCC_FLAGS, "-DIFGFB_DEVICE_CHECKS", "-o", "variants/checke
        *[str(b.CSRC / s) for s in b.SOURCES]]
 subprocess.run(cmd, check=True, cwd=b.CSRC.parent.parent)
 PY
-for k4 in l1free l1 ringfree ring; do
+for k4 in wide l1free l1 ringfree ring; do
   echo "== IFGFB_K4=$k4 (checked build)"
   IFGFB_LIB=$PWD/variants/checked.so IFGFB_K4=$k4 timeout 1200 python -m pytest \
     tests/test_gpu_far.py tests/test_gpu_apply.py tests/test_gpu_partition.py -q -x \
