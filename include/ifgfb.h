@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define IFGFB_ABI_VERSION 7
+#define IFGFB_ABI_VERSION 8
 
 enum {
   IFGFB_OK = 0,

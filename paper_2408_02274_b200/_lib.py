@@ -204,7 +204,7 @@ EXPORTS = {
                          C.c_void_p], C.c_int),
 }
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 _lib = None
 
 

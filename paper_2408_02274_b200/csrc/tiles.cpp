@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -52,7 +53,7 @@ struct RowIn {
 // state: exact for the two pure objectives, a heuristic (within ~1% of the
 // brute-force optimum, tests/test_plan.py) for mixed weights.
 bool wide_cuts(int ni, const uint8_t (*gs)[NN], int W, int R, int total_w, int balance_w,
-               uint8_t* cuts) {
+               uint8_t* cuts, int pass_w = 0) {
   constexpr int MAXW = 5, MAXR = 8, NO = 2 * MAXR + 1, WIDE_SET = 32;
   if (W < 1 || W > MAXW || R < 0 || R > MAXR) return false;
   auto sweep = [&](int a, int bmax, int* tiles_upto) {
@@ -60,9 +61,14 @@ bool wide_cuts(int ni, const uint8_t (*gs)[NN], int W, int R, int total_w, int b
     std::memset(cnt, 0, sizeof(cnt));
     int tot = 0;
     tiles_upto[0] = 0;
+    // cost in quarter tiles: 4 per row tile + pass_w per pass (a pass = up to
+    // 2 row tiles of one sigma group: its B-load latency and tile formation)
     for (int b = a; b < bmax; ++b) {
-      for (int i = 0; i < ni; ++i)
-        if (cnt[i][gs[i][b]]++ % 8 == 0) ++tot;
+      for (int i = 0; i < ni; ++i) {
+        const int c = cnt[i][gs[i][b]]++;
+        if (c % 8 == 0) tot += 4;
+        if (c % 16 == 0) tot += pass_w;
+      }
       tiles_upto[b + 1 - a] = tot;
     }
   };
@@ -115,7 +121,7 @@ bool wide_cuts(int ni, const uint8_t (*gs)[NN], int W, int R, int total_w, int b
 }
 
 bool row_partition(const RowIn& in, int64_t r, int R, uint8_t* order, uint8_t* cuts,
-                   int wide_w = 0, int total_w = 0, int balance_w = 1) {
+                   int wide_w = 0, int total_w = 0, int balance_w = 1, int pass_w = 0) {
   const int64_t i0 = in.inst_off[r], ni = in.inst_off[r + 1] - i0;
   if (ni < 0 || ni > MAX_INST) return false;
   int64_t key[NN];
@@ -137,7 +143,7 @@ bool row_partition(const RowIn& in, int64_t r, int R, uint8_t* order, uint8_t* c
     const uint8_t* g = in.group_id + in.inst_type[i0 + i] * NN;
     for (int n = 0; n < NN; ++n) gs[i][n] = g[idx[n]];
   }
-  if (wide_w > 0) return wide_cuts((int)ni, gs, wide_w, R, total_w, balance_w, cuts);
+  if (wide_w > 0) return wide_cuts((int)ni, gs, wide_w, R, total_w, balance_w, cuts, pass_w);
   // tiles of [a, b) summed over instances, for b swept upward from a
   auto sweep = [&](int a, int bmax, int* tiles_upto /* index b - a */) {
     uint8_t cnt[MAX_INST][MAX_GROUPS];
@@ -325,10 +331,14 @@ int ifgfb_row_cuts_wide(int64_t n_rows, const int64_t* inst_off, const int64_t* 
     }
   RowIn in{inst_off, inst_type, group_id};
   std::atomic<bool> bad{false};
+  // cost of a pass relative to a row tile, in quarter tiles (experiment knob;
+  // 0 = tiles only, the documented objective)
+  const char* pw_env = std::getenv("IFGFB_WIDE_PW");
+  const int pass_w = pw_env ? std::max(0, std::min(16, std::atoi(pw_env))) : 0;
   parallel_rows(n_rows, n_threads, [&](int64_t r0, int64_t r1) {
     for (int64_t r = r0; r < r1; ++r)
       if (!row_partition(in, r, cut_radius, row_order + r * NN, row_cuts + r * (WP + 1),
-                         n_warps, total_weight, balance_weight))
+                         n_warps, total_weight, balance_weight, pass_w))
         bad = true;
   });
   if (bad) {

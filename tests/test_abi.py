@@ -38,7 +38,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_abi_version(lib):
-    assert lib.ifgfb_abi_version() == _lib.ABI_VERSION == 7
+    assert lib.ifgfb_abi_version() == _lib.ABI_VERSION == 8
 
 
 STRUCTS = {
