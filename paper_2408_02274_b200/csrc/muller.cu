@@ -193,7 +193,7 @@ __device__ __forceinline__ void warp_reduce_owned(const double2 (&s)[8][2],
 // combination with the far field (operators.py:341-350), including
 // D_far = (S_disp - S) / h.  Three phases keep 28 complex accumulators live.
 #ifndef IFGFB_NEAR_MINB
-#define IFGFB_NEAR_MINB 1
+#define IFGFB_NEAR_MINB 3   // 168 registers, 3 CTAs/SM: 1.20 -> 1.08 ms at (8,10), 10.1 -> 8.8 ms on the (48,6,3) slab
 #endif
 __global__ void __launch_bounds__(128, IFGFB_NEAR_MINB) near_kernel(NearArgs a) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
