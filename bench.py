@@ -374,7 +374,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v,
             "unit": "unknowns*matvec/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": statistics.mean(walls) * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "c128/f64", "data": "synthetic (seeded N(0,1) densities)",
             "extrapolated": True,
             "config": {"workload": name, "unknowns": target["unknowns"],
