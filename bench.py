@@ -581,6 +581,11 @@ def run_b200(args):
                    "plan_build_s": round(t_plan, 1),
                    "device_plan_gib": round(op.plan.device_bytes() / 2**30, 2),
                    "geometry_on_device_levels": sorted(getattr(op.plan, "otf_levels", [])),
+                   "geometry_on_device_mode": (
+                       "in the propagation kernel (IFGFB_OTF_PRE_MB=0)"
+                       if os.environ.get("IFGFB_OTF_PRE_MB", "").strip() == "0"
+                       else "node tables per chunk of parent rows (otf_tables_kernel) "
+                            "ahead of each propagation launch; timed inside propagate"),
                    "k4_tiles": ("formed on the device (no tile records)"
                                 if getattr(op.plan, "tile_free", False) else "host records"),
                    "k4_kernel": engine.k4_mode(),

@@ -217,6 +217,7 @@ struct Level {
   double* node_r = nullptr;    // n_types*NN*2 (r_parent, r_child)
   double* ratio = nullptr;     // workspace n_types*NN*2 complex
   int* inst_off = nullptr;     // parent rows + 1
+  std::vector<int> h_inst_off; // host copy (on-device-geometry levels: row chunks of the node-table pre-pass)
   int* inst_type = nullptr;
   int* inst_crow_off = nullptr;
   int* crow = nullptr;
@@ -249,6 +250,11 @@ struct Plan {
   double* wt = nullptr;            // N * 8 complex (tree order, channels)
   double* coef[2] = {nullptr, nullptr};
   size_t coef_cap = 0;             // segments
+  // node tables of on-device-geometry levels, tabulated per (instance, node)
+  // for one chunk of parent rows ahead of its propagation launch (far.cu)
+  double* otf_geom = nullptr;      // otf_cap * NN * 3
+  double* otf_ratio = nullptr;     // otf_cap * NN * 2 complex
+  int64_t otf_cap = 0;             // instances; -1: allocation failed / disabled
   double* partial = nullptr;       // max pairs * 2 * NCOL complex
   // emission overlap: a level's emission (K5 + reduce) runs on `aux`
   // concurrently with the next propagation step on the apply stream

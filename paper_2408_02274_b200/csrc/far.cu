@@ -530,6 +530,9 @@ struct AccArgs {
   OtfGeom o;             // OTF instantiation only
   const unsigned char* gid;   // tile-free ring kernel: sigma group per (type, node)
   int child_lo, child_hi;     // child rows present in coef_child (checks)
+  // PRE instantiation of the wide kernel: node_geom / ratio hold one row per
+  // (instance, node), instance index relative to inst_base (otf_tables_kernel)
+  int inst_base = 0;
 };
 
 // cp.async (LDGSTS) helpers: global -> shared without a register round trip
@@ -934,8 +937,9 @@ __device__ __forceinline__ void wide_pass(const double* __restrict__ C, const do
 #endif
 }
 
-template <int NK, bool WIDE, bool OTF>
+template <int NK, bool WIDE, bool OTF, bool PRE = false>
 __global__ void __launch_bounds__(32 * WW, IFGFB_WIDE_MINB) accum_wide_kernel(AccArgs a) {
+  static_assert(!(OTF && PRE), "PRE reads tabulated node geometry");
   __shared__ double2 acc[NN * WIDE_RS];                     // 20.4 KB (padded rows)
   __shared__ WideStage stage[2];                            // 9.2 KB
   __shared__ double nodeT[NN * NT_STRIDE];                  // 7.8 KB
@@ -980,7 +984,7 @@ __global__ void __launch_bounds__(32 * WW, IFGFB_WIDE_MINB) accum_wide_kernel(Ac
     const int t = __shfl_sync(0xffffffffu, my_t, j);
     const int cs = __shfl_sync(0xffffffffu, my_co, j);
     const int ce = __shfl_sync(0xffffffffu, my_co, j + 1);
-    const size_t tb = (size_t)t * NN;
+    const size_t tb = PRE ? (size_t)(i0 + j - a.inst_base) * NN : (size_t)t * NN;
     if (!OTF && lane < nset) {   // one lane per owned node
       const size_t nd = tb + word[lane];
 #pragma unroll
@@ -1068,6 +1072,30 @@ __global__ void __launch_bounds__(32 * WW, IFGFB_WIDE_MINB) accum_wide_kernel(Ac
   if (WW == 4) store_segment128<true, WIDE_RS>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, inv, threadIdx.x);
   else store_segment<true, WIDE_RS>(a.coef_parent + (size_t)p * SEG_DOUBLES, acc, inv, threadIdx.x, 32 * WW);
 #endif
+}
+
+// Node tables of an on-device-geometry level for the parent rows
+// [row0, row_end): geometry and re-centering ratio of every (instance, node),
+// exactly what the OTF instantiations compute per owner lane (otf_node), but
+// with every lane busy and off the propagation kernel's FP64/DMMA critical
+// path.  The propagation then runs its table instantiation (PRE) on the
+// chunk.  One CTA per parent row (<= 8 instances x 75 nodes).
+template <int NK>
+__global__ void __launch_bounds__(128) otf_tables_kernel(AccArgs a, double* __restrict__ geom,
+                                                         double2* __restrict__ ratio) {
+  const int p = a.row0 + blockIdx.x;
+  if (p >= a.row_end) return;
+  const int i0 = a.inst_off[p], ni = a.inst_off[p + 1] - i0;
+  const int pseg = a.o.parent_seg_id[p];
+  for (int e = threadIdx.x; e < ni * NN; e += blockDim.x) {
+    const int j = e / NN, node = e - j * NN;
+    const int t = a.inst_type[i0 + j];
+    const int oct = a.o.type_octant[t];
+    const int g = a.gid[(size_t)t * NN + node];
+    const int cr = a.crow[a.inst_crow_off[i0 + j] + g];
+    const size_t o = (size_t)(i0 + j - a.inst_base) * NN + node;
+    otf_node<NK>(a.o, pseg, oct, node, a.o.child_seg_id[cr], geom + o * 3, ratio + o * NK);
+  }
 }
 
 // ------------------------------------------------- K4, ring-staged ----
@@ -1573,6 +1601,38 @@ static int ensure_aux(Plan& p) {
   return IFGFB_OK;
 }
 
+// Scratch for the node-table pre-pass of on-device-geometry levels
+// (otf_tables_kernel): IFGFB_OTF_PRE_MB MiB (default 4096, 0 = off: geometry
+// inside the propagation kernel), at most a quarter of the free device
+// memory.  Returns false when the pre-pass is off or the scratch does not fit.
+static bool ensure_otf_tables(Plan& p) {
+  if (p.otf_cap != 0) return p.otf_cap > 0;
+  p.otf_cap = -1;
+  const char* v = std::getenv("IFGFB_OTF_PRE_MB");
+  size_t want = (size_t)(v ? std::max(0L, std::atol(v)) : 4096L) << 20;
+  size_t free_b = 0, total_b = 0;
+  if (want == 0 || cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+  want = std::min(want, free_b / 4);
+  const size_t per_inst = (size_t)NN * (3 + 4) * sizeof(double);
+  // at least a few thousand rows per chunk, or the launches stop filling the GPU
+  int64_t cap = (int64_t)(want / per_inst);
+  if (cap < 65536) return false;
+  int64_t most = 0;   // no more than the largest on-device-geometry level needs
+  for (const Level& L : p.levels)
+    if (L.otf) most = std::max(most, L.n_instances);
+  cap = std::min(cap, std::max<int64_t>(most, 31));
+  // tests: capacity in instances (>= 31, the most one row can hold), to
+  // force several chunks on small plans
+  if (const char* ci = std::getenv("IFGFB_OTF_PRE_INST")) cap = std::max(31L, std::atol(ci));
+  if (dev_alloc(p, &p.otf_geom, (size_t)cap * NN * 3) != IFGFB_OK ||
+      dev_alloc(p, &p.otf_ratio, (size_t)cap * NN * 4) != IFGFB_OK) {
+    cudaGetLastError();
+    return false;
+  }
+  p.otf_cap = cap;
+  return true;
+}
+
 template <int NK>
 static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
                        double* out, double* out_disp, cudaStream_t st, int pm_stride) {
@@ -1684,7 +1744,30 @@ static int far_apply_t(Plan& p, const double* w, int nch, const double* kap,
               // the level's rows were cut for the wide-warp kernel
               // (ifgfb_row_cuts_wide; the plan builder decides per level)
               const dim3 wblk(32 * WW);
-              if (L.otf) {
+              if (L.otf && ensure_otf_tables(p)) {
+                // node tables of a chunk of rows, then its propagation from them
+                const std::vector<int>& io = L.h_inst_off;
+                AccArgs ab = aa;
+                ab.node_geom = p.otf_geom;
+                ab.ratio = reinterpret_cast<const double2*>(p.otf_ratio);
+                for (int r0 = U.seg_lo(); r0 < U.seg_hi();) {
+                  const int64_t lim = (int64_t)io[r0] + p.otf_cap;
+                  int r1 = (int)(std::upper_bound(io.begin() + r0 + 1, io.begin() + U.seg_hi() + 1,
+                                                  lim, [](int64_t v, int x) { return v < x; })
+                                 - io.begin()) - 1;
+                  r1 = std::min(std::max(r1, r0 + 1), U.seg_hi());
+                  ab.row0 = r0;
+                  ab.row_end = r1;
+                  ab.inst_base = io[r0];
+                  otf_tables_kernel<NK><<<r1 - r0, 128, 0, st>>>(
+                      ab, p.otf_geom, reinterpret_cast<double2*>(p.otf_ratio));
+                  if (wide) accum_wide_kernel<NK, true, false, true><<<r1 - r0, wblk, 0, st>>>(ab);
+                  else accum_wide_kernel<NK, false, false, true><<<r1 - r0, wblk, 0, st>>>(ab);
+                  launches += 2;
+                  r0 = r1;
+                }
+                --launches;   // the common ++launches below
+              } else if (L.otf) {
                 if (wide) accum_wide_kernel<NK, true, true><<<nrows, wblk, 0, st>>>(aa);
                 else accum_wide_kernel<NK, false, true><<<nrows, wblk, 0, st>>>(aa);
               } else {

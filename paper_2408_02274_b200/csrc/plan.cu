@@ -280,6 +280,7 @@ int ifgfb_plan_add_accum(ifgfb_plan* h, const ifgfb_accum_desc* a) {
   }
   if (!to_i32(a->inst_off, a->n_parent_rows + 1, tmp, "inst_off")) return IFGFB_ERR_ARG;
   RC(dev_upload(p, &L.inst_off, tmp.data(), tmp.size()));
+  if (L.otf) L.h_inst_off = tmp;
   L.n_instances = a->n_instances;
   for (int64_t i = 0; i < a->n_instances; ++i)
     CHECK_ARG(a->inst_type[i] >= 0 && a->inst_type[i] < nt, "inst_type out of range");

@@ -300,3 +300,47 @@ def test_wide_warp_propagation_is_bitwise_five_warp(monkeypatch, geometry_on_dev
         outs.append((out.cpu().numpy(), od.cpu().numpy()))
     assert np.isfinite(outs[1][0]).all() and np.abs(outs[1][0]).max() > 0
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("case", ["c1", "rand"])
+def test_node_table_prepass_equals_in_kernel_geometry(monkeypatch, case):
+    """On-device-geometry levels: the node tables tabulated per (instance,
+    node) by otf_tables_kernel ahead of each propagation launch (default; in
+    chunks of parent rows that fit the scratch) give the far field of the
+    geometry computed inside the propagation kernel (IFGFB_OTF_PRE_MB=0);
+    the chunking itself is bitwise neutral."""
+    import torch
+    from paper_2408_02274_b200.engine import FarFieldPlan
+    if case == "c1":
+        inp, z = inputs("c1"), golden("c1")
+        tree, hier, normals, kappas, w_h = (inp["tree"], inp["hier"], inp["disc"].normals,
+                                            inp["kappas"], z["weights"])
+    else:
+        from paper_2408_02274_b200 import octree, surface
+        disc = surface.make_sphere_surface(2, 6)
+        kappas = (3 * np.pi,)
+        tree = octree.build_box_tree(disc.points, max(kappas))
+        hier = octree.build_cone_hierarchy(tree)
+        rng = np.random.default_rng(12)
+        w_h = rng.normal(size=(5, disc.n_points)) + 1j * rng.normal(size=(5, disc.n_points))
+        normals = disc.normals
+    monkeypatch.setenv("IFGFB_K4", "wide")
+    outs = []
+    for env in ({"IFGFB_OTF_PRE_MB": "0"}, {}, {"IFGFB_OTF_PRE_INST": "40"}):
+        for k in ("IFGFB_OTF_PRE_MB", "IFGFB_OTF_PRE_INST"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        plan = FarFieldPlan(tree, hier, normals, 1e-6, kappas=kappas, geometry_on_device="all")
+        dev = torch.device("cuda")
+        w = torch.from_numpy(np.ascontiguousarray(w_h)).to(dev)
+        out = torch.empty((w.shape[0], len(kappas), w.shape[1]), dtype=torch.complex128,
+                          device=dev)
+        od = torch.empty_like(out)
+        plan.far_apply_device(w, kappas, out, od)
+        plan.far_apply_device(w, kappas, out, od)     # scratch reused across applies
+        outs.append((out.cpu().numpy(), od.cpu().numpy(), plan.device_bytes()))
+    assert np.isfinite(outs[1][0]).all() and np.abs(outs[1][0]).max() > 0
+    assert outs[1][2] > outs[0][2]                    # the scratch is part of the plan
+    assert np.array_equal(outs[1][0], outs[2][0]) and np.array_equal(outs[1][1], outs[2][1])
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
