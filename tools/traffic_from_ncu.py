@@ -4,7 +4,7 @@ propagation kernel's DRAM bytes per launch, read by bench.py's roofline
 object) and a per-kernel share summary.
 
   python tools/traffic_from_ncu.py gpurun_out/launches_r02_cfg5_wide.csv cfg5 \
-      "cfg5 sphere(n_refine=45, n_c=10) k0=32pi eps_r=2.25"
+      "cfg5 sphere(n_refine=45, n_c=10) k0=32pi eps_r=2.25" [launch count given to ncu -c]
 
 The command that produced the CSV is recorded in the JSON's `source`.
 """
@@ -48,18 +48,40 @@ def main():
     for k, (n, ms, b) in sorted(by.items(), key=lambda x: -x[1][1]):
         print(f"  {k:28s} {n:4d} launches {ms:9.2f} ms {100 * ms / tot:5.1f}%  "
               f"DRAM {b / 1e9:8.1f} GB")
-    acc = [L for L in launches.values() if "accum" in L["name"]]
+    # a propagation step (one timed K4 region of bench.py) is one accum launch,
+    # or on on-device-geometry levels a run of (node tables, propagation) pairs
+    # over chunks of parent rows
+    is_prop = lambda L: "accum" in L["name"] or "otf_tables" in L["name"]
+    ids = sorted(launches)
+    acc = [launches[i] for i in ids if is_prop(launches[i])]
+    kind = lambda i: ("tables" if "otf_tables" in launches[i]["name"]
+                      else "accum" if "accum" in launches[i]["name"] else "other")
+    n_steps, in_otf = 0, False
+    for a, b in zip([None] + ids[:-1], ids):
+        ka, kb = (kind(a) if a is not None else "other"), kind(b)
+        if kb == "tables":
+            if not (ka == "accum" and in_otf):
+                n_steps += 1            # first chunk of an on-device-geometry step
+            in_otf = True
+        elif kb == "accum":
+            if ka != "tables":
+                n_steps += 1            # a table level's single launch
+                in_otf = False
+        else:
+            in_otf = False
     bytes_total = sum(L["dram__bytes_read.sum"] + L["dram__bytes_write.sum"] for L in acc)
+    count = sys.argv[4] if len(sys.argv) > 4 else "340"
     out = {
         "workload": workload,
-        "propagate_bytes_per_launch": bytes_total / max(1, len(acc)),
+        "propagate_bytes_per_launch": bytes_total / max(1, n_steps),
         "bytes_per_matvec": bytes_total,
-        "propagate_launches": len(acc),
+        "propagate_launches": n_steps,
+        "propagate_kernel_launches": len(acc),
         "source": ("ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
-                   "gpu__time_duration.sum --clock-control none -c 340 python bench.py "
-                   "--steps 1 --warmup 0 (the process's first 340 launches: the device plan "
+                   f"gpu__time_duration.sum --clock-control none -c {count} python bench.py "
+                   f"--steps 1 --warmup 0 (the process's first {count} launches: the device plan "
                    "builder's kernels, then the first matvec's; per-launch times are "
-                   f"ncu-serialised; {len(acc)} propagation launches covered). "
+                   f"ncu-serialised; {n_steps} propagation steps = {len(acc)} kernel launches covered). "
                    f"CSV: profiles/{Path(path).name}"),
         "kernels": {k: {"launches": n, "ms": round(ms, 3), "dram_gb": round(b / 1e9, 2)}
                     for k, (n, ms, b) in by.items()},
