@@ -172,9 +172,10 @@ def work_counts(tree, hier):
     window's plan: that rank's share)."""
     from paper_2408_02274_b200 import octree
     D = tree.depth
-    prop, pbytes = {}, {}
+    prop, pbytes, ninst = {}, {}, {}
     for d in range(4, D + 1):
         ap = octree.accumulation_plan(tree, hier, d, geometry=False)
+        ninst[d] = int(ap.n_instances)
         prop[d] = W_PROP * ap.n_instances + W_COEF * hier.level(d - 1).n_segments
         # algorithmic HBM bytes of K4: child level read once, parent written once
         pbytes[d] = SEG_BYTES * (hier.level(d).n_segments + hier.level(d - 1).n_segments)
@@ -182,6 +183,7 @@ def work_counts(tree, hier):
     leaf = W_LEAF * 75 * int((cl.seg_off[1:] - cl.seg_off[:-1]) @ lvl.pt_count)
     emit = W_EMIT * sum(hier.level(d).cpt_idx.size for d in range(3, D + 1))
     return {"prop_by_level": prop, "prop": sum(prop.values()), "leaf": leaf,
+            "instances_by_level": ninst,
             "prop_bytes": sum(pbytes.values()),
             "leaf_coef": W_COEF * cl.n_segments, "emit": emit,
             "total": sum(prop.values()) + leaf + W_COEF * cl.n_segments + emit}
@@ -617,6 +619,17 @@ def run_b200(args):
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
     }
+    otf = sorted(getattr(op.plan, "otf_levels", []))
+    if otf and os.environ.get("IFGFB_OTF_PRE_MB", "").strip() != "0":
+        # node tables of the on-device-geometry levels: written by the pre-pass
+        # and read back by the propagation, 75 nodes x 56 B per instance
+        extra = 2 * 75 * 56 * sum(counts["instances_by_level"].get(d, 0) for d in otf)
+        line["roofline"]["traffic_prepass_tables"] = extra / max(1, prop_n // args.steps)
+        line["roofline"]["traffic_note"] = (
+            "traffic: ncu launch list captured before the node-table pre-pass "
+            "(profiles/launches_r02_cfg5_wide.csv); traffic_prepass_tables = the "
+            f"pre-pass's table bytes on levels {otf} per K4 launch, computed from the "
+            "plan (written once, read once), to be added to it")
     if world > 1 or emulate:
         line["ranks"] = rank_info if isinstance(rank_info, list) else [rank_info]
     if world == 1 and not emulate and not args.no_cpu_baseline:
