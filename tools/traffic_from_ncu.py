@@ -51,11 +51,15 @@ def main():
     # a propagation step (one timed K4 region of bench.py) is one accum launch,
     # or on on-device-geometry levels a run of (node tables, propagation) pairs
     # over chunks of parent rows
-    is_prop = lambda L: "accum" in L["name"] or "otf_tables" in L["name"]
     ids = sorted(launches)
-    acc = [launches[i] for i in ids if is_prop(launches[i])]
-    kind = lambda i: ("tables" if "otf_tables" in launches[i]["name"]
-                      else "accum" if "accum" in launches[i]["name"] else "other")
+    # (accum_types_kernel is the plan builder's, not a propagation launch)
+    def kind(i):
+        nm = launches[i]["name"]
+        if "otf_tables" in nm:
+            return "tables"
+        return "accum" if ("accum" in nm and "accum_types" not in nm) else "other"
+
+    acc = [launches[i] for i in ids if kind(i) != "other"]
     n_steps, in_otf = 0, False
     for a, b in zip([None] + ids[:-1], ids):
         ka, kb = (kind(a) if a is not None else "other"), kind(b)
