@@ -54,6 +54,25 @@ def test_apply_vs_reference_golden(name):
     assert rel(out, z["apply_y"]) < (1e-10 if name != "se1" else 3e-10)
 
 
+@pytest.mark.parametrize("name", ["c1", "c2n4"])
+def test_apply_with_on_device_geometry_vs_reference_golden(monkeypatch, name):
+    """Every propagation level on on-device geometry (what cfg 5 does on
+    levels 4-5): node tables from otf_tables_kernel per chunk of parent rows
+    (libdevice acos / atan2 / sincos instead of the host's numpy values),
+    still within the north-star tolerance of the reference's output."""
+    _have(name)
+    if not plan_matches_golden(name):
+        pytest.skip("host numpy produced a different plan than the golden host")
+    monkeypatch.setenv("IFGFB_GEOM_ON_DEVICE", "all")
+    monkeypatch.delenv("IFGFB_OTF_PRE_MB", raising=False)
+    z, inp = golden(name), inputs(name)
+    op = MullerOperator(inp["disc"], inp["mats"], inp["smap"], inp["moments"],
+                        (inp["corr"].ell_idx, inp["corr"].src_idx), tree=inp["tree"],
+                        hierarchy=inp["hier"])
+    assert sorted(op.plan.otf_levels) == list(range(4, inp["tree"].depth + 1))
+    assert rel(op.apply(z["y"]), z["apply_y"]) < 1e-10
+
+
 @pytest.mark.parametrize("name", ["s1", "c1", "c2n4", "c2n8"])
 def test_potentials_vs_reference_golden(name):
     _have(name)
